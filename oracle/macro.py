@@ -1,0 +1,227 @@
+"""ORACLE (test infrastructure): macro scale — Jacobian of F, macro field Ā,
+interpolation onto the Bernstein space Q_q.
+
+Ā_ij (Eq. 37; App. A.2 Eqs. 89-97) is
+computed by three independent routes:
+  A_closed  Ā_ij[a,b] = D (λ ǧ_i[a] ǧ_j[b] + μ ǧ_j[a] ǧ_i[b] + μ (ǧ_i·ǧ_j) δ_ab),
+            ǧ_i = row i of J⁻¹ (contravariant vectors, Eqs. 80-81), D = det J
+  A_voigt   Ā_ij = Ĝ_i Č Ĝ_jᵀ |det J| with Ĝ_i from Eq. 91 and Č from Eq. 84a / 93
+  A_tensor  Ā_ij[a,b] = D Σ_kl J⁻¹[i,k] C[a,k,b,l] J⁻¹[j,l] (isotropic C)
+Entry (a,b) multiplies u_a (trial, derivative ξ_i) against v_b (test,
+derivative ξ_j): K_AB[a,b] = Σ_ij ∫ ∂_iR_A ∂_jR_B Ā_ij[a,b] (Eq. 49).
+
+Interpolation (reading R1): the paper L2-projects (Eqs. 20-24, 42);
+BASELINE.json mandates interpolation.  The oracle interpolates at the (q+1)^d
+tensor Gauss–Legendre nodes by solving the full tensor Vandermonde system
+V c = s (V[m, C] = N_C(x_m)); this equals the L2 projection with a
+(q+1)-point Gauss right-hand side (pinned in tests).
+
+J is ∂F/∂ξ in the element-local frame ξ ∈ [0,1]^d (Eq. 7):
+∂F/∂u times the knot-span lengths (reading R4).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .bspline import basis_1d, bernstein, elements_of, gauss_01, multi_index
+
+
+def lame(E, nu):
+    """λ = Eν/((1+ν)(1-2ν)), μ = E/(2(1+ν)) (plane strain in 2D, reading R11)."""
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    return lam, mu
+
+
+# --------------------------------------------------------------------------
+# macro map evaluation in the element-local frame
+# --------------------------------------------------------------------------
+def element_grid(macro):
+    """Elements per direction (non-degenerate spans) of the macro patch."""
+    return [elements_of(U) for U in macro.knots]
+
+
+def tile_element(macro, t):
+    """Tile t <-> macro element (e0, e1[, e2]) flattened direction-0 fastest (reading R9)."""
+    els = element_grid(macro)
+    n = [len(e) for e in els]
+    ee = multi_index(n, t)
+    return tuple(els[k][ee[k]] for k in range(len(n)))
+
+
+def _active(macro, spans):
+    """Macro control points whose basis function is nonzero on the element: span-p..span."""
+    import itertools
+    n = macro.n_per_dir
+    rng = [range(spans[k] - macro.degree[k], spans[k] + 1) for k in range(macro.dim)]
+    out = []
+    for ii in itertools.product(*reversed(rng)):
+        ii = tuple(reversed(ii))
+        A = 0
+        for k in reversed(range(macro.dim)):
+            A = A * n[k] + ii[k]
+        out.append(A)
+    return out
+
+
+def macro_jacobian(macro, ctrl, t, xi):
+    """J[a, k] = ∂F_a/∂ξ_k at element-local points xi (n_pts, d) of tile t.
+
+    F(u) = Σ_i R_i^H(u) m_i (Eq. 4); u_k = U_k[s_k] + h_k ξ_k; ∂/∂ξ_k = h_k ∂/∂u_k.
+    `ctrl` may be complex (complex-step sensitivity).  Returns (n_pts, d, d)."""
+    d = macro.dim
+    spans = tile_element(macro, t)
+    vals, ders = [], []
+    for k in range(d):
+        U = macro.knots[k]
+        s = spans[k]
+        h = U[s + 1] - U[s]
+        u = U[s] + h * xi[:, k]
+        N, dN = basis_1d(U, macro.degree[k], s, u)
+        vals.append(N)
+        ders.append(dN * h)
+    n = macro.n_per_dir
+    J = np.zeros((xi.shape[0], d, d), dtype=np.result_type(ctrl, np.float64))
+    for A in _active(macro, spans):           # basis functions nonzero on the element
+        ii = multi_index(n, A)
+        for k in range(d):
+            g = np.ones(xi.shape[0])
+            for m in range(d):
+                g = g * (ders[m][ii[m]] if m == k else vals[m][ii[m]])
+            J[:, :, k] += g[:, None] * ctrl[A][None, :]
+    return J
+
+
+def macro_position(macro, ctrl, t, xi):
+    """F at element-local points xi of tile t (used by the energy-identity pin)."""
+    d = macro.dim
+    spans = tile_element(macro, t)
+    vals = []
+    for k in range(d):
+        U = macro.knots[k]
+        s = spans[k]
+        u = U[s] + (U[s + 1] - U[s]) * xi[:, k]
+        vals.append(basis_1d(U, macro.degree[k], s, u)[0])
+    n = macro.n_per_dir
+    X = np.zeros((xi.shape[0], d))
+    for A in _active(macro, spans):
+        ii = multi_index(n, A)
+        g = np.ones(xi.shape[0])
+        for m in range(d):
+            g = g * vals[m][ii[m]]
+        X += g[:, None] * ctrl[A][None, :]
+    return X
+
+
+# --------------------------------------------------------------------------
+# macro field Ā (three routes)
+# --------------------------------------------------------------------------
+def _det_inv(J):
+    D = np.linalg.det(J)
+    G = np.linalg.inv(J)          # G[i, a] = ǧ_i[a] (row i of J⁻¹)
+    return D, G
+
+
+def A_closed(J, lam, mu):
+    """Closed form of Eq. 37 (derivation in DESIGN.md §2).
+    J (..., d, d) -> A (..., d, d, d, d) indexed [i, j, a, b]."""
+    D, G = _det_inv(J)
+    d = J.shape[-1]
+    lam = np.asarray(lam)[..., None, None, None, None] if np.ndim(lam) else lam
+    mu = np.asarray(mu)[..., None, None, None, None] if np.ndim(mu) else mu
+    GiGj = np.einsum("...ia,...jb->...ijab", G, G)
+    GjGi = np.einsum("...ja,...ib->...ijab", G, G)
+    gg = np.einsum("...ic,...jc->...ij", G, G)
+    eye = np.eye(d)
+    A = lam * GiGj + mu * GjGi + mu * np.einsum("...ij,ab->...ijab", gg, eye)
+    return D[..., None, None, None, None] * A
+
+
+def _voigt_pairs(d):
+    return [(0, 0), (1, 1), (2, 2), (1, 2), (0, 2), (0, 1)] if d == 3 else [(0, 0), (1, 1), (0, 1)]
+
+
+def A_voigt(J, lam, mu):
+    """Paper route (App. A.2): Ā_ij = Ĝ_i Č Ĝ_jᵀ |det J| (Eq. 37, 97).
+
+    ĝ_k = column k of J (Eq. 79); ǧ^{kl} = [ĝ_k·ĝ_l]⁻¹ (Eq. 81);
+    Č_{ijkl} = λ ǧ^{ij} ǧ^{kl} + μ (ǧ^{ik} ǧ^{jl} + ǧ^{il} ǧ^{jk}) (Eq. 84a) in
+    Voigt order (11,22,33,23,13,12) (Eq. 93); Ĝ_i (d × n_v) has column v equal
+    to ĝ_l if Voigt pair v = {i, l} (l ≠ i or l = i), else 0 (Eq. 91)."""
+    J = np.asarray(J)
+    d = J.shape[-1]
+    pairs = _voigt_pairs(d)
+    nv = len(pairs)
+    gcov = np.swapaxes(J, -1, -2)                     # gcov[..., k, :] = ĝ_k
+    metric = np.einsum("...ka,...la->...kl", gcov, gcov)
+    gcon = np.linalg.inv(metric)
+    C = np.zeros(J.shape[:-2] + (nv, nv), dtype=J.dtype)
+    for v, (i, j) in enumerate(pairs):
+        for w, (k, l) in enumerate(pairs):
+            C[..., v, w] = lam * gcon[..., i, j] * gcon[..., k, l] + mu * (
+                gcon[..., i, k] * gcon[..., j, l] + gcon[..., i, l] * gcon[..., j, k])
+    Gh = np.zeros(J.shape[:-2] + (d, d, nv), dtype=J.dtype)   # Gh[..., i, :, v] = Ĝ_i column v
+    for i in range(d):
+        for v, (a, b) in enumerate(pairs):
+            if a == i:
+                Gh[..., i, :, v] = gcov[..., b, :]
+            elif b == i:
+                Gh[..., i, :, v] = gcov[..., a, :]
+    D = np.abs(np.linalg.det(J))
+    A = np.einsum("...iav,...vw,...jbw->...ijab", Gh, C, Gh)
+    return D[..., None, None, None, None] * A
+
+
+def A_tensor(J, lam, mu):
+    """Third route: Ā_ij[a,b] = D Σ_kl J⁻¹[i,k] C_{akbl} J⁻¹[j,l] with the isotropic
+    C_{akbl} = λ δ_ak δ_bl + μ (δ_ab δ_kl + δ_al δ_kb)."""
+    D, G = _det_inv(J)
+    d = J.shape[-1]
+    e = np.eye(d)
+    C = lam * np.einsum("ak,bl->akbl", e, e) + mu * (np.einsum("ab,kl->akbl", e, e) + np.einsum("al,kb->akbl", e, e))
+    return D[..., None, None, None, None] * np.einsum("...ik,akbl,...jl->...ijab", G, C, G)
+
+
+# --------------------------------------------------------------------------
+# interpolation onto Q_q (reading R1)
+# --------------------------------------------------------------------------
+def interp_nodes(q, d):
+    """(q+1)^d tensor Gauss–Legendre nodes on [0,1]^d, direction-0 fastest, ascending."""
+    x, _ = gauss_01(q + 1)
+    n1 = q + 1
+    pts = np.zeros((n1 ** d, d))
+    for m in range(n1 ** d):
+        for k in range(d):
+            pts[m, k] = x[(m // n1 ** k) % n1]
+    return pts
+
+
+def interpolate(samples, q, d):
+    """Coefficients c_C with Σ_C c_C N_C(x_m) = samples[m] at the interpolation
+    nodes: solves V c = s, V[m, C] = N_C(x_m) (plain definition).
+    samples: (n_pi, ...) -> coefficients (n_pi, ...)."""
+    V = bernstein(q, interp_nodes(q, d)).T      # (m, C)
+    s = np.asarray(samples)
+    flat = s.reshape(s.shape[0], -1)
+    c = np.linalg.solve(V.astype(np.result_type(flat, np.float64)), flat)
+    return c.reshape(s.shape)
+
+
+def tile_coefficients(prob, ctrl, t, E=None, route=A_closed):
+    """⟨Ā_ij⟩_C for tile t (Eq. 42 in interpolation form): shape (n_pi, d, d, d, d)
+    indexed [C, i, j, a, b].  Raises if det J <= 0 at a node (reading R5)."""
+    d, q = prob.d, prob.q
+    E = prob.young[t] if E is None else E
+    lam, mu = lame(E, prob.nu)
+    X = interp_nodes(q, d)
+    J = macro_jacobian(prob.macro, ctrl, t, X)
+    if np.any(np.real(np.linalg.det(J)) <= 0):
+        raise ValueError(f"degenerate macro element: tile {t}")
+    A = route(J, lam, mu)                       # (m, i, j, a, b)
+    return interpolate(A, q, d)
+
+
+def field_from_coefficients(coef, q, xi):
+    """Π_q Ā at points xi: Σ_C N_C(ξ) coef[C] (Eq. 42)."""
+    N = bernstein(q, xi)                        # (C, n_pts)
+    return np.einsum("cp,c...->p...", N, coef)

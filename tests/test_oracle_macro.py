@@ -1,0 +1,120 @@
+"""Pins for oracle/macro.py: the macro field Ā (Eq. 37, App. A) and
+the interpolation onto Q_q (reading R1)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import macro as M
+from oracle.bspline import bernstein, gauss_01
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+rng = np.random.default_rng(7)
+
+
+def rand_J(d, n=6):
+    return np.eye(d) * 1.5 + 0.4 * rng.standard_normal((n, d, d))
+
+
+def test_cube_golden_eq98_100():
+    g = json.load(open(os.path.join(GOLD, "cube_eq98_100.json")))
+    L, E, nu = g["L"], g["E"], g["nu"]
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    vals = {"a1": (lam + 2 * mu) * L, "a2": mu * L, "a3": lam * L, 0: 0.0}
+    J = np.eye(3)[None] * L                       # Eq. 98: M(ξ) = L ξ
+    A = M.A_closed(J, *M.lame(E, nu))[0]
+    for (i, j) in [(1, 1), (2, 2), (3, 3), (1, 2), (1, 3), (2, 3)]:
+        ref = np.array([[vals[x] for x in row] for row in g[f"A{i}{j}"]])
+        assert np.allclose(A[i - 1, j - 1], ref, rtol=1e-15, atol=1e-15), (i, j)
+        assert np.allclose(A[j - 1, i - 1], ref.T, rtol=1e-15, atol=1e-15)
+    # Voigt route (the paper's own Eqs. 89-97) gives the same cube
+    Av = M.A_voigt(J, *M.lame(E, nu))[0]
+    assert np.allclose(Av, A, rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_three_routes_agree(d):
+    J = rand_J(d)
+    lam, mu = 0.8, 0.45
+    A = M.A_closed(J, lam, mu)
+    assert np.allclose(M.A_voigt(J, lam, mu), A, rtol=0, atol=2e-14 * np.abs(A).max())
+    assert np.allclose(M.A_tensor(J, lam, mu), A, rtol=0, atol=2e-14 * np.abs(A).max())
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_block_symmetry_eq38(d):
+    A = M.A_closed(rand_J(d), 1.1, 0.6)
+    assert np.array_equal(A, np.transpose(A, (0, 2, 1, 4, 3))) or np.allclose(
+        A, np.transpose(A, (0, 2, 1, 4, 3)), rtol=0, atol=1e-15 * np.abs(A).max())
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_homogeneity(d):
+    J = rand_J(d)
+    A1 = M.A_closed(J, 1.0, 0.5)
+    A2 = M.A_closed(2.0 * J, 1.0, 0.5)
+    assert np.allclose(A2, 2.0 ** (d - 2) * A1, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_energy_form_equivalence(d):
+    """Σ_ij u_{,ξi}ᵀ Ā_ij v_{,ξj} == det J σ(u):ε(v) computed componentwise from the
+    physical gradients (Eqs. 28, 36)."""
+    J = rand_J(d, 1)[0]
+    lam, mu = 0.7, 0.3
+    A = M.A_closed(J[None], lam, mu)[0]
+    du = rng.standard_normal((d, d))     # du[a, i] = ∂u_a/∂ξ_i
+    dv = rng.standard_normal((d, d))
+    lhs = np.einsum("ai,ijab,bj->", du, A, dv)
+    Jinv = np.linalg.inv(J)
+    gu = du @ Jinv                        # ∂u_a/∂x_c
+    gv = dv @ Jinv
+    eu, ev = 0.5 * (gu + gu.T), 0.5 * (gv + gv.T)
+    sig = lam * np.trace(eu) * np.eye(d) + 2 * mu * eu
+    rhs = np.linalg.det(J) * np.sum(sig * ev)
+    assert abs(lhs - rhs) < 1e-13 * abs(rhs) + 1e-14
+
+
+@pytest.mark.parametrize("q,d", [(0, 2), (1, 2), (2, 2), (2, 3), (3, 3), (4, 2)])
+def test_interpolation_exact_on_Qq_and_idempotent(q, d):
+    c = rng.standard_normal((q + 1) ** d)
+    nodes = M.interp_nodes(q, d)
+    samples = bernstein(q, nodes).T @ c
+    c2 = M.interpolate(samples, q, d)
+    assert np.allclose(c2, c, atol=1e-12)
+    # idempotent: interpolating the interpolant reproduces it
+    c3 = M.interpolate(bernstein(q, nodes).T @ c2, q, d)
+    assert np.allclose(c3, c2, atol=1e-12)
+
+
+@pytest.mark.parametrize("q,d", [(1, 2), (2, 2), (2, 3), (3, 2)])
+def test_interpolation_equals_gauss_discretised_L2(q, d):
+    """Reading R1: interpolation at the (q+1) Gauss nodes == L2 projection (Eqs. 23-24)
+    whose mass matrix and right-hand side use the (q+1)-point Gauss rule."""
+    f = lambda x: np.exp(x[:, 0]) * np.cos(2 * x[:, -1]) + x[:, 0] ** 5
+    nodes = M.interp_nodes(q, d)
+    x1, w1 = gauss_01(q + 1)
+    w = np.ones(len(nodes))
+    n1 = q + 1
+    for m in range(len(nodes)):
+        for k in range(d):
+            w[m] *= w1[(m // n1 ** k) % n1]
+    N = bernstein(q, nodes)                      # (C, m)
+    Mpi = (N * w) @ N.T                          # Eq. 24 (mass)
+    r = (N * w) @ f(nodes)                       # Eq. 24 (rhs)
+    c_l2 = np.linalg.solve(Mpi, r)
+    c_int = M.interpolate(f(nodes), q, d)
+    assert np.allclose(c_l2, c_int, atol=1e-12)
+
+
+def test_affine_macro_field_is_constant():
+    """Affine F -> Ā constant -> interpolation coefficients are equal for every C."""
+    from synth import make_config
+    p = make_config(2, macro_amp=0.0)
+    coef = M.tile_coefficients(p, p.macro.ctrl, 5)
+    assert np.allclose(coef, coef[0][None], rtol=0, atol=1e-13 * np.abs(coef).max())
+    # box [0,4]x[0,1]^2 with 4x4x4 elements: J = diag(1, .25, .25)
+    A = M.A_closed(np.diag([1.0, 0.25, 0.25])[None], *M.lame(1.0, 0.3))[0]
+    assert np.allclose(coef[0], A, atol=1e-14)
