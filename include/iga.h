@@ -1,0 +1,193 @@
+/*
+ * iga.h — C ABI of libiga: B200-native interpolation-and-lookup formation of the
+ * isogeometric linear-elasticity stiffness matrix K of a microstructured geometry
+ * F∘M (Hirschler, Antolin, Buffa, arXiv 2107.09568; /root/reference/PAPER.md).
+ *
+ * Citations "P:L" are PAPER.md lines; "Rn" are the readings listed in DESIGN.md §4.
+ *
+ * Problem statement carried by the arguments:
+ *   - the reference tile 𝒯^r as a multi-patch spline into [0,1]^d (Eq. 3),
+ *   - the macro map ℳ = F, a single B-spline patch (Eq. 4); one tile per macro
+ *     element (Eqs. 5-10),
+ *   - the analysis degree p = the tile degree (the solution space recycles the tile
+ *     basis, Eq. 13) and the interpolation degree q = p_π (Eq. 21),
+ *   - isotropic elasticity constants E (per tile allowed) and ν.
+ *
+ * Pointers.  Entry points marked [any] accept host OR device pointers for their
+ * array arguments (the library inspects each pointer; host arrays are staged with
+ * cudaMemcpyAsync on the caller's stream).  [host] arguments must be host memory.
+ * All inputs are borrowed for the duration of the call; no input is retained.
+ *
+ * Errors.  Nothing throws across the ABI.  Every entry point returns an iga_status;
+ * on failure the outputs are unspecified and iga_last_error() (thread-local) names
+ * the offending patch / tile / node.  Calls enqueue work on `stream` (a
+ * cudaStream_t, NULL = legacy default stream) and synchronise that stream once at
+ * the end, so that the device-side degeneracy flag can be reported.
+ *
+ * Concurrency.  A handle is immutable after iga_build_tables except for its
+ * internal workspace; concurrent calls on one handle must be serialised by the
+ * caller (different handles are independent).
+ */
+#ifndef IGA_H
+#define IGA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  IGA_OK = 0,
+  IGA_EINVAL = 1,          /* invalid argument: dimension, degree, knots, sizes */
+  IGA_EDEGENERATE = 2,     /* det J <= 0 at a table point (tile) or interpolation node (macro), R5 */
+  IGA_ENONCONFORMING = 3,  /* tile faces / declared interfaces do not match (R10) */
+  IGA_ENOMEM = 4,          /* host or device allocation failed */
+  IGA_ECUDA = 5,           /* CUDA runtime error */
+  IGA_ELIMIT = 6           /* problem exceeds an index-width limit of this build */
+} iga_status;
+
+/* A tensor-product B-spline patch (Eq. 2).  [host]
+ * dim: parametric = physical dimension d (2 or 3).
+ * degree[k] >= 1, knots[k] (n_knots[k] values): open, non-decreasing, first = 0,
+ * last = 1, interior multiplicity <= degree[k].  n_ctrl = Π_k (n_knots[k]-degree[k]-1).
+ * ctrl: n_ctrl*dim doubles, point A = i0 + n0*(i1 + n1*i2) (direction-0 fastest),
+ * coordinates contiguous; may be NULL where only the topology is needed (macro). */
+typedef struct {
+  int32_t dim;
+  int32_t degree[3];
+  int32_t n_knots[3];
+  const double *knots[3];
+  const double *ctrl;
+} iga_spline;
+
+/* Declared intra-tile interface (R10): face (dir_a, side_a) of patch_a is glued to
+ * face (dir_b, side_b) of patch_b; side 0 = parameter 0, side 1 = parameter 1.
+ * Control points on the two faces are matched by position (|Δ| <= 1e-10). */
+typedef struct {
+  int32_t patch_a, dir_a, side_a;
+  int32_t patch_b, dir_b, side_b;
+} iga_interface;
+
+typedef struct iga_handle iga_handle;
+
+typedef struct {
+  int32_t dim;            /* d */
+  int32_t q;              /* interpolation degree p_π */
+  int32_t n_pi;           /* (q+1)^d Bernstein functions N_C (Eq. 21) */
+  int32_t n_k;            /* table columns κ = (i*d + j)*n_pi + C: d²·n_pi (Eq. 57) */
+  int32_t k_stride;       /* padded row stride (doubles) of the table / coefficient buffers */
+  int32_t n_patches;
+  int32_t n_gauss;        /* Gauss points per direction per tile knot span (R3) */
+  int32_t reserved;
+  int64_t n_tiles;        /* m_M = macro elements (Eq. 5) */
+  int64_t n_local_rows;   /* Σ_p n_nz,p = rows of the stacked mat𝔎 (Eqs. 56-57) */
+  int64_t n_macro_cp;     /* macro control points (Eq. 4) */
+  int64_t n_nodes;        /* global nodes after merging (R10) */
+  int64_t n_dof;          /* n_nodes * d, interleaved DOF = node*d + a (R9) */
+  int64_t nnz;            /* scalar CSR non-zeros of K (both triangles, R9) */
+  int64_t n_blocks;       /* d×d structural blocks */
+  int64_t n_contrib;      /* (tile, local row) -> block contributions (K4 gather list) */
+} iga_sizes;
+
+/* ---------------------------------------------------------------------------
+ * iga_build_tables — offline step ("the tables are built off-line").
+ *  tile_patches[n_patches]  the reference tile 𝒯^r (Eq. 3) [host]; all patches share
+ *                           dim and degree (p); control points must lie in [0,1]^d.
+ *  interfaces[n_interfaces] declared patch interfaces (may be NULL if 0) [host].
+ *  macro_topology           degree and knots of F (ctrl ignored) [host].
+ *  q                        interpolation degree (0..4).
+ *  n_gauss                  Gauss points per direction per span; 0 = p + ceil((q+1)/2) (R3).
+ *  stream                   cudaStream_t used for the device work.
+ *  out                      receives a new handle (owned by the caller; free with iga_free).
+ * Device work: K1 (lookup tables 𝔎_p by micro Gauss quadrature, Eq. 52).
+ * Host work: validation, I_coo (Eq. 56), DofMap (R10), CSR pattern + gather lists (R9).
+ * Errors: EINVAL (bad spline / degrees / sizes), ENONCONFORMING (unmatched face or
+ * interface control point, two points of one patch merged), EDEGENERATE (det J_T <= 0
+ * at a table quadrature point), ENOMEM, ECUDA, ELIMIT (index packing limits).
+ * ------------------------------------------------------------------------- */
+iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches,
+                            const iga_interface *interfaces, int32_t n_interfaces,
+                            const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
+                            void *stream, iga_handle **out);
+
+/* iga_build_topology — host-only variant of iga_build_tables: validation, I_coo,
+ * DofMap and the CSR pattern, no device work and no tables.  The handle answers
+ * iga_get_sizes / iga_get_pattern (host pointers) / iga_get_block_map /
+ * iga_get_node_map / iga_get_pairs; kernel entry points return IGA_EINVAL.  Lets a
+ * caller size a problem (nnz, n_dof) before committing device memory. */
+iga_status iga_build_topology(const iga_spline *tile_patches, int32_t n_patches,
+                              const iga_interface *interfaces, int32_t n_interfaces,
+                              const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
+                              iga_handle **out);
+
+/* ---------------------------------------------------------------------------
+ * iga_assemble — form K^π (Eq. 50) into CSR values: the hot path (§3.2.4 steps 1-4).
+ *  macro_ctrl   [any] n_macro_cp*d doubles: the control net of F (Eq. 4).
+ *  young        [any] E: one double (young_per_tile = 0) or n_tiles doubles (= 1).
+ *  nu           Poisson ratio, -1 < ν < 0.5.
+ *  csr_values   [any] nnz doubles, overwritten, ordered as the pattern of iga_get_pattern.
+ *  local_values [any] optional (NULL = skip): n_local_rows*n_tiles*d² doubles receiving
+ *               nzdata (Eq. 58) as local[row][t*d² + a*d + b].
+ * Kernels: K2 (per-tile ∇F at the (q+1)^d Gauss nodes -> Ā (Eq. 37) -> interpolation
+ * coefficients, R1), K3 (FP64 DMMA contraction nzdata = mat𝔎·mat⟨Ā⟩, Eq. 58),
+ * K4 (atomic-free owner-computes gather into the full symmetric CSR, R9).
+ * Errors: EINVAL, EDEGENERATE (det ∇F <= 0 at an interpolation node), ECUDA.
+ * ------------------------------------------------------------------------- */
+iga_status iga_assemble(const iga_handle *h, const double *macro_ctrl, const double *young,
+                        int32_t young_per_tile, double nu, double *csr_values,
+                        double *local_values, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * iga_sensitivity — g[k*d + α] = uᵀ (∂K^π/∂P_{k,α}) v for every macro control-point
+ * coordinate (Eqs. 70-73; R13: u ≠ v allowed, K^π as assembled by R9).
+ *  u, v  [any] n_dof doubles (interleaved DOF).   grad [any] n_macro_cp*d, overwritten.
+ * Kernels: K5a (W_t = mat𝔎ᵀ X_t, FP64 DMMA, X_t generated from u, v on the fly),
+ * K5b (Ŵ = Πᵀ W, analytic reverse mode of Ā(J), chain to P), K5c (deterministic
+ * reduction over the tiles sharing a control point).
+ * ------------------------------------------------------------------------- */
+iga_status iga_sensitivity(const iga_handle *h, const double *macro_ctrl, const double *young,
+                           int32_t young_per_tile, double nu, const double *u, const double *v,
+                           double *grad, void *stream);
+
+/* iga_interpolate — K2 only (parity): coefficients ⟨Ā_ij⟩_C of every tile, written as
+ * coef[(t*d² + a*d + b)*k_stride + κ] with κ = (i*d + j)*n_pi + C.  [any] pointers. */
+iga_status iga_interpolate(const iga_handle *h, const double *macro_ctrl, const double *young,
+                           int32_t young_per_tile, double nu, double *coef, void *stream);
+
+/* Accessors.  iga_get_sizes: [host] out. */
+iga_status iga_get_sizes(const iga_handle *h, iga_sizes *out);
+
+/* iga_get_pattern — row_ptr (n_dof+1 int64), col_idx (nnz int32); either may be NULL.
+ * [any] pointers. */
+iga_status iga_get_pattern(const iga_handle *h, int64_t *row_ptr, int32_t *col_idx);
+
+/* iga_get_block_map — for tiles [t_begin, t_end): (pos(I*d,J*d), pos(J*d,I*d)) per
+ * (tile, local row) as 2 int64 each, tile-major (R9). [host] out. */
+iga_status iga_get_block_map(const iga_handle *h, int64_t t_begin, int64_t t_end, int64_t *out);
+
+/* iga_get_node_map — node[t*n_local_ctrl + off_p + A] for all tiles (R10). [host] out
+ * (n_tiles * Σ_p n_ctrl,p int32).  */
+iga_status iga_get_node_map(const iga_handle *h, int32_t *out);
+
+/* iga_get_tables — the stacked table mat𝔎 (n_local_rows × n_k, row-major, unpadded). [any] */
+iga_status iga_get_tables(const iga_handle *h, double *out);
+
+/* iga_get_pairs — (A, B) of every stacked table row, 2 int32 per row. [host] */
+iga_status iga_get_pairs(const iga_handle *h, int32_t *out);
+
+/* Per-kernel device time accumulated by the last iga_assemble / iga_sensitivity calls
+ * while profiling is enabled (CUDA events on the caller's stream).  Slots:
+ * 0 K2 interpolate, 1 K3 contraction, 2 K4 scatter, 3 K5a W-GEMM, 4 K5b reverse,
+ * 5 K5c reduce, 6 host<->device staging.  enable != 0 resets the accumulators. */
+iga_status iga_set_profiling(iga_handle *h, int32_t enable);
+iga_status iga_get_kernel_times(const iga_handle *h, double *ms_out /* 8 */, int64_t *launches_out /* 8 */);
+
+void iga_free(iga_handle *h);
+const char *iga_last_error(void);
+const char *iga_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGA_H */

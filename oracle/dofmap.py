@@ -184,3 +184,33 @@ class Pattern:
         fwd = self.pos(self.I.ravel(), self.J.ravel())
         bwd = self.pos(self.J.ravel(), self.I.ravel())
         return np.stack([fwd, bwd], axis=1)
+
+
+def node_locations(dm):
+    """node -> list of flat (t*n_local + loc) indices (CSR-like arrays)."""
+    flat = dm.node.ravel()
+    order = np.argsort(flat, kind="stable")
+    starts = np.searchsorted(flat[order], np.arange(dm.n_nodes + 1))
+    return order, starts
+
+
+def row_contributions(prob, dm, pairs, I, locs=None):
+    """For one node row I (no full pattern needed): the sorted block columns J and,
+    per J, the contributing (t, row, transposed) triples in (t, row) order (R9)."""
+    order, starts = locs if locs is not None else node_locations(dm)
+    nl = dm.n_local_ctrl
+    row_off = np.cumsum([0] + [len(p) for p in pairs])
+    contrib = {}
+    for f in order[starts[I]:starts[I + 1]]:
+        t, loc = divmod(int(f), nl)
+        p = int(np.searchsorted(dm.offsets, loc, side="right") - 1)
+        A = loc - dm.offsets[p]
+        pr = pairs[p]
+        for k in np.nonzero((pr[:, 0] == A) | (pr[:, 1] == A))[0]:
+            a, b = int(pr[k, 0]), int(pr[k, 1])
+            other = b if a == A else a
+            J = int(dm.node[t, dm.offsets[p] + other])
+            tr = int(a != A)                 # I is the B-side of the pair -> transposed block
+            contrib.setdefault(J, []).append((t, int(row_off[p] + k), tr))
+    cols = sorted(contrib)
+    return cols, [sorted(contrib[J]) for J in cols]

@@ -1,0 +1,209 @@
+"""Thin ctypes binding of libiga (include/iga.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; there is no
+Python or CPU fallback.  If libiga.so is missing this module raises at import of
+`load()` — build it with `python -m paper_2107_09568_b200.build` (or
+`__graft_entry__.build()`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libiga.so")
+
+IGA_STATUS = {0: "IGA_OK", 1: "IGA_EINVAL", 2: "IGA_EDEGENERATE", 3: "IGA_ENONCONFORMING", 4: "IGA_ENOMEM",
+              5: "IGA_ECUDA", 6: "IGA_ELIMIT"}
+
+
+class IgaError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{IGA_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class iga_spline(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("degree", C.c_int32 * 3), ("n_knots", C.c_int32 * 3),
+                ("knots", C.POINTER(C.c_double) * 3), ("ctrl", C.POINTER(C.c_double))]
+
+
+class iga_interface(C.Structure):
+    _fields_ = [("patch_a", C.c_int32), ("dir_a", C.c_int32), ("side_a", C.c_int32),
+                ("patch_b", C.c_int32), ("dir_b", C.c_int32), ("side_b", C.c_int32)]
+
+
+class iga_sizes(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("q", C.c_int32), ("n_pi", C.c_int32), ("n_k", C.c_int32),
+                ("k_stride", C.c_int32), ("n_patches", C.c_int32), ("n_gauss", C.c_int32), ("reserved", C.c_int32),
+                ("n_tiles", C.c_int64), ("n_local_rows", C.c_int64), ("n_macro_cp", C.c_int64),
+                ("n_nodes", C.c_int64), ("n_dof", C.c_int64), ("nnz", C.c_int64), ("n_blocks", C.c_int64),
+                ("n_contrib", C.c_int64)]
+
+
+EXPORTS = ["iga_build_tables", "iga_build_topology", "iga_assemble", "iga_sensitivity", "iga_interpolate", "iga_get_sizes",
+           "iga_get_pattern", "iga_get_block_map", "iga_get_node_map", "iga_get_tables", "iga_get_pairs",
+           "iga_set_profiling", "iga_get_kernel_times", "iga_free", "iga_last_error", "iga_version"]
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libiga.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64, d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    lib.iga_build_tables.argtypes = [C.POINTER(iga_spline), i32, C.POINTER(iga_interface), i32,
+                                     C.POINTER(iga_spline), i32, i32, vp, C.POINTER(vp)]
+    lib.iga_build_topology.argtypes = [C.POINTER(iga_spline), i32, C.POINTER(iga_interface), i32,
+                                       C.POINTER(iga_spline), i32, i32, C.POINTER(vp)]
+    lib.iga_assemble.argtypes = [vp, vp, vp, i32, d, vp, vp, vp]
+    lib.iga_sensitivity.argtypes = [vp, vp, vp, i32, d, vp, vp, vp, vp]
+    lib.iga_interpolate.argtypes = [vp, vp, vp, i32, d, vp, vp]
+    lib.iga_get_sizes.argtypes = [vp, C.POINTER(iga_sizes)]
+    lib.iga_get_pattern.argtypes = [vp, vp, vp]
+    lib.iga_get_block_map.argtypes = [vp, i64, i64, vp]
+    lib.iga_get_node_map.argtypes = [vp, vp]
+    lib.iga_get_tables.argtypes = [vp, vp]
+    lib.iga_get_pairs.argtypes = [vp, vp]
+    lib.iga_set_profiling.argtypes = [vp, i32]
+    lib.iga_get_kernel_times.argtypes = [vp, vp, vp]
+    lib.iga_free.argtypes = [vp]
+    lib.iga_free.restype = None
+    lib.iga_last_error.restype = C.c_char_p
+    lib.iga_version.restype = C.c_char_p
+    for name in EXPORTS:
+        if name not in ("iga_free", "iga_last_error", "iga_version"):
+            getattr(lib, name).restype = C.c_int
+    _lib = lib
+    return lib
+
+
+def _check(status):
+    if status != 0:
+        raise IgaError(status, load().iga_last_error().decode())
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor (any device) or a C-contiguous numpy array."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data
+    assert x.is_contiguous(), "tensor must be contiguous"
+    return x.data_ptr()
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _spline(s, keep):
+    sp = iga_spline()
+    sp.dim = s.dim
+    for k in range(3):
+        if k < s.dim:
+            U = np.ascontiguousarray(s.knots[k], dtype=np.float64)
+            keep.append(U)
+            sp.degree[k] = s.degree[k]
+            sp.n_knots[k] = len(U)
+            sp.knots[k] = U.ctypes.data_as(C.POINTER(C.c_double))
+    if s.ctrl is not None:
+        P = np.ascontiguousarray(s.ctrl, dtype=np.float64)
+        keep.append(P)
+        sp.ctrl = P.ctypes.data_as(C.POINTER(C.c_double))
+    return sp
+
+
+class Assembler:
+    """Handle around iga_build_tables for a problem description (synth.Problem-like:
+    .tile (patches), .interfaces, .macro (degree/knots), .q, .n_gauss)."""
+
+    def __init__(self, prob, n_gauss=0, stream=None, topology_only=False):
+        lib = load()
+        keep = []
+        arr = (iga_spline * len(prob.tile))(*[_spline(s, keep) for s in prob.tile])
+        ifs = (iga_interface * max(1, len(prob.interfaces)))()
+        for n, f in enumerate(prob.interfaces):
+            ifs[n] = iga_interface(f.patch_a, f.dir_a, f.side_a, f.patch_b, f.dir_b, f.side_b)
+        mac = _spline(prob.macro, keep)
+        h = C.c_void_p()
+        if topology_only:
+            _check(lib.iga_build_topology(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), prob.q,
+                                          n_gauss, C.byref(h)))
+        else:
+            _check(lib.iga_build_tables(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), prob.q,
+                                        n_gauss, _stream_ptr(stream), C.byref(h)))
+        self._h = h
+        self.sizes = iga_sizes()
+        _check(lib.iga_get_sizes(h, C.byref(self.sizes)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.iga_free(self._h)
+            self._h = None
+
+    # --- hot path -----------------------------------------------------------
+    def assemble(self, ctrl, young, nu, values, local=None, stream=None):
+        _check(load().iga_assemble(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
+                                   _ptr(values), _ptr(local), _stream_ptr(stream)))
+
+    def sensitivity(self, ctrl, young, nu, u, v, grad, stream=None):
+        _check(load().iga_sensitivity(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
+                                      _ptr(u), _ptr(v), _ptr(grad), _stream_ptr(stream)))
+
+    def interpolate(self, ctrl, young, nu, coef, stream=None):
+        _check(load().iga_interpolate(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
+                                      _ptr(coef), _stream_ptr(stream)))
+
+    # --- accessors ----------------------------------------------------------
+    def pattern(self, row_ptr=None, col_idx=None):
+        _check(load().iga_get_pattern(self._h, _ptr(row_ptr), _ptr(col_idx)))
+
+    def block_map(self, t_begin=0, t_end=None):
+        t_end = self.sizes.n_tiles if t_end is None else t_end
+        out = np.empty(((t_end - t_begin) * self.sizes.n_local_rows, 2), dtype=np.int64)
+        _check(load().iga_get_block_map(self._h, t_begin, t_end, out.ctypes.data))
+        return out
+
+    def node_map_for(self, n_local_ctrl):
+        out = np.empty(self.sizes.n_tiles * n_local_ctrl, dtype=np.int32)
+        _check(load().iga_get_node_map(self._h, out.ctypes.data))
+        return out.reshape(self.sizes.n_tiles, n_local_ctrl)
+
+    def tables(self):
+        out = np.empty((self.sizes.n_local_rows, self.sizes.n_k), dtype=np.float64)
+        _check(load().iga_get_tables(self._h, out.ctypes.data))
+        return out
+
+    def pairs(self):
+        out = np.empty((self.sizes.n_local_rows, 2), dtype=np.int32)
+        _check(load().iga_get_pairs(self._h, out.ctypes.data))
+        return out
+
+    def set_profiling(self, enable=True):
+        _check(load().iga_set_profiling(self._h, int(enable)))
+
+    def kernel_times(self):
+        ms = np.zeros(8, dtype=np.float64)
+        n = np.zeros(8, dtype=np.int64)
+        _check(load().iga_get_kernel_times(self._h, ms.ctypes.data, n.ctypes.data))
+        return ms, n
+
+
+def _numel(x):
+    return x.size if isinstance(x, np.ndarray) else x.numel()

@@ -1,0 +1,99 @@
+// device_common.cuh — small device helpers shared by the libiga kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include "internal.h"
+
+namespace iga {
+
+// Nonzero B-spline basis values N[r] = N_{s-p+r,p}(u) and first derivatives on knot
+// span s (Cox–de Boor triangle; derivative from the degree p-1 values:
+// N'_{i,p} = p N_{i,p-1}/(U_{i+p}-U_i) - p N_{i+1,p-1}/(U_{i+p+1}-U_{i+1})).
+__device__ __forceinline__ void bspline_eval(const double *U, int p, int s, double u, double *N, double *dN) {
+  double left[IGA_MAXP + 1], right[IGA_MAXP + 1], Nd[IGA_MAXP + 1], Nm1[IGA_MAXP + 1];
+  Nd[0] = 1.0;
+  Nm1[0] = 1.0;
+  for (int j = 1; j <= p; ++j) {
+    left[j] = u - U[s + 1 - j];
+    right[j] = U[s + j] - u;
+    double saved = 0.0;
+    for (int r = 0; r < j; ++r) {
+      double temp = Nd[r] / (right[r + 1] + left[j - r]);
+      Nd[r] = saved + right[r + 1] * temp;
+      saved = left[j - r] * temp;
+    }
+    Nd[j] = saved;
+    if (j == p - 1)
+      for (int r = 0; r < p; ++r) Nm1[r] = Nd[r];
+  }
+  for (int r = 0; r <= p; ++r) {
+    N[r] = Nd[r];
+    int i = s - p + r;
+    double t1 = (r >= 1) ? Nm1[r - 1] / (U[i + p] - U[i]) : 0.0;
+    double t2 = (r <= p - 1) ? Nm1[r] / (U[i + p + 1] - U[i + 1]) : 0.0;
+    dN[r] = p * (t1 - t2);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ double det_inv(const double J[D][D], double G[D][D]) {
+  if (D == 2) {
+    double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    double id = 1.0 / det;
+    G[0][0] = J[1][1] * id;
+    G[0][1] = -J[0][1] * id;
+    G[1][0] = -J[1][0] * id;
+    G[1][1] = J[0][0] * id;
+    return det;
+  } else {
+    double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    double id = 1.0 / det;
+    G[0][0] = c00 * id;
+    G[1][0] = c01 * id;
+    G[2][0] = c02 * id;
+    G[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+    G[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+    G[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+    G[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+    G[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+    G[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+    return det;
+  }
+}
+
+__device__ __forceinline__ double bernstein1(int q, int k, double x) {
+  double b = 1.0;
+  for (int i = 1; i <= k; ++i) b = b * (q - k + i) / i;   // binom(q, k)
+  double r = b;
+  for (int i = 0; i < k; ++i) r *= x;
+  for (int i = 0; i < q - k; ++i) r *= (1.0 - x);
+  return r;
+}
+
+// record the first degeneracy (flag[0] = code, flag[1] = tile/patch, flag[2] = node/point)
+__device__ __forceinline__ void raise_flag(int *flag, int code, int a, int b) {
+  if (atomicCAS(flag, 0, code) == 0) {
+    flag[1] = a;
+    flag[2] = b;
+  }
+}
+
+// FP64 tensor core: D = A(8x4,row) * B(4x8,col) + C, per-lane fragments
+// a = A[l/4][l%4], b = B[l%4][l/4], c = C[l/4][2(l%4)+{0,1}]  (verified, profiles/r01_fp64_ceiling.md)
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+}  // namespace iga

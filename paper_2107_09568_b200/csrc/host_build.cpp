@@ -1,0 +1,403 @@
+// host_build.cpp — host side of iga_build_tables: validation, I_coo (Eq. 56),
+// DofMap (reading R10), full symmetric CSR pattern and the atomic-free gather
+// lists of K4 (reading R9), Gauss rules and the interpolation operator (R1).
+// Everything here is integer/topology work done once per handle.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <omp.h>
+#include "internal.h"
+
+namespace iga {
+
+static thread_local char g_err[1024] = "";
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char *get_error() { return g_err; }
+
+// n-point Gauss–Legendre rule mapped to [0,1], nodes ascending (Newton on P_n).
+iga_status upload_topology(Handle &h) {
+  auto up = [&](void **dst, const void *src, size_t bytes) -> bool {
+    if (cudaMalloc(dst, std::max<size_t>(bytes, 8)) != cudaSuccess) { set_error("cudaMalloc(%zu) failed", bytes); return false; }
+    if (bytes && cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) { set_error("H2D copy failed"); return false; }
+    return true;
+  };
+  if (!up((void **)&h.d_node_map, h.node_map.data(), h.node_map.size() * 4) ||
+      !up((void **)&h.d_pairA, h.pairA.data(), h.pairA.size() * 4) ||
+      !up((void **)&h.d_pairB, h.pairB.data(), h.pairB.size() * 4) ||
+      !up((void **)&h.d_brow_ptr, h.brow_ptr.data(), h.brow_ptr.size() * 8) ||
+      !up((void **)&h.d_bcol, h.bcol.data(), h.bcol.size() * 4) ||
+      !up((void **)&h.d_bcnt, h.bcnt.data(), h.bcnt.size()) ||
+      !up((void **)&h.d_cstart, h.cstart.data(), h.cstart.size() * 8) ||
+      !up((void **)&h.d_contrib, h.contrib.data(), h.contrib.size() * 4))
+    return IGA_ENOMEM;
+  // the gather lists live on the device only from here on
+  std::vector<uint8_t>().swap(h.bcnt);
+  std::vector<uint32_t>().swap(h.contrib);
+  std::vector<int64_t>().swap(h.cstart);
+  return IGA_OK;
+}
+
+void gauss_legendre01(int n, double *x, double *w) {
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < (n + 1) / 2; ++i) {
+    double z = std::cos(pi * (i + 0.75) / (n + 0.5)), pp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int j = 1; j <= n; ++j) {
+        double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = n * (z * p1 - p2) / (z * z - 1.0);
+      double z1 = z;
+      z = z1 - p1 / pp;
+      if (std::fabs(z - z1) < 1e-16) break;
+    }
+    double wi = 2.0 / ((1.0 - z * z) * pp * pp);
+    // z > 0 is the (i)-th largest root
+    x[n - 1 - i] = 0.5 * (1.0 + z);
+    x[i] = 0.5 * (1.0 - z);
+    w[n - 1 - i] = 0.5 * wi;
+    w[i] = 0.5 * wi;
+  }
+}
+
+static double binom(int n, int k) {
+  double r = 1.0;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
+// Gauss–Jordan inverse with partial pivoting (n <= 5).
+static bool invert(int n, const double *a, double *inv) {
+  double m[5][10];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < 2 * n; ++j) m[i][j] = j < n ? a[i * n + j] : (j - n == i ? 1.0 : 0.0);
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(m[r][c]) > std::fabs(m[piv][c])) piv = r;
+    if (std::fabs(m[piv][c]) < 1e-300) return false;
+    for (int j = 0; j < 2 * n; ++j) std::swap(m[c][j], m[piv][j]);
+    double f = 1.0 / m[c][c];
+    for (int j = 0; j < 2 * n; ++j) m[c][j] *= f;
+    for (int r = 0; r < n; ++r)
+      if (r != c) {
+        double g = m[r][c];
+        for (int j = 0; j < 2 * n; ++j) m[r][j] -= g * m[c][j];
+      }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) inv[i * n + j] = m[i][j + n];
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// validation of one spline's knots (open, normalised, multiplicities)
+static bool check_knots(const iga_spline &s, int k, const char *what, int idx,
+                        std::vector<double> &U, std::vector<int> &el) {
+  int p = s.degree[k], nk = s.n_knots[k];
+  if (p < 1 || p > IGA_MAXP) { set_error("%s %d: degree[%d]=%d outside [1,%d]", what, idx, k, p, IGA_MAXP); return false; }
+  if (nk < 2 * (p + 1) || !s.knots[k]) { set_error("%s %d: too few knots in direction %d", what, idx, k); return false; }
+  U.assign(s.knots[k], s.knots[k] + nk);
+  for (int i = 0; i + 1 < nk; ++i)
+    if (!(U[i] <= U[i + 1])) { set_error("%s %d: knots of direction %d not non-decreasing", what, idx, k); return false; }
+  for (int i = 0; i <= p; ++i)
+    if (U[i] != 0.0 || U[nk - 1 - i] != 1.0) { set_error("%s %d: knot vector %d not open on [0,1]", what, idx, k); return false; }
+  if (!(U[p + 1] > 0.0) || !(U[nk - p - 2] < 1.0)) { set_error("%s %d: end knot multiplicity > degree+1 in direction %d", what, idx, k); return false; }
+  for (int i = p + 1; i < nk - p - 1;) {
+    int j = i;
+    while (j + 1 < nk - p - 1 && U[j + 1] == U[i]) ++j;
+    if (j - i + 1 > p) { set_error("%s %d: interior knot multiplicity > degree in direction %d", what, idx, k); return false; }
+    i = j + 1;
+  }
+  el.clear();
+  for (int i = p; i < nk - p - 1; ++i)
+    if (U[i] < U[i + 1]) el.push_back(i);
+  return true;
+}
+
+static int ceil_log2(int64_t v) {
+  int b = 0;
+  while ((int64_t(1) << b) < v) ++b;
+  return b;
+}
+
+struct UF {
+  std::vector<int64_t> par;
+  explicit UF(int64_t n) : par(n) { std::iota(par.begin(), par.end(), 0); }
+  int64_t find(int64_t x) {
+    while (par[x] != x) { par[x] = par[par[x]]; x = par[x]; }
+    return x;
+  }
+  void unite(int64_t a, int64_t b) {
+    a = find(a); b = find(b);
+    if (a == b) return;
+    if (a < b) par[b] = a; else par[a] = b;
+  }
+};
+
+iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const iga_interface *ifc,
+                      int n_ifc, const iga_spline *macro, int q, int n_gauss) {
+  if (!tile || n_patches <= 0 || !macro) { set_error("no tile patches or no macro topology"); return IGA_EINVAL; }
+  const int d = tile[0].dim;
+  if (d != 2 && d != 3) { set_error("dim must be 2 or 3 (got %d)", d); return IGA_EINVAL; }
+  if (macro->dim != d) { set_error("macro dim %d != tile dim %d", macro->dim, d); return IGA_EINVAL; }
+  if (q < 0 || q > IGA_MAXQ) { set_error("q=%d outside [0,%d]", q, IGA_MAXQ); return IGA_EINVAL; }
+  h.d = d;
+  h.q = q;
+  h.p = tile[0].degree[0];
+  h.n_patches = n_patches;
+  h.patches.resize(n_patches);
+  int off = 0;
+  for (int pi = 0; pi < n_patches; ++pi) {
+    const iga_spline &s = tile[pi];
+    PatchInfo &P = h.patches[pi];
+    if (s.dim != d) { set_error("tile patch %d: dim %d != %d", pi, s.dim, d); return IGA_EINVAL; }
+    P.n_ctrl = 1;
+    P.n_spans = 1;
+    for (int k = 0; k < 3; ++k) { P.deg[k] = 0; P.n[k] = 1; P.n_span[k] = 1; }
+    for (int k = 0; k < d; ++k) {
+      if (!check_knots(s, k, "tile patch", pi, P.knots[k], P.el_span[k])) return IGA_EINVAL;
+      if (s.degree[k] != h.p) { set_error("tile patch %d: all tile directions/patches must share degree p=%d", pi, h.p); return IGA_EINVAL; }
+      P.deg[k] = s.degree[k];
+      P.n[k] = s.n_knots[k] - s.degree[k] - 1;
+      P.n_span[k] = (int)P.el_span[k].size();
+      P.n_ctrl *= P.n[k];
+      P.n_spans *= P.n_span[k];
+    }
+    if (!s.ctrl) { set_error("tile patch %d: no control points", pi); return IGA_EINVAL; }
+    P.ctrl.assign(s.ctrl, s.ctrl + (size_t)P.n_ctrl * d);
+    for (double c : P.ctrl)
+      if (!(c >= -1e-12 && c <= 1.0 + 1e-12)) { set_error("tile patch %d: control point outside [0,1]^d (Eq. 10 condition)", pi); return IGA_EINVAL; }
+    P.ctrl_off = off;
+    off += P.n_ctrl;
+  }
+  h.n_local_ctrl = off;
+  h.n_cp = 1;
+  h.n_tiles = 1;
+  for (int k = 0; k < d; ++k) {
+    if (!check_knots(*macro, k, "macro", 0, h.mknots[k], h.mel_span[k])) return IGA_EINVAL;
+    h.pm[k] = macro->degree[k];
+    h.mn[k] = macro->n_knots[k] - macro->degree[k] - 1;
+    h.mel[k] = (int)h.mel_span[k].size();
+    h.n_cp *= h.mn[k];
+    h.n_tiles *= h.mel[k];
+  }
+  h.n_g = n_gauss > 0 ? n_gauss : h.p + (q + 2) / 2;
+  if (h.n_g > 12) { set_error("n_gauss=%d > 12", h.n_g); return IGA_EINVAL; }
+  h.npi = 1;
+  for (int k = 0; k < d; ++k) h.npi *= (q + 1);
+  h.nk = d * d * h.npi;
+  h.kstride = (h.nk + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK;
+
+  // ---- I_coo per patch (Eq. 56; R8: supports share a knot span) -------------
+  h.M = 0;
+  h.pairA.clear();
+  h.pairB.clear();
+  int span_off = 0;
+  for (int pi = 0; pi < n_patches; ++pi) {
+    PatchInfo &P = h.patches[pi];
+    // 1D: function a is nonzero on knot spans a..a+p; spans must be elements
+    std::vector<std::vector<char>> share(d);
+    for (int k = 0; k < d; ++k) {
+      int n = P.n[k], p = P.deg[k];
+      share[k].assign((size_t)n * n, 0);
+      for (int s : P.el_span[k])
+        for (int a = std::max(0, s - p); a <= std::min(n - 1, s); ++a)
+          for (int b = std::max(0, s - p); b <= std::min(n - 1, s); ++b) share[k][(size_t)a * n + b] = 1;
+    }
+    P.row_off = (int)h.M;
+    int cnt = 0;
+    for (int A = 0; A < P.n_ctrl; ++A) {
+      int ia[3] = {A % P.n[0], (A / P.n[0]) % P.n[1], A / (P.n[0] * P.n[1])};
+      for (int B = A; B < P.n_ctrl; ++B) {
+        int ib[3] = {B % P.n[0], (B / P.n[0]) % P.n[1], B / (P.n[0] * P.n[1])};
+        bool ok = true;
+        for (int k = 0; k < d && ok; ++k) ok = share[k][(size_t)ia[k] * P.n[k] + ib[k]];
+        if (ok) {
+          h.pairA.push_back(P.ctrl_off + A);
+          h.pairB.push_back(P.ctrl_off + B);
+          ++cnt;
+        }
+      }
+    }
+    P.n_nz = cnt;
+    h.M += cnt;
+    P.span_off = span_off;
+    span_off += P.n_spans;
+  }
+
+  // ---- DofMap (R10) ------------------------------------------------------------
+  const double TOL = 1e-10;
+  auto pos = [&](int loc, int k) -> double {
+    for (int pi = n_patches - 1; pi >= 0; --pi)
+      if (loc >= h.patches[pi].ctrl_off) return h.patches[pi].ctrl[(size_t)(loc - h.patches[pi].ctrl_off) * d + k];
+    return 0.0;
+  };
+  auto close = [&](int a, int b, const double *shift) {
+    for (int k = 0; k < d; ++k)
+      if (std::fabs(pos(a, k) - shift[k] - pos(b, k)) > TOL) return false;
+    return true;
+  };
+  std::vector<std::pair<int, int>> intra;
+  for (int f = 0; f < n_ifc; ++f) {
+    const iga_interface &I = ifc[f];
+    if (I.patch_a < 0 || I.patch_a >= n_patches || I.patch_b < 0 || I.patch_b >= n_patches || I.dir_a < 0 ||
+        I.dir_a >= d || I.dir_b < 0 || I.dir_b >= d) { set_error("interface %d: bad patch/direction", f); return IGA_EINVAL; }
+    auto members = [&](int pi, int dir, int side) {
+      std::vector<int> m;
+      const PatchInfo &P = h.patches[pi];
+      int want = side ? P.n[dir] - 1 : 0;
+      for (int A = 0; A < P.n_ctrl; ++A) {
+        int ii[3] = {A % P.n[0], (A / P.n[0]) % P.n[1], A / (P.n[0] * P.n[1])};
+        if (ii[dir] == want) m.push_back(P.ctrl_off + A);
+      }
+      return m;
+    };
+    auto ma = members(I.patch_a, I.dir_a, I.side_a), mb = members(I.patch_b, I.dir_b, I.side_b);
+    double zero[3] = {0, 0, 0};
+    for (int a : ma) {
+      int hit = -1, nh = 0;
+      for (int b : mb)
+        if (close(a, b, zero)) { hit = b; ++nh; }
+      if (nh != 1) { set_error("interface %d: control point %d of patch %d has %d partners", f, a, I.patch_a, nh); return IGA_ENONCONFORMING; }
+      intra.push_back({a, hit});
+    }
+  }
+  std::vector<std::vector<std::pair<int, int>>> inter(d);
+  for (int k = 0; k < d; ++k) {
+    std::vector<int> hi, lo;
+    for (int a = 0; a < h.n_local_ctrl; ++a) {
+      if (std::fabs(pos(a, k) - 1.0) <= TOL) hi.push_back(a);
+      if (std::fabs(pos(a, k)) <= TOL) lo.push_back(a);
+    }
+    if (hi.size() != lo.size()) { set_error("tile faces xi_%d=0 and xi_%d=1 carry %zu vs %zu control points", k, k, lo.size(), hi.size()); return IGA_ENONCONFORMING; }
+    double e[3] = {0, 0, 0};
+    e[k] = 1.0;
+    for (int a : hi) {
+      int hit = -1, nh = 0;
+      for (int b : lo)
+        if (close(a, b, e)) { hit = b; ++nh; }
+      if (nh != 1) { set_error("tile face xi_%d=1: control point %d has %d partners on xi_%d=0", k, a, nh, k); return IGA_ENONCONFORMING; }
+      inter[k].push_back({a, hit});
+    }
+  }
+  const int64_t nl = h.n_local_ctrl, nt = h.n_tiles;
+  if (nt * nl >= (int64_t(1) << 31)) { set_error("n_tiles * n_local_ctrl exceeds int32"); return IGA_ELIMIT; }
+  UF uf(nt * nl);
+  int64_t stride[3] = {1, h.mel[0], (int64_t)h.mel[0] * h.mel[1]};
+  for (int64_t t = 0; t < nt; ++t) {
+    for (auto &pr : intra) uf.unite(t * nl + pr.first, t * nl + pr.second);
+    int64_t tk[3] = {t % h.mel[0], (t / h.mel[0]) % h.mel[1], t / stride[2]};
+    for (int k = 0; k < d; ++k)
+      if (tk[k] < h.mel[k] - 1)
+        for (auto &pr : inter[k]) uf.unite(t * nl + pr.first, (t + stride[k]) * nl + pr.second);
+  }
+  h.node_map.assign(nt * nl, -1);
+  {
+    std::vector<int32_t> id(nt * nl, -1);
+    int64_t next = 0;
+    for (int64_t f = 0; f < nt * nl; ++f) {
+      int64_t r = uf.find(f);
+      if (id[r] < 0) id[r] = (int32_t)next++;
+      h.node_map[f] = id[r];
+    }
+    h.n_nodes = next;
+  }
+  h.n_dof = h.n_nodes * d;
+  for (int64_t t = 0; t < nt; ++t)
+    for (int pi = 0; pi < n_patches; ++pi) {
+      const PatchInfo &P = h.patches[pi];
+      std::vector<int32_t> ids(h.node_map.begin() + t * nl + P.ctrl_off, h.node_map.begin() + t * nl + P.ctrl_off + P.n_ctrl);
+      std::sort(ids.begin(), ids.end());
+      for (size_t i = 1; i < ids.size(); ++i)
+        if (ids[i] == ids[i - 1]) { set_error("tile %lld patch %d: two control points merged", (long long)t, pi); return IGA_ENONCONFORMING; }
+    }
+
+  // ---- gather lists + pattern (R9) ----------------------------------------------
+  h.row_bits = ceil_log2(std::max<int64_t>(h.M, 2));
+  if (((nt - 1) << (h.row_bits + 1)) >> 32) { set_error("packed (tile,row) does not fit 32 bits"); return IGA_ELIMIT; }
+  const int64_t nn = h.n_nodes;
+  std::vector<int64_t> cnt(nn + 1, 0);
+  std::vector<std::atomic<int64_t>> acnt(nn);
+  for (auto &a : acnt) a.store(0, std::memory_order_relaxed);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < nt; ++t)
+    for (int64_t r = 0; r < h.M; ++r) {
+      int32_t I = h.node_map[t * nl + h.pairA[r]], J = h.node_map[t * nl + h.pairB[r]];
+      acnt[I].fetch_add(1, std::memory_order_relaxed);
+      if (I != J) acnt[J].fetch_add(1, std::memory_order_relaxed);
+    }
+  for (int64_t i = 0; i < nn; ++i) cnt[i + 1] = cnt[i] + acnt[i].load(std::memory_order_relaxed);
+  h.n_contrib = cnt[nn];
+  std::vector<uint64_t> keys(h.n_contrib);
+  for (int64_t i = 0; i < nn; ++i) acnt[i].store(cnt[i], std::memory_order_relaxed);
+  const int rb = h.row_bits;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < nt; ++t)
+    for (int64_t r = 0; r < h.M; ++r) {
+      int32_t I = h.node_map[t * nl + h.pairA[r]], J = h.node_map[t * nl + h.pairB[r]];
+      uint64_t pk = ((uint64_t)t << (rb + 1)) | ((uint64_t)r << 1);
+      keys[acnt[I].fetch_add(1, std::memory_order_relaxed)] = ((uint64_t)J << 32) | pk;
+      if (I != J) keys[acnt[J].fetch_add(1, std::memory_order_relaxed)] = ((uint64_t)I << 32) | pk | 1u;
+    }
+  std::vector<int64_t> nnzb(nn + 1, 0);
+  int bad_cnt = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : bad_cnt)
+  for (int64_t i = 0; i < nn; ++i) {
+    std::sort(keys.begin() + cnt[i], keys.begin() + cnt[i + 1]);
+    int64_t nb = 0, run = 0;
+    for (int64_t k = cnt[i]; k < cnt[i + 1]; ++k) {
+      if (k == cnt[i] || (keys[k] >> 32) != (keys[k - 1] >> 32)) { ++nb; run = 0; }
+      if (++run > 255) ++bad_cnt;
+    }
+    nnzb[i + 1] = nb;
+  }
+  if (bad_cnt) { set_error("a block has more than 255 contributions"); return IGA_ELIMIT; }
+  h.brow_ptr.assign(nn + 1, 0);
+  for (int64_t i = 0; i < nn; ++i) h.brow_ptr[i + 1] = h.brow_ptr[i] + nnzb[i + 1];
+  h.n_blocks = h.brow_ptr[nn];
+  h.nnz = h.n_blocks * d * d;
+  h.bcol.assign(h.n_blocks, 0);
+  std::vector<uint8_t> bcnt(h.n_blocks, 0);
+  std::vector<uint32_t> contrib(h.n_contrib);
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t i = 0; i < nn; ++i) {
+    int64_t b = h.brow_ptr[i] - 1;
+    for (int64_t k = cnt[i]; k < cnt[i + 1]; ++k) {
+      if (k == cnt[i] || (keys[k] >> 32) != (keys[k - 1] >> 32)) {
+        ++b;
+        h.bcol[b] = (int32_t)(keys[k] >> 32);
+      }
+      bcnt[b]++;
+      contrib[k] = (uint32_t)(keys[k] & 0xffffffffu);
+    }
+  }
+  keys.clear();
+  keys.shrink_to_fit();
+
+  h.bcnt = std::move(bcnt);
+  h.contrib = std::move(contrib);
+  h.cstart = std::move(cnt);
+
+  // ---- interpolation operator Π1 = V1^{-1} (R1) --------------------------------
+  double w[IGA_MAXQ + 1], V[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
+  gauss_legendre01(q + 1, h.interp_x, w);
+  for (int m = 0; m <= q; ++m)
+    for (int k = 0; k <= q; ++k)
+      V[m * (q + 1) + k] = binom(q, k) * std::pow(h.interp_x[m], k) * std::pow(1.0 - h.interp_x[m], q - k);
+  if (!invert(q + 1, V, h.Pi1)) { set_error("singular interpolation matrix"); return IGA_EINVAL; }
+  return IGA_OK;
+}
+
+}  // namespace iga

@@ -1,0 +1,509 @@
+// iga_api.cu — the C ABI of libiga (include/iga.h): handle lifecycle, host/device
+// pointer staging, the kernel sequence of each entry point, profiling events and
+// the device degeneracy flag.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include "internal.h"
+
+namespace iga {
+const char *get_error();
+
+Handle::~Handle() {
+  void *bufs[] = {d_table, d_tableT, d_coef, d_local, d_W, d_gpart, d_node_map, d_pairA, d_pairB, d_row_ptr,
+                  d_col_idx, d_brow_ptr, d_bcol, d_bcnt, d_cstart, d_contrib, d_mknots, d_mspan, d_flag,
+                  d_stage_ctrl, d_stage_young, d_stage_u, d_stage_v, d_stage_out};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  for (auto e : ev_pool) cudaEventDestroy(e);
+}
+
+static std::mutex g_build_mutex;   // K1 uses __constant__ patch descriptors
+
+static bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+#define CU(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t _e = (x);                                                                \
+    if (_e != cudaSuccess) {                                                             \
+      set_error("CUDA error %s at %s:%d (%s)", cudaGetErrorString(_e), __FILE__, __LINE__, #x); \
+      return IGA_ECUDA;                                                                  \
+    }                                                                                    \
+  } while (0)
+
+// Staging of [any] pointers: device pointers pass through; host pointers are copied.
+struct Stager {
+  Handle &h;
+  cudaStream_t s;
+  std::vector<std::pair<double *, const double *>> pending_out;   // (device, host) with bytes
+  std::vector<size_t> pending_bytes;
+  std::vector<void *> temps;
+  Stager(Handle &hh, cudaStream_t ss) : h(hh), s(ss) {}
+  ~Stager() {
+    for (void *t : temps) cudaFreeAsync(t, s);
+  }
+  bool in(const double *p, size_t n, const double **out) {
+    if (!p || is_device_ptr(p)) { *out = p; return true; }
+    double *d = nullptr;
+    if (cudaMallocAsync((void **)&d, std::max<size_t>(n, 1) * 8, s) != cudaSuccess) return false;
+    temps.push_back(d);
+    if (cudaMemcpyAsync(d, p, n * 8, cudaMemcpyHostToDevice, s) != cudaSuccess) return false;
+    *out = d;
+    return true;
+  }
+  bool out(double *p, size_t n, double **dev) {
+    if (!p || is_device_ptr(p)) { *dev = p; return true; }
+    double *d = nullptr;
+    if (cudaMallocAsync((void **)&d, std::max<size_t>(n, 1) * 8, s) != cudaSuccess) return false;
+    temps.push_back(d);
+    pending_out.push_back({d, p});
+    pending_bytes.push_back(n * 8);
+    *dev = d;
+    return true;
+  }
+  bool flush() {
+    for (size_t i = 0; i < pending_out.size(); ++i)
+      if (cudaMemcpyAsync((void *)pending_out[i].second, pending_out[i].first, pending_bytes[i], cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return false;
+    return true;
+  }
+};
+
+// profiling helper: record event pairs around launches
+struct Prof {
+  Handle &h;
+  cudaStream_t s;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  size_t next = 0;
+  Prof(Handle &hh, cudaStream_t ss) : h(hh), s(ss) {}
+  cudaEvent_t ev() {
+    if (next >= h.ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      h.ev_pool.push_back(e);
+    }
+    return h.ev_pool[next++];
+  }
+  int begin(int slot) {
+    if (!h.profiling) return -1;
+    cudaEvent_t a = ev(), b = ev();
+    cudaEventRecord(a, s);
+    marks.push_back({slot, {a, b}});
+    return (int)marks.size() - 1;
+  }
+  void end(int id) {
+    if (id >= 0) cudaEventRecord(marks[id].second.second, s);
+  }
+  void collect() {
+    for (auto &m : marks) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, m.second.first, m.second.second);
+      h.prof_ms[m.first] += ms;
+      h.prof_launches[m.first] += 1;
+    }
+  }
+};
+
+static iga_status check_flag(Handle &h, cudaStream_t s) {
+  int f[3];
+  CU(cudaMemcpyAsync(f, h.d_flag, sizeof(f), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (f[0] == 1) {
+    set_error("degenerate tile Jacobian (det J_T <= 0) in patch %d at quadrature point %d", f[1], f[2]);
+    return IGA_EDEGENERATE;
+  }
+  if (f[0] == 2) {
+    set_error("degenerate macro element: det grad F <= 0 in tile %d at interpolation node %d", f[1], f[2]);
+    return IGA_EDEGENERATE;
+  }
+  return IGA_OK;
+}
+
+static iga_status check_material(const Handle &h, const double *young, double nu) {
+  if (!young) { set_error("young is NULL"); return IGA_EINVAL; }
+  if (!(nu > -1.0 && nu < 0.5)) { set_error("nu=%g outside (-1, 0.5)", nu); return IGA_EINVAL; }
+  return IGA_OK;
+}
+
+}  // namespace iga
+
+using namespace iga;
+
+struct iga_handle {
+  Handle h;
+};
+
+extern "C" {
+
+const char *iga_last_error(void) { return get_error(); }
+const char *iga_version(void) { return "libiga 0.1 (sm_100a, FP64 DMMA)"; }
+
+iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
+                            int32_t n_interfaces, const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
+                            void *stream, iga_handle **out) {
+  if (!out) { set_error("out is NULL"); return IGA_EINVAL; }
+  *out = nullptr;
+  if (n_patches > 64) { set_error("at most 64 tile patches"); return IGA_EINVAL; }
+  std::lock_guard<std::mutex> lock(g_build_mutex);
+  iga_handle *H = new (std::nothrow) iga_handle();
+  if (!H) { set_error("out of host memory"); return IGA_ENOMEM; }
+  Handle &h = H->h;
+  cudaStream_t s = (cudaStream_t)stream;
+  iga_status st;
+  try {
+    st = build_host(h, tile_patches, n_patches, interfaces, n_interfaces, macro_topology, q, n_gauss);
+  } catch (std::bad_alloc &) {
+    set_error("out of host memory during the host build");
+    st = IGA_ENOMEM;
+  }
+  if (st != IGA_OK) { delete H; return st; }
+  auto fail = [&](iga_status e) { delete H; return e; };
+#define CUB(x)                                                                                   \
+  do {                                                                                           \
+    cudaError_t _e = (x);                                                                        \
+    if (_e != cudaSuccess) {                                                                     \
+      set_error("CUDA error %s at %s:%d (%s)", cudaGetErrorString(_e), __FILE__, __LINE__, #x);  \
+      return fail(_e == cudaErrorMemoryAllocation ? IGA_ENOMEM : IGA_ECUDA);                     \
+    }                                                                                            \
+  } while (0)
+  st = upload_topology(h);
+  if (st != IGA_OK) return fail(st);
+  h.on_device = true;
+  const int d = h.d;
+  const int64_t N = h.n_tiles * d * d;
+  const int64_t ldT = (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK;
+  CUB(cudaMalloc((void **)&h.d_flag, 4 * sizeof(int)));
+  CUB(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  CUB(cudaMalloc((void **)&h.d_table, sizeof(double) * h.M * h.kstride));
+  CUB(cudaMemsetAsync(h.d_table, 0, sizeof(double) * h.M * h.kstride, s));
+  CUB(cudaMalloc((void **)&h.d_tableT, sizeof(double) * h.kstride * ldT));
+  CUB(cudaMemsetAsync(h.d_tableT, 0, sizeof(double) * h.kstride * ldT, s));
+  CUB(cudaMalloc((void **)&h.d_coef, sizeof(double) * N * h.kstride));
+  CUB(cudaMemsetAsync(h.d_coef, 0, sizeof(double) * N * h.kstride, s));
+  CUB(cudaMalloc((void **)&h.d_local, sizeof(double) * h.M * N));
+  CUB(cudaMalloc((void **)&h.d_W, sizeof(double) * N * h.kstride));
+  int nact_m = 1;
+  for (int k = 0; k < d; ++k) nact_m *= h.pm[k] + 1;
+  CUB(cudaMalloc((void **)&h.d_gpart, sizeof(double) * h.n_tiles * nact_m * d));
+  CUB(cudaMalloc((void **)&h.d_row_ptr, sizeof(int64_t) * (h.n_dof + 1)));
+  CUB(cudaMalloc((void **)&h.d_col_idx, sizeof(int32_t) * std::max<int64_t>(h.nnz, 1)));
+  // macro knots / element spans
+  std::vector<double> mk;
+  std::vector<int> ms;
+  for (int k = 0; k < d; ++k) {
+    mk.insert(mk.end(), h.mknots[k].begin(), h.mknots[k].end());
+    ms.insert(ms.end(), h.mel_span[k].begin(), h.mel_span[k].end());
+  }
+  CUB(cudaMalloc((void **)&h.d_mknots, sizeof(double) * mk.size()));
+  CUB(cudaMemcpy(h.d_mknots, mk.data(), sizeof(double) * mk.size(), cudaMemcpyHostToDevice));
+  CUB(cudaMalloc((void **)&h.d_mspan, sizeof(int) * ms.size()));
+  CUB(cudaMemcpy(h.d_mspan, ms.data(), sizeof(int) * ms.size(), cudaMemcpyHostToDevice));
+  // tile data for K1
+  std::vector<DevPatch> dp(n_patches);
+  std::vector<double> tctrl, tknots;
+  std::vector<int> tel;
+  int pt_off = 0, ngd = 1;
+  for (int k = 0; k < d; ++k) ngd *= h.n_g;
+  for (int pi = 0; pi < n_patches; ++pi) {
+    PatchInfo &P = h.patches[pi];
+    DevPatch &D = dp[pi];
+    memset(&D, 0, sizeof(D));
+    D.deg = h.p;
+    D.ctrl_off = P.ctrl_off;
+    for (int k = 0; k < 3; ++k) {
+      D.n[k] = P.n[k];
+      D.n_span[k] = P.n_span[k];
+      D.knot_off[k] = (int)tknots.size();
+      D.elspan_off[k] = (int)tel.size();
+      if (k < d) {
+        tknots.insert(tknots.end(), P.knots[k].begin(), P.knots[k].end());
+        tel.insert(tel.end(), P.el_span[k].begin(), P.el_span[k].end());
+      }
+    }
+    D.n_spans = P.n_spans;
+    D.pt_off = pt_off;
+    P.pt_off = pt_off;
+    pt_off += P.n_spans * ngd;
+    tctrl.insert(tctrl.end(), P.ctrl.begin(), P.ctrl.end());
+  }
+  double *d_tctrl, *d_tknots;
+  int *d_tel;
+  CUB(cudaMalloc((void **)&d_tctrl, sizeof(double) * tctrl.size()));
+  CUB(cudaMemcpy(d_tctrl, tctrl.data(), sizeof(double) * tctrl.size(), cudaMemcpyHostToDevice));
+  CUB(cudaMalloc((void **)&d_tknots, sizeof(double) * tknots.size()));
+  CUB(cudaMemcpy(d_tknots, tknots.data(), sizeof(double) * tknots.size(), cudaMemcpyHostToDevice));
+  CUB(cudaMalloc((void **)&d_tel, sizeof(int) * tel.size()));
+  CUB(cudaMemcpy(d_tel, tel.data(), sizeof(int) * tel.size(), cudaMemcpyHostToDevice));
+  double gx[16], gw[16];
+  gauss_legendre01(h.n_g, gx, gw);
+  CUB(launch_tables(h, dp.data(), n_patches, d_tctrl, d_tknots, d_tel, gx, gw, pt_off, s));
+  CUB(launch_expand_pattern(h, s));
+  CUB(cudaStreamSynchronize(s));
+  cudaFree(d_tctrl);
+  cudaFree(d_tknots);
+  cudaFree(d_tel);
+  st = check_flag(h, s);
+  if (st != IGA_OK) return fail(st);
+#undef CUB
+  *out = H;
+  return IGA_OK;
+}
+
+iga_status iga_build_topology(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
+                              int32_t n_interfaces, const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
+                              iga_handle **out) {
+  if (!out) { set_error("out is NULL"); return IGA_EINVAL; }
+  *out = nullptr;
+  iga_handle *H = new (std::nothrow) iga_handle();
+  if (!H) { set_error("out of host memory"); return IGA_ENOMEM; }
+  iga_status st;
+  try {
+    st = build_host(H->h, tile_patches, n_patches, interfaces, n_interfaces, macro_topology, q, n_gauss);
+  } catch (std::bad_alloc &) {
+    set_error("out of host memory during the host build");
+    st = IGA_ENOMEM;
+  }
+  if (st != IGA_OK) { delete H; return st; }
+  *out = H;
+  return IGA_OK;
+}
+
+void iga_free(iga_handle *H) { delete H; }
+
+iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
+  if (!H || !o) { set_error("NULL argument"); return IGA_EINVAL; }
+  const Handle &h = H->h;
+  memset(o, 0, sizeof(*o));
+  o->dim = h.d;
+  o->q = h.q;
+  o->n_pi = h.npi;
+  o->n_k = h.nk;
+  o->k_stride = h.kstride;
+  o->n_patches = h.n_patches;
+  o->n_gauss = h.n_g;
+  o->n_tiles = h.n_tiles;
+  o->n_local_rows = h.M;
+  o->n_macro_cp = h.n_cp;
+  o->n_nodes = h.n_nodes;
+  o->n_dof = h.n_dof;
+  o->nnz = h.nnz;
+  o->n_blocks = h.n_blocks;
+  o->n_contrib = h.n_contrib;
+  return IGA_OK;
+}
+
+static iga_status run_interp(Handle &h, Stager &sg, Prof &pf, const double *ctrl, const double *young, int ypt,
+                             double nu, cudaStream_t s) {
+  const double *dctrl, *dyoung;
+  if (!sg.in(ctrl, (size_t)h.n_cp * h.d, &dctrl) || !sg.in(young, ypt ? (size_t)h.n_tiles : 1, &dyoung)) {
+    set_error("staging of host inputs failed");
+    return IGA_ENOMEM;
+  }
+  int id = pf.begin(0);
+  CU(launch_interpolate(h, dctrl, dyoung, ypt, nu, h.d_coef, s));
+  pf.end(id);
+  return IGA_OK;
+}
+
+iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const double *young, int32_t young_per_tile,
+                        double nu, double *csr_values, double *local_values, void *stream) {
+  if (!Hc || !macro_ctrl || !csr_values) { set_error("NULL argument"); return IGA_EINVAL; }
+  Handle &h = const_cast<iga_handle *>(Hc)->h;
+  if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
+  iga_status st = check_material(h, young, nu);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  Stager sg(h, s);
+  Prof pf(h, s);
+  int idst = pf.begin(6);
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  const double *dctrl, *dyoung;
+  if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles : 1, &dyoung)) {
+    set_error("staging of host inputs failed");
+    return IGA_ENOMEM;
+  }
+  double *dvals, *dlocal_out;
+  if (!sg.out(csr_values, (size_t)h.nnz, &dvals) ||
+      !sg.out(local_values, (size_t)(h.M * h.n_tiles * h.d * h.d), &dlocal_out)) {
+    set_error("staging of host outputs failed");
+    return IGA_ENOMEM;
+  }
+  pf.end(idst);
+  int id = pf.begin(0);
+  CU(launch_interpolate(h, dctrl, dyoung, young_per_tile, nu, h.d_coef, s));
+  pf.end(id);
+  const int64_t N = h.n_tiles * h.d * h.d;
+  double *loc = dlocal_out ? dlocal_out : h.d_local;
+  id = pf.begin(1);
+  CU(launch_contraction(h, h.d_table, h.d_coef, loc, h.M, N, h.nk, h.kstride, s));
+  pf.end(id);
+  id = pf.begin(2);
+  CU(launch_scatter(h, loc, dvals, s));
+  pf.end(id);
+  idst = pf.begin(6);
+  if (!sg.flush()) { set_error("D2H copy of outputs failed"); return IGA_ECUDA; }
+  pf.end(idst);
+  st = check_flag(h, s);
+  pf.collect();
+  return st;
+}
+
+iga_status iga_interpolate(const iga_handle *Hc, const double *macro_ctrl, const double *young, int32_t young_per_tile,
+                           double nu, double *coef, void *stream) {
+  if (!Hc || !macro_ctrl || !coef) { set_error("NULL argument"); return IGA_EINVAL; }
+  Handle &h = const_cast<iga_handle *>(Hc)->h;
+  if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
+  iga_status st = check_material(h, young, nu);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  Stager sg(h, s);
+  Prof pf(h, s);
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  st = run_interp(h, sg, pf, macro_ctrl, young, young_per_tile, nu, s);
+  if (st) return st;
+  CU(cudaMemcpyAsync(coef, h.d_coef, sizeof(double) * h.n_tiles * h.d * h.d * h.kstride, cudaMemcpyDefault, s));
+  st = check_flag(h, s);
+  pf.collect();
+  return st;
+}
+
+iga_status iga_sensitivity(const iga_handle *Hc, const double *macro_ctrl, const double *young,
+                           int32_t young_per_tile, double nu, const double *u, const double *v, double *grad,
+                           void *stream) {
+  if (!Hc || !macro_ctrl || !u || !v || !grad) { set_error("NULL argument"); return IGA_EINVAL; }
+  Handle &h = const_cast<iga_handle *>(Hc)->h;
+  if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
+  iga_status st = check_material(h, young, nu);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  Stager sg(h, s);
+  Prof pf(h, s);
+  int idst = pf.begin(6);
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  const double *dctrl, *dyoung, *du, *dv;
+  double *dgrad;
+  if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles : 1, &dyoung) || !sg.in(u, (size_t)h.n_dof, &du) ||
+      !sg.in(v, (size_t)h.n_dof, &dv) || !sg.out(grad, (size_t)(h.n_cp * h.d), &dgrad)) {
+    set_error("staging failed");
+    return IGA_ENOMEM;
+  }
+  pf.end(idst);
+  int id = pf.begin(3);
+  CU(launch_sens_W(h, du, dv, h.d_W, s));
+  pf.end(id);
+  id = pf.begin(4);
+  CU(launch_sens_reverse(h, dctrl, dyoung, young_per_tile, nu, h.d_W, h.d_gpart, s));
+  pf.end(id);
+  id = pf.begin(5);
+  CU(launch_sens_reduce(h, h.d_gpart, dgrad, s));
+  pf.end(id);
+  idst = pf.begin(6);
+  if (!sg.flush()) { set_error("D2H copy failed"); return IGA_ECUDA; }
+  pf.end(idst);
+  st = check_flag(h, s);
+  pf.collect();
+  return st;
+}
+
+iga_status iga_get_pattern(const iga_handle *Hc, int64_t *row_ptr, int32_t *col_idx) {
+  if (!Hc) { set_error("NULL handle"); return IGA_EINVAL; }
+  const Handle &h = Hc->h;
+  if (h.on_device) {
+    if (row_ptr) CU(cudaMemcpy(row_ptr, h.d_row_ptr, sizeof(int64_t) * (h.n_dof + 1), cudaMemcpyDefault));
+    if (col_idx) CU(cudaMemcpy(col_idx, h.d_col_idx, sizeof(int32_t) * h.nnz, cudaMemcpyDefault));
+    return IGA_OK;
+  }
+  // topology-only handle: expand the block CSR on the host (host pointers only)
+  const int d = h.d;
+  for (int64_t I = 0; I < h.n_nodes; ++I) {
+    int64_t b0 = h.brow_ptr[I], nb = h.brow_ptr[I + 1] - b0;
+    for (int a = 0; a < d; ++a) {
+      int64_t base = (int64_t)d * d * b0 + a * d * nb;
+      if (row_ptr) row_ptr[I * d + a] = base;
+      if (col_idx)
+        for (int64_t j = 0; j < nb; ++j)
+          for (int b = 0; b < d; ++b) col_idx[base + d * j + b] = h.bcol[b0 + j] * d + b;
+    }
+  }
+  if (row_ptr) row_ptr[h.n_dof] = h.nnz;
+  return IGA_OK;
+}
+
+iga_status iga_get_block_map(const iga_handle *Hc, int64_t t_begin, int64_t t_end, int64_t *out) {
+  if (!Hc || !out) { set_error("NULL argument"); return IGA_EINVAL; }
+  const Handle &h = Hc->h;
+  if (t_begin < 0 || t_end > h.n_tiles || t_begin > t_end) { set_error("bad tile range"); return IGA_EINVAL; }
+  const int d = h.d;
+  const int64_t nl = h.n_local_ctrl;
+  auto pos = [&](int64_t I, int64_t J) -> int64_t {
+    const int32_t *b = h.bcol.data() + h.brow_ptr[I], *e = h.bcol.data() + h.brow_ptr[I + 1];
+    const int32_t *f = std::lower_bound(b, e, (int32_t)J);
+    return (int64_t)d * d * h.brow_ptr[I] + (int64_t)d * (f - b);
+  };
+#pragma omp parallel for schedule(static)
+  for (int64_t t = t_begin; t < t_end; ++t)
+    for (int64_t r = 0; r < h.M; ++r) {
+      int64_t I = h.node_map[t * nl + h.pairA[r]], J = h.node_map[t * nl + h.pairB[r]];
+      int64_t o = ((t - t_begin) * h.M + r) * 2;
+      out[o] = pos(I, J);
+      out[o + 1] = pos(J, I);
+    }
+  return IGA_OK;
+}
+
+iga_status iga_get_node_map(const iga_handle *Hc, int32_t *out) {
+  if (!Hc || !out) { set_error("NULL argument"); return IGA_EINVAL; }
+  memcpy(out, Hc->h.node_map.data(), Hc->h.node_map.size() * sizeof(int32_t));
+  return IGA_OK;
+}
+
+iga_status iga_get_tables(const iga_handle *Hc, double *out) {
+  if (!Hc || !out) { set_error("NULL argument"); return IGA_EINVAL; }
+  const Handle &h = Hc->h;
+  if (!h.on_device) { set_error("topology-only handle has no tables"); return IGA_EINVAL; }
+  CU(cudaMemcpy2D(out, sizeof(double) * h.nk, h.d_table, sizeof(double) * h.kstride, sizeof(double) * h.nk, h.M,
+                  cudaMemcpyDefault));
+  return IGA_OK;
+}
+
+iga_status iga_get_pairs(const iga_handle *Hc, int32_t *out) {
+  if (!Hc || !out) { set_error("NULL argument"); return IGA_EINVAL; }
+  const Handle &h = Hc->h;
+  for (int64_t r = 0; r < h.M; ++r) {
+    int pa = h.pairA[r], pb = h.pairB[r];
+    int pi = 0;
+    while (pi + 1 < h.n_patches && pa >= h.patches[pi + 1].ctrl_off) ++pi;
+    out[2 * r] = pa - h.patches[pi].ctrl_off;
+    out[2 * r + 1] = pb - h.patches[pi].ctrl_off;
+  }
+  return IGA_OK;
+}
+
+iga_status iga_set_profiling(iga_handle *H, int32_t enable) {
+  if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
+  H->h.profiling = enable != 0;
+  if (enable)
+    for (int i = 0; i < 8; ++i) { H->h.prof_ms[i] = 0; H->h.prof_launches[i] = 0; }
+  return IGA_OK;
+}
+
+iga_status iga_get_kernel_times(const iga_handle *H, double *ms_out, int64_t *launches_out) {
+  if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
+  for (int i = 0; i < 8; ++i) {
+    if (ms_out) ms_out[i] = H->h.prof_ms[i];
+    if (launches_out) launches_out[i] = H->h.prof_launches[i];
+  }
+  return IGA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle, element by element on the
+same seeded inputs (BASELINE.json north_star tolerances: pattern and maps bit-exact,
+≤ 1e-12 relative Frobenius per element matrix, ≤ 1e-11 on K's values; tables
+≤ 1e-13, coefficients ≤ 1e-12; sensitivity ≤ 1e-11 relative 2-norm — DESIGN.md §5)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+TOL_TABLE = 1e-13
+TOL_COEF = 1e-12   # κ(V1)^d rounding amplification: 6.48^3 ≈ 272 at q=3
+TOL_ELEM = 1e-12
+TOL_K = 1e-11
+TOL_SENS = 1e-11
+
+_gpu = {}
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def gpu_case(c, **kw):
+    """Build the Assembler and run assemble (+ local values) for config c (cached)."""
+    key = (c, tuple(sorted(kw.items())))
+    if key in _gpu:
+        return _gpu[key]
+    from paper_2107_09568_b200 import Assembler
+    from synth import make_config
+    prob = make_config(c, **kw)
+    A = Assembler(prob)
+    s = A.sizes
+    dev = torch.device("cuda:0")
+    ctrl = torch.tensor(prob.macro.ctrl, dtype=torch.float64, device=dev)
+    young = torch.tensor(prob.young, dtype=torch.float64, device=dev)
+    vals = torch.empty(s.nnz, dtype=torch.float64, device=dev)
+    keep_local = s.n_local_rows * s.n_tiles * prob.d ** 2 < 3e9
+    local = torch.empty(s.n_local_rows * s.n_tiles * prob.d ** 2, dtype=torch.float64, device=dev) if keep_local else None
+    A.assemble(ctrl, young, prob.nu, vals, local)
+    torch.cuda.synchronize()
+    out = dict(prob=prob, A=A, ctrl=ctrl, young=young, vals=vals, local=local)
+    _gpu[key] = out
+    return out
+
+
+def local_np(g, tiles):
+    """GPU element matrices of the given tiles: (len, n_rows, d, d)."""
+    prob, s = g["prob"], g["A"].sizes
+    d = prob.d
+    L = g["local"].view(s.n_local_rows, s.n_tiles, d, d)
+    return L[:, torch.as_tensor(tiles, device=L.device)].permute(1, 0, 2, 3).cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_tables_parity(c, oracle_problem):
+    g = gpu_case(c)
+    if c == 4:
+        from synth import make_config
+        from oracle.tables import lookup_table
+        prob = make_config(4)
+        T0, pairs0 = lookup_table(prob.tile[0], prob.q, prob.n_gauss)
+        Tg = g["A"].tables()[:len(pairs0)]
+        assert np.array_equal(g["A"].pairs()[:len(pairs0)], pairs0)
+        assert rel(Tg, T0) < TOL_TABLE
+        return
+    ob = oracle_problem(c)
+    Tg = g["A"].tables()
+    assert np.array_equal(g["A"].pairs(), np.concatenate(ob["tabs"].pairs))
+    off = 0
+    for Tp, _ in ob["tabs"].per_patch:
+        assert rel(Tg[off:off + len(Tp)], Tp) < TOL_TABLE
+        off += len(Tp)
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_interpolation_parity(c):
+    from oracle import macro as M
+    g = gpu_case(c)
+    prob, A = g["prob"], g["A"]
+    s = A.sizes
+    d = prob.d
+    coef = torch.zeros(s.n_tiles * d * d * s.k_stride, dtype=torch.float64, device="cuda")
+    A.interpolate(g["ctrl"], g["young"], prob.nu, coef)
+    cg = coef.view(s.n_tiles, d * d, s.k_stride)[:, :, :s.n_k].cpu().numpy()
+    tiles = range(prob.n_tiles) if prob.n_tiles <= 64 else np.random.default_rng(c).choice(prob.n_tiles, 24, replace=False)
+    for t in tiles:
+        ref = M.tile_coefficients(prob, prob.macro.ctrl, int(t))            # [C, i, j, a, b]
+        refm = np.transpose(ref, (3, 4, 1, 2, 0)).reshape(d * d, -1)          # [(a,b)][(i,j,C)]
+        assert rel(cg[t], refm) < TOL_COEF, t
+    # padding columns stay zero
+    assert torch.count_nonzero(coef.view(s.n_tiles, d * d, s.k_stride)[:, :, s.n_k:]) == 0
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_element_matrix_parity(c, oracle_problem):
+    from oracle import assemble as As
+    g = gpu_case(c)
+    prob = g["prob"]
+    if c == 4:
+        from oracle.assemble import Tables
+        tabs = Tables(prob)
+    else:
+        tabs = oracle_problem(c)["tabs"]
+    tiles = list(range(prob.n_tiles)) if prob.n_tiles <= 64 else \
+        sorted(np.random.default_rng(10 + c).choice(prob.n_tiles, 12, replace=False).tolist() + [0, prob.n_tiles - 1])
+    ref = As.local_lookup(prob, tabs, prob.macro.ctrl, tiles)
+    got = local_np(g, tiles)
+    for n, t in enumerate(tiles):
+        assert rel(got[n], ref[n]) < TOL_ELEM, (t, rel(got[n], ref[n]))
+
+
+@pytest.mark.parametrize("c", [1, 2, 3])
+def test_pattern_bit_exact(c, oracle_problem):
+    g = gpu_case(c)
+    ob = oracle_problem(c)
+    s = g["A"].sizes
+    rp = torch.empty(s.n_dof + 1, dtype=torch.int64, device="cuda")
+    ci = torch.empty(s.nnz, dtype=torch.int32, device="cuda")
+    g["A"].pattern(rp, ci)
+    assert np.array_equal(rp.cpu().numpy(), ob["pattern"].row_ptr)
+    if c < 3:
+        assert np.array_equal(ci.cpu().numpy(), ob["pattern"].col_idx())
+    else:   # cfg3: compare through the block structure (179M entries)
+        pt = ob["pattern"]
+        cin = ci.cpu().numpy()
+        d = 3
+        first = cin[pt.row_ptr[:-1:d][:len(pt.nnzb)]]   # first column of each node row
+        assert np.array_equal(first, pt.bcol[pt.brow_ptr[:-1]] * d)
+        rng = np.random.default_rng(3)
+        for I in rng.choice(ob["dm"].n_nodes, 200, replace=False):
+            cols = pt.bcol[pt.brow_ptr[I]:pt.brow_ptr[I + 1]]
+            sc = (cols[:, None] * d + np.arange(d)).ravel()
+            for a in range(d):
+                r = I * d + a
+                assert np.array_equal(cin[pt.row_ptr[r]:pt.row_ptr[r + 1]], sc)
+    bm = g["A"].block_map(0, min(prob_tiles(g), 8))
+    assert np.array_equal(bm, ob["pattern"].block_map()[:len(bm)])
+    nl = sum(t.n_ctrl for t in g["prob"].tile)
+    assert np.array_equal(g["A"].node_map_for(nl), ob["dm"].node)
+
+
+def prob_tiles(g):
+    return g["prob"].n_tiles
+
+
+@pytest.mark.parametrize("c", [1, 2, 3])
+def test_csr_values_parity(c, oracle_problem):
+    from oracle import assemble as As
+    g = gpu_case(c)
+    ob = oracle_problem(c)
+    vals_ref, _ = As.assemble_lookup(ob["prob"], ob["tabs"], ob["pattern"])
+    got = g["vals"].cpu().numpy()
+    assert rel(got, vals_ref) < TOL_K
+
+
+@pytest.mark.parametrize("c", [1, 2, 3])
+def test_K_bitwise_symmetric_and_deterministic(c):
+    g = gpu_case(c)
+    A, prob = g["A"], g["prob"]
+    s = A.sizes
+    rp = torch.empty(s.n_dof + 1, dtype=torch.int64, device="cuda")
+    ci = torch.empty(s.nnz, dtype=torch.int32, device="cuda")
+    A.pattern(rp, ci)
+    K = torch.sparse_csr_tensor(rp, ci.to(torch.int64), g["vals"], size=(s.n_dof, s.n_dof))
+    Kt = K.to_sparse_coo().t().coalesce()
+    Kc = K.to_sparse_coo().coalesce()
+    assert torch.equal(Kt.indices(), Kc.indices()) and torch.equal(Kt.values(), Kc.values())
+    vals2 = torch.empty_like(g["vals"])
+    A.assemble(g["ctrl"], g["young"], prob.nu, vals2)
+    assert torch.equal(vals2, g["vals"])
+    # rigid translations in the kernel (any F)
+    for a in range(prob.d):
+        tr = torch.zeros(s.n_dof, dtype=torch.float64, device="cuda")
+        tr[a::prob.d] = 1.0
+        r = torch.mv(K, tr).abs().max().item()
+        assert r < 1e-12 * g["vals"].abs().max().item() * 10
+
+
+def test_host_pointers_match_device_pointers():
+    """The [any]-pointer contract: host numpy buffers give the same bits (e2e path)."""
+    g = gpu_case(2)
+    prob, A = g["prob"], g["A"]
+    vals_h = np.empty(A.sizes.nnz)
+    A.assemble(np.ascontiguousarray(prob.macro.ctrl), np.ascontiguousarray(prob.young), prob.nu, vals_h)
+    assert np.array_equal(vals_h, g["vals"].cpu().numpy())
+
+
+def test_young_scaling_and_homogeneity_gpu():
+    g = gpu_case(2)
+    prob, A = g["prob"], g["A"]
+    v2 = torch.empty_like(g["vals"])
+    A.assemble(2.0 * g["ctrl"], g["young"], prob.nu, v2)          # K(2P) = 2 K(P) in 3D, bitwise
+    assert torch.equal(v2, 2.0 * g["vals"])
+    A.assemble(g["ctrl"], 3.0 * g["young"], prob.nu, v2)
+    assert torch.allclose(v2, 3.0 * g["vals"], rtol=1e-14, atol=0)
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("c,kw", [(1, {}), (2, dict(n_el=(2, 1, 1))), (2, {})])
+def test_sensitivity_parity(c, kw, oracle_problem):
+    from oracle import sensitivity as S
+    from synth import draw_uv_seeded
+    ob = oracle_problem(c, **kw)
+    g = gpu_case(c, **kw)
+    prob, A = g["prob"], g["A"]
+    u, v = draw_uv_seeded(c, ob["dm"].n_dof)
+    ref = S.sensitivity(ob["prob"], ob["tabs"], ob["pattern"], u, v)
+    grad = torch.empty(A.sizes.n_macro_cp * prob.d, dtype=torch.float64, device="cuda")
+    A.sensitivity(g["ctrl"], g["young"], prob.nu, torch.tensor(u, device="cuda"), torch.tensor(v, device="cuda"), grad)
+    got = grad.cpu().numpy().reshape(-1, prob.d)
+    assert rel(got, ref) < TOL_SENS, rel(got, ref)
+
+
+def test_sensitivity_cfg3_sampled():
+    from oracle.assemble import Tables
+    from oracle.dofmap import DofMap, Pattern
+    from oracle import sensitivity as S
+    from synth import draw_uv_seeded
+    g = gpu_case(3)
+    prob, A = g["prob"], g["A"]
+    u, v = draw_uv_seeded(3, A.sizes.n_dof)
+    grad = torch.empty(A.sizes.n_macro_cp * 3, dtype=torch.float64, device="cuda")
+    A.sensitivity(g["ctrl"], g["young"], prob.nu, torch.tensor(u, device="cuda"), torch.tensor(v, device="cuda"), grad)
+    got = grad.cpu().numpy().reshape(-1, 3)
+    assert np.abs(got.sum(0)).max() < 1e-10 * np.abs(got).max()          # translation invariance
+    dm = DofMap(prob)
+    tabs = Tables(prob)
+    pt = Pattern(prob, dm, tabs.pairs)
+    rng = np.random.default_rng(5)
+    ent = [(int(k), int(a)) for k, a in zip(rng.integers(0, len(got), 6), rng.integers(0, 3, 6))]
+    ref = S.sensitivity(prob, tabs, pt, u, v, entries=ent)
+    for k, a in ent:
+        assert abs(got[k, a] - ref[k, a]) < TOL_SENS * np.abs(got).max() * 10, (k, a)
+
+
+# ---------------------------------------------------------------------------
+def test_degenerate_macro_raises():
+    from paper_2107_09568_b200 import IgaError
+    g = gpu_case(1)
+    prob, A = g["prob"], g["A"]
+    bad = prob.macro.ctrl.copy()
+    bad[7, 0] += 3.0                     # drag an interior point across two elements: folds F
+    vals = torch.empty(A.sizes.nnz, dtype=torch.float64, device="cuda")
+    with pytest.raises(IgaError, match="EDEGENERATE"):
+        A.assemble(torch.tensor(bad, device="cuda"), g["young"], prob.nu, vals)
+    # the handle stays usable afterwards
+    A.assemble(g["ctrl"], g["young"], prob.nu, vals)
+    assert torch.equal(vals, g["vals"])
+
+
+def test_invalid_arguments_raise():
+    from paper_2107_09568_b200 import Assembler, IgaError
+    from synth import make_config
+    g = gpu_case(1)
+    prob, A = g["prob"], g["A"]
+    vals = torch.empty(A.sizes.nnz, dtype=torch.float64, device="cuda")
+    with pytest.raises(IgaError, match="EINVAL"):
+        A.assemble(g["ctrl"], g["young"], 0.5, vals)
+    p2 = make_config(1)
+    p2.tile[0].ctrl[6, 1] += 1e-3
+    with pytest.raises(IgaError, match="ENONCONFORMING"):
+        Assembler(p2)
+    p3 = make_config(1)
+    p3.tile[0].ctrl[14] = p3.tile[0].ctrl[15] + np.array([0.3, 0.0])   # folds the tile
+    with pytest.raises(IgaError, match="EDEGENERATE|EINVAL"):
+        Assembler(p3)
