@@ -1,0 +1,350 @@
+"""bench.py — K formation (+ sensitivity) throughput of libiga on B200.
+
+Workload (default): BASELINE.json configs[4] = cfg5 — cfg3's quarter-annulus macro map
+refined to 32×16×16 elements (8192 tiles) with the 6-strut lattice tile, p = q = 2,
+FP64, plus uᵀ(∂K/∂P)v with seeded N(0,1) u, v.  One step = the whole hot path of
+SURVEY.md §8(a) rows a2-a5: K2 interpolation -> K3 DMMA contraction -> K4 CSR gather
+(iga_assemble) and K5a -> K5b -> K5c (iga_sensitivity).  Row a1 (tables) is offline per
+the paper and reported separately (`offline`).
+
+Timing: W warm-up steps, then K steps bracketed by barrier + cuda synchronize, CUDA
+events on the launching stream, max over ranks.  The working set (CSR values 22.9 GB,
+local values 12 GB) is >> the 126 MB L2, so no explicit flush is needed.
+Per-kernel device times come from libiga's own CUDA events on the same stream
+(iga_set_profiling) over the timed region.
+
+--impl reference: the oracle (oracle/, NumPy FP64) on host cores, on a bounded sample
+of the same workload (cfg5 generator at a reduced macro grid), same metric/unit.
+Multi-GPU (torchrun): every rank forms K and g for its own problem instance (weak
+scaling, no data-path collective); value = all ranks' tiles / max-over-ranks time.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.15      # measured DMMA ceiling, profiles/r01_fp64_ceiling.md
+METRIC = "K formation tiles/s and nnz/s at 1 B200; % of FP64-tensor / HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--no-sensitivity", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend)
+    return rank, world
+
+
+def reduce_max(x, world):
+    """Max over ranks of a float (device timing rule)."""
+    if world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def algorithmic(prob, s, sens):
+    """Algorithmic work per launch."""
+    d = prob.d
+    N = s.n_tiles * d * d
+    gemm = 2.0 * s.n_local_rows * s.n_k * N                       # unpadded K = d² n_pi
+    k2_bytes = 8.0 * (s.n_tiles * s.n_k * d * d + s.n_tiles + s.n_macro_cp * d)
+    k4_bytes = 8.0 * s.n_local_rows * N + 8.0 * s.nnz + 4.0 * s.n_contrib + 1.0 * s.n_blocks + 16.0 * s.n_nodes
+    return dict(k3_flops=gemm, k5a_flops=gemm if sens else 0.0, k2_bytes=k2_bytes, k4_bytes=k4_bytes)
+
+
+def load_traffic():
+    """dram bytes per launch from the committed ncu --set full summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+def cpu_baseline_oracle(n_el=(8, 4, 4), sens=True, repeats=1):
+    """The oracle (NumPy FP64, as it stands) on a bounded sample of the cfg5 workload:
+    the cfg5 generator (same tile, p=q=2) at a reduced macro grid.  Tables, DofMap and
+    pattern are built untimed (offline, as for the GPU).  Timed: K^π (interpolation,
+    table·coefficient product, CSR scatter) + g = uᵀ(∂K^π/∂P)v for every coordinate."""
+    from oracle import assemble as As, sensitivity as S
+    from oracle.dofmap import DofMap, Pattern
+    from synth import make_config, draw_uv_seeded
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        cores = max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    prob = make_config(5, n_el=n_el)
+    dm = DofMap(prob)
+    tabs = As.Tables(prob)
+    pt = Pattern(prob, dm, tabs.pairs)
+    u, v = draw_uv_seeded(5, dm.n_dof)
+    best = None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        As.assemble_lookup(prob, tabs, pt)
+        if sens:
+            S.sensitivity(prob, tabs, pt, u, v)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return prob.n_tiles, best, cores, pt.nnz
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n_el = (4, 2, 2)
+    times = []
+    n_tiles = nnz = cores = None
+    for i in range(args.warmup + args.steps):
+        n_tiles, dt, cores, nnz = cpu_baseline_oracle(n_el=n_el, sens=not args.no_sensitivity)
+        if i >= args.warmup:
+            times.append(dt)
+    t = float(np.mean(times))
+    value = n_tiles / t
+    sample = (f"cfg5 generator at macro grid {n_el} ({n_tiles} tiles, nnz {nnz}): oracle K^pi "
+              f"(interpolation + table product + CSR scatter)" + ("" if args.no_sensitivity else " + full gradient")
+              + "; tables/DofMap/pattern untimed (offline)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg5-sample{n_el}", "n_tiles": n_tiles, "nnz": nnz, "p": 2, "q": 2},
+            "nnz_per_s": nnz / t,
+            "cpu_baseline": {"value": value, "unit": "tiles/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tiles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world):
+    import torch
+    from paper_2107_09568_b200 import Assembler
+    from synth import make_config, draw_uv_seeded
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    sens = not args.no_sensitivity
+    prob = make_config(args.config)
+    t0 = time.perf_counter()
+    A = Assembler(prob)
+    build_s = time.perf_counter() - t0
+    s = A.sizes
+    d = prob.d
+    ctrl = torch.tensor(prob.macro.ctrl, dtype=torch.float64, device=dev)
+    young = torch.tensor(prob.young, dtype=torch.float64, device=dev)
+    vals = torch.empty(s.nnz, dtype=torch.float64, device=dev)
+    u_np, v_np = draw_uv_seeded(args.config, s.n_dof)
+    u = torch.tensor(u_np, device=dev)
+    v = torch.tensor(v_np, device=dev)
+    grad = torch.empty(s.n_macro_cp * d, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        A.assemble(ctrl, young, prob.nu, vals, stream=stream)
+        if sens:
+            A.sensitivity(ctrl, young, prob.nu, u, v, grad, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    A.set_profiling(True)
+    clocks = ClockSampler(local_rank)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    kms, kn = A.kernel_times()
+    A.set_profiling(False)
+    ms = reduce_max(ms_local, world)
+    tiles_total = s.n_tiles * world
+    value = tiles_total / (ms * 1e-3)
+    nnz_per_s = s.nnz * world / (ms * 1e-3)
+
+    # ---- e2e: host (pinned) inputs through the C ABI, gradient read back ---------
+    e2e = None
+    if not args.no_e2e:
+        h_ctrl = torch.tensor(prob.macro.ctrl, dtype=torch.float64).pin_memory()
+        h_young = torch.tensor(prob.young, dtype=torch.float64).pin_memory()
+        h_u = torch.tensor(u_np).pin_memory()
+        h_v = torch.tensor(v_np).pin_memory()
+        h_grad = torch.empty(s.n_macro_cp * d, dtype=torch.float64).pin_memory()
+        h_grad_np = h_grad.numpy()
+
+        def step_e2e():
+            A.assemble(h_ctrl.numpy(), h_young.numpy(), prob.nu, vals, stream=stream)
+            if sens:
+                A.sensitivity(h_ctrl.numpy(), h_young.numpy(), prob.nu, h_u.numpy(), h_v.numpy(), h_grad_np,
+                              stream=stream)
+        step_e2e()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms_e2e = reduce_max(e0.elapsed_time(e1) / args.steps, world)
+        h2d = 8 * (s.n_macro_cp * d * (2 if sens else 1) + s.n_tiles * (2 if sens else 1) + (2 * s.n_dof if sens else 0))
+        e2e = {"value": tiles_total / (ms_e2e * 1e-3), "unit": "tiles/s", "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * s.n_macro_cp * d if sens else 0),
+               "note": "inputs P, E (and u, v) from pinned host memory via the C ABI [any]-pointer staging; "
+                       "K stays device-resident (consumer is a GPU solver / matrix-free); gradient read back"}
+
+    alg = algorithmic(prob, s, sens)
+    per = lambda slot: kms[slot] / max(kn[slot], 1)
+    k3_ms, k5a_ms, k2_ms, k4_ms = per(1), per(3), per(0), per(2)
+    traffic = load_traffic()
+    rooflines = {
+        "K3_contraction": {"bound": "tensor", "achieved": alg["k3_flops"] / (k3_ms * 1e-3) / 1e12,
+                           "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "ms": k3_ms},
+        "K2_interpolation": {"bound": "hbm", "achieved": alg["k2_bytes"] / (k2_ms * 1e-3) / 1e9,
+                             "peak": None, "unit": "GB/s", "ms": k2_ms},
+        "K4_scatter": {"bound": "hbm", "achieved": alg["k4_bytes"] / (k4_ms * 1e-3) / 1e9,
+                       "peak": None, "unit": "GB/s", "ms": k4_ms},
+    }
+    if sens:
+        rooflines["K5a_W_gemm"] = {"bound": "tensor", "achieved": alg["k5a_flops"] / (k5a_ms * 1e-3) / 1e12,
+                                   "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "ms": k5a_ms}
+        rooflines["K5b_reverse"] = {"ms": per(4)}
+        rooflines["K5c_reduce"] = {"ms": per(5)}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm = peaks.get("hbm_gbs")
+    except Exception:
+        hbm = None
+    hbm = hbm or 6650.0
+    for k in ("K2_interpolation", "K4_scatter"):
+        rooflines[k]["peak"] = hbm
+    for k, r in rooflines.items():
+        if r.get("peak"):
+            r["frac"] = r["achieved"] / r["peak"]
+    dom = rooflines["K3_contraction"]
+    roofline = {"bound": "tensor", "kernel": "K3_contraction (FP64 DMMA)", "achieved": dom["achieved"],
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": dom["frac"],
+                "traffic": traffic.get("K3_dram_bytes_per_launch"),
+                "peak_source": "measured DMMA ceiling, profiles/r01_fp64_ceiling.md (MEASURED_PEAKS.json has no FP64 entry)",
+                "algorithmic_flops_per_launch": alg["k3_flops"]}
+
+    line = {"metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg{args.config}" + ("" if sens else " (K only)"),
+                       "n_tiles_per_gpu": int(s.n_tiles), "nnz": int(s.nnz), "n_dof": int(s.n_dof), "p": prob.p,
+                       "q": prob.q, "sensitivity": sens,
+                       "l2": "working set >> 126 MB L2 (CSR values alone 8*nnz bytes); no explicit flush"},
+            "nnz_per_s": nnz_per_s, "roofline": roofline, "rooflines_all": rooflines,
+            "clocks": clk, "e2e": e2e,
+            "gpu_launches": int(args.steps * (3 + (3 if sens else 0))),
+            "kernel_ms_per_step": {"K2": k2_ms, "K3": k3_ms, "K4": k4_ms, "K5a": k5a_ms if sens else 0.0,
+                                   "K5b": per(4) if sens else 0.0, "K5c": per(5) if sens else 0.0},
+            "offline": {"build_s (host topology + K1 tables + pattern)": build_s}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_t, dt, cores, nnz = cpu_baseline_oracle(sens=sens)
+        line["cpu_baseline"] = {"value": n_t / dt, "unit": "tiles/s", "cores": cores, "kind": "oracle",
+                                "sample": f"cfg5 generator at macro grid (8,4,4) = {n_t} tiles (nnz {nnz}), "
+                                          f"oracle K^pi + full gradient, {dt:.1f} s; tables/pattern untimed"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
