@@ -87,7 +87,9 @@ typedef struct {
   int64_t n_dof;          /* n_nodes * d, interleaved DOF = node*d + a (R9) */
   int64_t nnz;            /* scalar CSR non-zeros of K (both triangles, R9) */
   int64_t n_blocks;       /* d×d structural blocks */
-  int64_t n_contrib;      /* (tile, local row) -> block contributions (K4 gather list) */
+  int64_t n_contrib;      /* (tile, local row) -> block contributions, both triangles */
+  int64_t n_multi_blocks; /* blocks (I <= J) with more than one contribution (K4 gathers them) */
+  int64_t n_side_slots;   /* contributions to those blocks (K3 side slots, d² doubles each) */
 } iga_sizes;
 
 /* ---------------------------------------------------------------------------
@@ -176,12 +178,15 @@ iga_status iga_get_tables(const iga_handle *h, double *out);
 /* iga_get_pairs — (A, B) of every stacked table row, 2 int32 per row. [host] */
 iga_status iga_get_pairs(const iga_handle *h, int32_t *out);
 
-/* Per-kernel device time accumulated by the last iga_assemble / iga_sensitivity calls
- * while profiling is enabled (CUDA events on the caller's stream).  Slots:
- * 0 K2 interpolate, 1 K3 contraction, 2 K4 scatter, 3 K5a W-GEMM, 4 K5b reverse,
- * 5 K5c reduce, 6 host<->device staging.  enable != 0 resets the accumulators. */
+/* Per-kernel device time accumulated by iga_assemble / iga_sensitivity calls while
+ * profiling is enabled (CUDA events on the caller's stream).  IGA_N_PROF slots:
+ * 0 K2 interpolate, 1 K3 contraction + fused scatter, 2 K4 multi-contribution gather,
+ * 3 K5a W-GEMM, 4 K5b reverse, 5 K5c reduce, 6 host<->device staging, 7 K5x X generation,
+ * 8 K3 nzdata output (local_values).  enable != 0 resets the accumulators. */
+#define IGA_N_PROF 10
 iga_status iga_set_profiling(iga_handle *h, int32_t enable);
-iga_status iga_get_kernel_times(const iga_handle *h, double *ms_out /* 8 */, int64_t *launches_out /* 8 */);
+iga_status iga_get_kernel_times(const iga_handle *h, double *ms_out /* IGA_N_PROF */,
+                                int64_t *launches_out /* IGA_N_PROF */);
 
 void iga_free(iga_handle *h);
 const char *iga_last_error(void);

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libiga.so")
+LIB_PATH = os.environ.get("IGA_LIB") or os.path.join(HERE, "libiga.so")   # IGA_LIB: experiment builds only
 
 IGA_STATUS = {0: "IGA_OK", 1: "IGA_EINVAL", 2: "IGA_EDEGENERATE", 3: "IGA_ENONCONFORMING", 4: "IGA_ENOMEM",
               5: "IGA_ECUDA", 6: "IGA_ELIMIT"}
@@ -40,9 +40,10 @@ class iga_sizes(C.Structure):
                 ("k_stride", C.c_int32), ("n_patches", C.c_int32), ("n_gauss", C.c_int32), ("reserved", C.c_int32),
                 ("n_tiles", C.c_int64), ("n_local_rows", C.c_int64), ("n_macro_cp", C.c_int64),
                 ("n_nodes", C.c_int64), ("n_dof", C.c_int64), ("nnz", C.c_int64), ("n_blocks", C.c_int64),
-                ("n_contrib", C.c_int64)]
+                ("n_contrib", C.c_int64), ("n_multi_blocks", C.c_int64), ("n_side_slots", C.c_int64)]
 
 
+N_PROF = 10   # IGA_N_PROF: 0 K2, 1 K3(+scatter), 2 K4, 3 K5a, 4 K5b, 5 K5c, 6 staging, 7 K5x, 8 K3 nzdata
 EXPORTS = ["iga_build_tables", "iga_build_topology", "iga_assemble", "iga_sensitivity", "iga_interpolate", "iga_get_sizes",
            "iga_get_pattern", "iga_get_block_map", "iga_get_node_map", "iga_get_tables", "iga_get_pairs",
            "iga_set_profiling", "iga_get_kernel_times", "iga_free", "iga_last_error", "iga_version"]
@@ -199,8 +200,8 @@ class Assembler:
         _check(load().iga_set_profiling(self._h, int(enable)))
 
     def kernel_times(self):
-        ms = np.zeros(8, dtype=np.float64)
-        n = np.zeros(8, dtype=np.int64)
+        ms = np.zeros(N_PROF, dtype=np.float64)
+        n = np.zeros(N_PROF, dtype=np.int64)
         _check(load().iga_get_kernel_times(self._h, ms.ctypes.data, n.ctypes.data))
         return ms, n
 

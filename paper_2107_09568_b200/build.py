@@ -13,18 +13,19 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC,-fopenmp,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, defines=(), lib=None):
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(HERE, "..", "include", "iga.h"))
-    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
-        return LIB
-    objdir = os.path.join(HERE, "build")
+    LIBP = lib or LIB
+    if not force and os.path.exists(LIBP) and all(os.path.getmtime(LIBP) >= os.path.getmtime(d) for d in deps):
+        return LIBP
+    objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(defines))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in srcs:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + FLAGS + ["-D" + x for x in defines] + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -32,12 +33,12 @@ def build(verbose=False, force=False):
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lgomp"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIBP] + objs + ["-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    return LIB
+    return LIBP
 
 
 if __name__ == "__main__":

@@ -88,6 +88,47 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
                : "d"(a), "d"(b));
 }
 
+// ---- bulk async copies (cp.async.bulk, SASS UBLKCP) + mbarrier pipelines ----------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// bytes: multiple of 16; both addresses 16-B aligned.  Completion is signalled on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Fragment-major ("FM") operand layout of an R×K matrix for mma.m8n8k4:
+// chunks of BR rows × 16 columns are contiguous (BR*16 doubles, ordered [row block][k
+// chunk]); inside a chunk, 8-row group g and 4-column step kk hold the 32 values a warp
+// loads as one fragment, in lane order lane = (row%8)*4 + k%4.  One bulk copy moves a
+// chunk; one LDS.64 per lane (256 contiguous bytes per warp) loads a fragment.
+__host__ __device__ __forceinline__ int64_t fm_index(int64_t r, int k, int BR, int nkc) {
+  const int64_t rb = r / BR;
+  const int rr = (int)(r - rb * BR);
+  return ((rb * nkc + (k >> 4)) * BR + (rr & ~7)) * 16 + ((k >> 2) & 3) * 32 + ((rr & 7) << 2) + (k & 3);
+}
+
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));

@@ -30,19 +30,38 @@ iga_status upload_topology(Handle &h) {
     if (bytes && cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) { set_error("H2D copy failed"); return false; }
     return true;
   };
+  std::vector<int32_t> pinfo(3 * (h.n_patches + 1), 0);
+  for (int pi = 0; pi <= h.n_patches; ++pi) {
+    pinfo[3 * pi] = h.pcol[pi] / IGA_KCHUNK;
+    if (pi < h.n_patches) {
+      pinfo[3 * pi + 1] = h.patches[pi].ctrl_off;
+      pinfo[3 * pi + 2] = h.patches[pi].n_ctrl;
+    }
+  }
   if (!up((void **)&h.d_node_map, h.node_map.data(), h.node_map.size() * 4) ||
       !up((void **)&h.d_pairA, h.pairA.data(), h.pairA.size() * 4) ||
       !up((void **)&h.d_pairB, h.pairB.data(), h.pairB.size() * 4) ||
       !up((void **)&h.d_brow_ptr, h.brow_ptr.data(), h.brow_ptr.size() * 8) ||
       !up((void **)&h.d_bcol, h.bcol.data(), h.bcol.size() * 4) ||
-      !up((void **)&h.d_bcnt, h.bcnt.data(), h.bcnt.size()) ||
-      !up((void **)&h.d_cstart, h.cstart.data(), h.cstart.size() * 8) ||
-      !up((void **)&h.d_contrib, h.contrib.data(), h.contrib.size() * 4))
+      !up((void **)&h.d_rowinfo, h.rowinfo.data(), h.rowinfo.size() * 8) ||
+      !up((void **)&h.d_emap, h.emap.data(), h.emap.size() * 4) ||
+      !up((void **)&h.d_mblk, h.mblk.data(), h.mblk.size() * sizeof(MultiBlock)) ||
+      !up((void **)&h.d_mslot0, h.mslot0.data(), h.mslot0.size() * 4) ||
+      !up((void **)&h.d_slot_tr, h.slot_tr.data(), h.slot_tr.size()) ||
+      !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
+      !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
+      !up((void **)&h.d_patch_info, pinfo.data(), pinfo.size() * 4))
     return IGA_ENOMEM;
-  // the gather lists live on the device only from here on
-  std::vector<uint8_t>().swap(h.bcnt);
-  std::vector<uint32_t>().swap(h.contrib);
-  std::vector<int64_t>().swap(h.cstart);
+  if (cudaMalloc((void **)&h.d_side, std::max<size_t>(8, (size_t)h.n_slots * h.d * h.d * 8)) != cudaSuccess) {
+    set_error("cudaMalloc of the multi-contribution slots failed");
+    return IGA_ENOMEM;
+  }
+  // the epilogue maps live on the device only from here on
+  std::vector<int64_t>().swap(h.rowinfo);
+  std::vector<int32_t>().swap(h.emap);
+  std::vector<MultiBlock>().swap(h.mblk);
+  std::vector<int32_t>().swap(h.mslot0);
+  std::vector<uint8_t>().swap(h.slot_tr);
   return IGA_OK;
 }
 
@@ -124,12 +143,6 @@ static bool check_knots(const iga_spline &s, int k, const char *what, int idx,
   for (int i = p; i < nk - p - 1; ++i)
     if (U[i] < U[i + 1]) el.push_back(i);
   return true;
-}
-
-static int ceil_log2(int64_t v) {
-  int b = 0;
-  while ((int64_t(1) << b) < v) ++b;
-  return b;
 }
 
 struct UF {
@@ -324,9 +337,13 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
         if (ids[i] == ids[i - 1]) { set_error("tile %lld patch %d: two control points merged", (long long)t, pi); return IGA_ENONCONFORMING; }
     }
 
-  // ---- gather lists + pattern (R9) ----------------------------------------------
-  h.row_bits = ceil_log2(std::max<int64_t>(h.M, 2));
-  if (((nt - 1) << (h.row_bits + 1)) >> 32) { set_error("packed (tile,row) does not fit 32 bits"); return IGA_ELIMIT; }
+  // ---- pattern (R9) and the K3 fused-epilogue maps ------------------------------
+  // Every (tile t, table row r) with I = node(A_r), J = node(B_r) contributes the local
+  // block L to K(I,J) and Lᵀ to K(J,I).  Blocks with exactly one contribution are
+  // written straight from the K3 epilogue (emap holds rank(J in row I) | rank(I in row
+  // J) << 16); blocks with several contributions (tile faces, patch interfaces) get
+  // one side slot per contribution and are summed in a fixed order by K4.
+  if (nt * h.M >= (int64_t(1) << 40)) { set_error("n_tiles * table rows exceeds 2^40"); return IGA_ELIMIT; }
   const int64_t nn = h.n_nodes;
   std::vector<int64_t> cnt(nn + 1, 0);
   std::vector<std::atomic<int64_t>> acnt(nn);
@@ -340,55 +357,143 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     }
   for (int64_t i = 0; i < nn; ++i) cnt[i + 1] = cnt[i] + acnt[i].load(std::memory_order_relaxed);
   h.n_contrib = cnt[nn];
+  // key = J << 40 | t*M + r  << 1 | transposed   (transposed: this row's node is B's)
   std::vector<uint64_t> keys(h.n_contrib);
   for (int64_t i = 0; i < nn; ++i) acnt[i].store(cnt[i], std::memory_order_relaxed);
-  const int rb = h.row_bits;
+  std::vector<uint64_t> kcol(h.n_contrib);   // J per key (sort by (J, code))
 #pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < nt; ++t)
     for (int64_t r = 0; r < h.M; ++r) {
       int32_t I = h.node_map[t * nl + h.pairA[r]], J = h.node_map[t * nl + h.pairB[r]];
-      uint64_t pk = ((uint64_t)t << (rb + 1)) | ((uint64_t)r << 1);
-      keys[acnt[I].fetch_add(1, std::memory_order_relaxed)] = ((uint64_t)J << 32) | pk;
-      if (I != J) keys[acnt[J].fetch_add(1, std::memory_order_relaxed)] = ((uint64_t)I << 32) | pk | 1u;
+      uint64_t code = (uint64_t)(t * h.M + r) << 1;
+      int64_t k = acnt[I].fetch_add(1, std::memory_order_relaxed);
+      keys[k] = code;
+      kcol[k] = (uint64_t)J;
+      if (I != J) {
+        k = acnt[J].fetch_add(1, std::memory_order_relaxed);
+        keys[k] = code | 1u;
+        kcol[k] = (uint64_t)I;
+      }
     }
   std::vector<int64_t> nnzb(nn + 1, 0);
   int bad_cnt = 0;
-#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : bad_cnt)
-  for (int64_t i = 0; i < nn; ++i) {
-    std::sort(keys.begin() + cnt[i], keys.begin() + cnt[i + 1]);
-    int64_t nb = 0, run = 0;
-    for (int64_t k = cnt[i]; k < cnt[i + 1]; ++k) {
-      if (k == cnt[i] || (keys[k] >> 32) != (keys[k - 1] >> 32)) { ++nb; run = 0; }
-      if (++run > 255) ++bad_cnt;
+#pragma omp parallel reduction(+ : bad_cnt)
+  {
+    std::vector<std::pair<uint64_t, uint64_t>> tmp;
+#pragma omp for schedule(dynamic, 1024)
+    for (int64_t i = 0; i < nn; ++i) {
+      const int64_t k0 = cnt[i], k1 = cnt[i + 1];
+      tmp.resize(k1 - k0);
+      for (int64_t k = k0; k < k1; ++k) tmp[k - k0] = {kcol[k], keys[k]};
+      std::sort(tmp.begin(), tmp.end());
+      for (int64_t k = k0; k < k1; ++k) { kcol[k] = tmp[k - k0].first; keys[k] = tmp[k - k0].second; }
+      int64_t nb = 0;
+      for (int64_t k = k0; k < k1; ++k)
+        if (k == k0 || kcol[k] != kcol[k - 1]) ++nb;
+      if (nb >= 32768) ++bad_cnt;
+      nnzb[i + 1] = nb;
     }
-    nnzb[i + 1] = nb;
   }
-  if (bad_cnt) { set_error("a block has more than 255 contributions"); return IGA_ELIMIT; }
+  if (bad_cnt) { set_error("a block row has >= 32768 blocks (emap rank width)"); return IGA_ELIMIT; }
   h.brow_ptr.assign(nn + 1, 0);
   for (int64_t i = 0; i < nn; ++i) h.brow_ptr[i + 1] = h.brow_ptr[i] + nnzb[i + 1];
   h.n_blocks = h.brow_ptr[nn];
   h.nnz = h.n_blocks * d * d;
+  if (h.n_blocks >= (int64_t(1) << 39)) { set_error("too many blocks"); return IGA_ELIMIT; }
   h.bcol.assign(h.n_blocks, 0);
-  std::vector<uint8_t> bcnt(h.n_blocks, 0);
-  std::vector<uint32_t> contrib(h.n_contrib);
+  h.emap.assign(nt * h.M, 0);
+  uint16_t *e16 = reinterpret_cast<uint16_t *>(h.emap.data());
+  std::vector<int64_t> mcount(nn + 1, 0), scount(nn + 1, 0);
+  // pass 1: block columns, direct ranks, multi-block counts (canonical I <= J)
 #pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t i = 0; i < nn; ++i) {
     int64_t b = h.brow_ptr[i] - 1;
-    for (int64_t k = cnt[i]; k < cnt[i + 1]; ++k) {
-      if (k == cnt[i] || (keys[k] >> 32) != (keys[k - 1] >> 32)) {
-        ++b;
-        h.bcol[b] = (int32_t)(keys[k] >> 32);
+    for (int64_t k = cnt[i]; k < cnt[i + 1];) {
+      int64_t k1 = k + 1;
+      while (k1 < cnt[i + 1] && kcol[k1] == kcol[k]) ++k1;
+      ++b;
+      const int64_t J = (int64_t)kcol[k];
+      h.bcol[b] = (int32_t)J;
+      if (k1 - k == 1) {
+        const uint64_t code = keys[k] >> 1;
+        e16[2 * code + (keys[k] & 1u)] = (uint16_t)(b - h.brow_ptr[i]);
+      } else if (J >= i) {
+        mcount[i + 1] += 1;
+        scount[i + 1] += k1 - k;
       }
-      bcnt[b]++;
-      contrib[k] = (uint32_t)(keys[k] & 0xffffffffu);
+      k = k1;
     }
   }
-  keys.clear();
-  keys.shrink_to_fit();
+  for (int64_t i = 0; i < nn; ++i) { mcount[i + 1] += mcount[i]; scount[i + 1] += scount[i]; }
+  h.n_multi = mcount[nn];
+  h.n_slots = scount[nn];
+  if (h.n_slots >= (int64_t(1) << 31) - 1) { set_error("too many multi-contribution slots"); return IGA_ELIMIT; }
+  h.mblk.assign(h.n_multi, MultiBlock{});
+  h.mslot0.assign(h.n_multi + 1, 0);
+  h.slot_tr.assign(h.n_slots, 0);
+  h.mslot0[h.n_multi] = (int32_t)h.n_slots;
+  auto rank_in_row = [&](int64_t row, int64_t col) -> int64_t {
+    const int32_t *bb = h.bcol.data() + h.brow_ptr[row], *ee = h.bcol.data() + h.brow_ptr[row + 1];
+    return std::lower_bound(bb, ee, (int32_t)col) - bb;
+  };
+  // pass 2: multi blocks and their slots (needs all of bcol)
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t i = 0; i < nn; ++i) {
+    int64_t m = mcount[i], sl = scount[i], b = h.brow_ptr[i] - 1;
+    for (int64_t k = cnt[i]; k < cnt[i + 1];) {
+      int64_t k1 = k + 1;
+      while (k1 < cnt[i + 1] && kcol[k1] == kcol[k]) ++k1;
+      ++b;
+      const int64_t J = (int64_t)kcol[k];
+      if (k1 - k > 1 && J >= i) {
+        MultiBlock &mb = h.mblk[m];
+        mb.off_ij = (int64_t)d * d * h.brow_ptr[i] + (int64_t)d * (b - h.brow_ptr[i]);
+        mb.off_ji = (int64_t)d * d * h.brow_ptr[J] + (int64_t)d * rank_in_row(J, i);
+        mb.stride_i = (int32_t)(d * (h.brow_ptr[i + 1] - h.brow_ptr[i]));
+        mb.stride_j = (int32_t)(d * (h.brow_ptr[J + 1] - h.brow_ptr[J]));
+        h.mslot0[m] = (int32_t)sl;
+        for (int64_t kk = k; kk < k1; ++kk, ++sl) {
+          h.slot_tr[sl] = (uint8_t)(keys[kk] & 1u);
+          h.emap[keys[kk] >> 1] = -(int32_t)(sl + 1);
+        }
+        ++m;
+      }
+      k = k1;
+    }
+  }
+  std::vector<uint64_t>().swap(keys);
+  std::vector<uint64_t>().swap(kcol);
+  h.rowinfo.assign(nt * nl, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t f = 0; f < nt * nl; ++f) {
+    const int64_t I = h.node_map[f];
+    h.rowinfo[f] = (h.brow_ptr[I] << 24) | (h.brow_ptr[I + 1] - h.brow_ptr[I]);
+  }
 
-  h.bcnt = std::move(bcnt);
-  h.contrib = std::move(contrib);
-  h.cstart = std::move(cnt);
+  // ---- operand layouts: K3 A rows, coefficient rows, K5a padded reduction columns --
+  h.Mpad = (h.M + IGA_K3_BM - 1) / IGA_K3_BM * IGA_K3_BM;
+  h.Npad = (nt * d * d + IGA_GEMM_BN - 1) / IGA_GEMM_BN * IGA_GEMM_BN;
+  h.pcol.assign(n_patches + 1, 0);
+  h.max_patch_ctrl = 0;
+  for (int pi = 0; pi < n_patches; ++pi) {
+    h.pcol[pi + 1] = h.pcol[pi] + (h.patches[pi].n_nz + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK;
+    h.max_patch_ctrl = std::max(h.max_patch_ctrl, h.patches[pi].n_ctrl);
+  }
+  if (h.max_patch_ctrl >= 32768) { set_error("tile patch with >= 32768 control points"); return IGA_ELIMIT; }
+  h.Kp = h.pcol[n_patches];
+  h.k5_pair.assign(h.Kp, -1);
+  h.k5_col.assign(h.M, 0);
+  for (int pi = 0; pi < n_patches; ++pi) {
+    const PatchInfo &P = h.patches[pi];
+    for (int i = 0; i < P.n_nz; ++i) {
+      const int64_t r = P.row_off + i;
+      h.k5_pair[h.pcol[pi] + i] = (h.pairA[r] - P.ctrl_off) | ((h.pairB[r] - P.ctrl_off) << 16);
+      h.k5_col[r] = h.pcol[pi] + i;
+    }
+  }
+  // K5a CTA height IGA_K3_BM κ rows
+  h.k5_rows = (h.kstride + IGA_K3_BM - 1) / IGA_K3_BM * IGA_K3_BM;
+  if (k5x_smem_bytes(d, h.max_patch_ctrl) > 227 * 1024) { set_error("tile patch too large for the K5 shared-memory staging (%d control points)", h.max_patch_ctrl); return IGA_ELIMIT; }
 
   // ---- interpolation operator Π1 = V1^{-1} (R1) --------------------------------
   double w[IGA_MAXQ + 1], V[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];

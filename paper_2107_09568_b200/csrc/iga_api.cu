@@ -10,11 +10,13 @@ namespace iga {
 const char *get_error();
 
 Handle::~Handle() {
-  void *bufs[] = {d_table, d_tableT, d_coef, d_local, d_W, d_gpart, d_node_map, d_pairA, d_pairB, d_row_ptr,
-                  d_col_idx, d_brow_ptr, d_bcol, d_bcnt, d_cstart, d_contrib, d_mknots, d_mspan, d_flag,
-                  d_stage_ctrl, d_stage_young, d_stage_u, d_stage_v, d_stage_out};
+  void *bufs[] = {d_table, d_tabA, d_tabAT, d_coef, d_side, d_W, d_X, d_gpart, d_node_map, d_pairA, d_pairB,
+                  d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_slot_tr,
+                  d_k5_pair, d_k5_col, d_patch_info, d_mknots, d_mspan, d_flag};
   for (void *b : bufs)
     if (b) cudaFree(b);
+  for (int i = 0; i < N_STAGE; ++i)
+    if (d_stage[i]) cudaFree(d_stage[i]);
   for (auto e : ev_pool) cudaEventDestroy(e);
 }
 
@@ -39,31 +41,44 @@ static bool is_device_ptr(const void *p) {
     }                                                                                    \
   } while (0)
 
-// Staging of [any] pointers: device pointers pass through; host pointers are copied.
+// Staging of [any] pointers: device pointers pass through; host pointers are copied
+// through per-handle grow-only device buffers (one per argument slot), so repeated
+// calls with host arguments cost only the copies.
 struct Stager {
   Handle &h;
   cudaStream_t s;
-  std::vector<std::pair<double *, const double *>> pending_out;   // (device, host) with bytes
+  int slot = 0;
+  std::vector<std::pair<double *, const double *>> pending_out;   // (device, host)
   std::vector<size_t> pending_bytes;
-  std::vector<void *> temps;
   Stager(Handle &hh, cudaStream_t ss) : h(hh), s(ss) {}
-  ~Stager() {
-    for (void *t : temps) cudaFreeAsync(t, s);
+  double *buffer(size_t n) {
+    if (slot >= Handle::N_STAGE) return nullptr;
+    const int i = slot++;
+    const size_t bytes = std::max<size_t>(n, 1) * 8;
+    if (h.stage_cap[i] < bytes) {
+      if (h.d_stage[i]) {
+        cudaStreamSynchronize(s);
+        cudaFree(h.d_stage[i]);
+        h.d_stage[i] = nullptr;
+        h.stage_cap[i] = 0;
+      }
+      if (cudaMalloc((void **)&h.d_stage[i], bytes) != cudaSuccess) return nullptr;
+      h.stage_cap[i] = bytes;
+    }
+    return h.d_stage[i];
   }
   bool in(const double *p, size_t n, const double **out) {
     if (!p || is_device_ptr(p)) { *out = p; return true; }
-    double *d = nullptr;
-    if (cudaMallocAsync((void **)&d, std::max<size_t>(n, 1) * 8, s) != cudaSuccess) return false;
-    temps.push_back(d);
+    double *d = buffer(n);
+    if (!d) return false;
     if (cudaMemcpyAsync(d, p, n * 8, cudaMemcpyHostToDevice, s) != cudaSuccess) return false;
     *out = d;
     return true;
   }
   bool out(double *p, size_t n, double **dev) {
     if (!p || is_device_ptr(p)) { *dev = p; return true; }
-    double *d = nullptr;
-    if (cudaMallocAsync((void **)&d, std::max<size_t>(n, 1) * 8, s) != cudaSuccess) return false;
-    temps.push_back(d);
+    double *d = buffer(n);
+    if (!d) return false;
     pending_out.push_back({d, p});
     pending_bytes.push_back(n * 8);
     *dev = d;
@@ -179,17 +194,19 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, c
   h.on_device = true;
   const int d = h.d;
   const int64_t N = h.n_tiles * d * d;
-  const int64_t ldT = (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK;
   CUB(cudaMalloc((void **)&h.d_flag, 4 * sizeof(int)));
   CUB(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
   CUB(cudaMalloc((void **)&h.d_table, sizeof(double) * h.M * h.kstride));
   CUB(cudaMemsetAsync(h.d_table, 0, sizeof(double) * h.M * h.kstride, s));
-  CUB(cudaMalloc((void **)&h.d_tableT, sizeof(double) * h.kstride * ldT));
-  CUB(cudaMemsetAsync(h.d_tableT, 0, sizeof(double) * h.kstride * ldT, s));
-  CUB(cudaMalloc((void **)&h.d_coef, sizeof(double) * N * h.kstride));
-  CUB(cudaMemsetAsync(h.d_coef, 0, sizeof(double) * N * h.kstride, s));
-  CUB(cudaMalloc((void **)&h.d_local, sizeof(double) * h.M * N));
+  // fragment-major operands; the zero padding (rows, κ >= n_k, patch columns) is never rewritten
+  CUB(cudaMalloc((void **)&h.d_tabA, sizeof(double) * h.Mpad * h.kstride));
+  CUB(cudaMemsetAsync(h.d_tabA, 0, sizeof(double) * h.Mpad * h.kstride, s));
+  CUB(cudaMalloc((void **)&h.d_tabAT, sizeof(double) * h.k5_rows * h.Kp));
+  CUB(cudaMemsetAsync(h.d_tabAT, 0, sizeof(double) * h.k5_rows * h.Kp, s));
+  CUB(cudaMalloc((void **)&h.d_coef, sizeof(double) * h.Npad * h.kstride));
+  CUB(cudaMemsetAsync(h.d_coef, 0, sizeof(double) * h.Npad * h.kstride, s));
   CUB(cudaMalloc((void **)&h.d_W, sizeof(double) * N * h.kstride));
+  CUB(cudaMalloc((void **)&h.d_X, sizeof(double) * h.Npad * h.Kp));
   int nact_m = 1;
   for (int k = 0; k < d; ++k) nact_m *= h.pm[k] + 1;
   CUB(cudaMalloc((void **)&h.d_gpart, sizeof(double) * h.n_tiles * nact_m * d));
@@ -245,6 +262,7 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, c
   double gx[16], gw[16];
   gauss_legendre01(h.n_g, gx, gw);
   CUB(launch_tables(h, dp.data(), n_patches, d_tctrl, d_tknots, d_tel, gx, gw, pt_off, s));
+  CUB(launch_pack_tables(h, s));
   CUB(launch_expand_pattern(h, s));
   CUB(cudaStreamSynchronize(s));
   cudaFree(d_tctrl);
@@ -297,19 +315,8 @@ iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
   o->nnz = h.nnz;
   o->n_blocks = h.n_blocks;
   o->n_contrib = h.n_contrib;
-  return IGA_OK;
-}
-
-static iga_status run_interp(Handle &h, Stager &sg, Prof &pf, const double *ctrl, const double *young, int ypt,
-                             double nu, cudaStream_t s) {
-  const double *dctrl, *dyoung;
-  if (!sg.in(ctrl, (size_t)h.n_cp * h.d, &dctrl) || !sg.in(young, ypt ? (size_t)h.n_tiles : 1, &dyoung)) {
-    set_error("staging of host inputs failed");
-    return IGA_ENOMEM;
-  }
-  int id = pf.begin(0);
-  CU(launch_interpolate(h, dctrl, dyoung, ypt, nu, h.d_coef, s));
-  pf.end(id);
+  o->n_multi_blocks = h.n_multi;
+  o->n_side_slots = h.n_slots;
   return IGA_OK;
 }
 
@@ -339,16 +346,19 @@ iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const do
   }
   pf.end(idst);
   int id = pf.begin(0);
-  CU(launch_interpolate(h, dctrl, dyoung, young_per_tile, nu, h.d_coef, s));
+  CU(launch_interpolate(h, dctrl, dyoung, young_per_tile, nu, h.d_coef, true, s));
   pf.end(id);
-  const int64_t N = h.n_tiles * h.d * h.d;
-  double *loc = dlocal_out ? dlocal_out : h.d_local;
   id = pf.begin(1);
-  CU(launch_contraction(h, h.d_table, h.d_coef, loc, h.M, N, h.nk, h.kstride, s));
+  CU(launch_contraction(h, dvals, nullptr, s));
   pf.end(id);
   id = pf.begin(2);
-  CU(launch_scatter(h, loc, dvals, s));
+  CU(launch_scatter_multi(h, dvals, s));
   pf.end(id);
+  if (dlocal_out) {   // optional nzdata output (parity of the element matrices, R17): K3 again
+    id = pf.begin(8);
+    CU(launch_contraction(h, nullptr, dlocal_out, s));
+    pf.end(id);
+  }
   idst = pf.begin(6);
   if (!sg.flush()) { set_error("D2H copy of outputs failed"); return IGA_ECUDA; }
   pf.end(idst);
@@ -368,9 +378,19 @@ iga_status iga_interpolate(const iga_handle *Hc, const double *macro_ctrl, const
   Stager sg(h, s);
   Prof pf(h, s);
   CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
-  st = run_interp(h, sg, pf, macro_ctrl, young, young_per_tile, nu, s);
-  if (st) return st;
-  CU(cudaMemcpyAsync(coef, h.d_coef, sizeof(double) * h.n_tiles * h.d * h.d * h.kstride, cudaMemcpyDefault, s));
+  const double *dctrl, *dyoung;
+  double *dcoef;
+  const size_t ncoef = (size_t)h.n_tiles * h.d * h.d * h.kstride;
+  if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles : 1, &dyoung) || !sg.out(coef, ncoef, &dcoef)) {
+    set_error("staging failed");
+    return IGA_ENOMEM;
+  }
+  CU(cudaMemsetAsync(dcoef, 0, ncoef * sizeof(double), s));
+  int id = pf.begin(0);
+  CU(launch_interpolate(h, dctrl, dyoung, young_per_tile, nu, dcoef, false, s));
+  pf.end(id);
+  if (!sg.flush()) { set_error("D2H copy failed"); return IGA_ECUDA; }
   st = check_flag(h, s);
   pf.collect();
   return st;
@@ -398,8 +418,11 @@ iga_status iga_sensitivity(const iga_handle *Hc, const double *macro_ctrl, const
     return IGA_ENOMEM;
   }
   pf.end(idst);
-  int id = pf.begin(3);
-  CU(launch_sens_W(h, du, dv, h.d_W, s));
+  int id = pf.begin(7);
+  CU(launch_sens_X(h, du, dv, s));
+  pf.end(id);
+  id = pf.begin(3);
+  CU(launch_sens_W(h, h.d_W, s));
   pf.end(id);
   id = pf.begin(4);
   CU(launch_sens_reverse(h, dctrl, dyoung, young_per_tile, nu, h.d_W, h.d_gpart, s));
@@ -493,13 +516,13 @@ iga_status iga_set_profiling(iga_handle *H, int32_t enable) {
   if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
   H->h.profiling = enable != 0;
   if (enable)
-    for (int i = 0; i < 8; ++i) { H->h.prof_ms[i] = 0; H->h.prof_launches[i] = 0; }
+    for (int i = 0; i < IGA_N_PROF; ++i) { H->h.prof_ms[i] = 0; H->h.prof_launches[i] = 0; }
   return IGA_OK;
 }
 
 iga_status iga_get_kernel_times(const iga_handle *H, double *ms_out, int64_t *launches_out) {
   if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < IGA_N_PROF; ++i) {
     if (ms_out) ms_out[i] = H->h.prof_ms[i];
     if (launches_out) launches_out[i] = H->h.prof_launches[i];
   }

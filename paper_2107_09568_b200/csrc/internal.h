@@ -11,6 +11,8 @@
 #define IGA_MAXP 4          // max spline degree (tile and macro)
 #define IGA_MAXQ 4          // max interpolation degree
 #define IGA_KCHUNK 16       // GEMM k-chunk; k_stride is a multiple of it
+#define IGA_K3_BM 128       // K3 CTA rows (table rows)
+#define IGA_GEMM_BN 72      // K3/K5a CTA columns (tiles × d²): 8 tiles in 3D, 18 in 2D
 
 namespace iga {
 
@@ -44,6 +46,14 @@ struct DevPatch {
   int n_spans;
 };
 
+// one d×d block of K that several (tile, local row) contributions share (K4 gather)
+struct MultiBlock {
+  int64_t off_ij;      // scalar CSR offset of element (0,0) of block (I,J)
+  int64_t off_ji;      // ... of block (J,I)
+  int32_t stride_i;    // d * (blocks in block row I) = scalar row pitch of row I
+  int32_t stride_j;
+};
+
 struct Handle {
   int d = 0, p = 0, q = 0, n_g = 0, npi = 0, nk = 0, kstride = 0;
   int n_patches = 0;
@@ -60,23 +70,37 @@ struct Handle {
   int64_t n_cp = 0, n_tiles = 0;
   // global numbering / pattern
   int64_t n_nodes = 0, n_dof = 0, nnz = 0, n_blocks = 0, n_contrib = 0;
-  int row_bits = 0;
   std::vector<int32_t> node_map;     // [n_tiles][n_local_ctrl]
   std::vector<int64_t> brow_ptr;     // [n_nodes+1]
   std::vector<int32_t> bcol;         // [n_blocks]
-  std::vector<uint8_t> bcnt;         // [n_blocks] contributions per block (until upload)
-  std::vector<uint32_t> contrib;     // packed gather list (until upload)
-  std::vector<int64_t> cstart;       // [n_nodes+1] (until upload)
+  // K3 fused-epilogue maps (reading R9; until upload)
+  std::vector<int64_t> rowinfo;      // [n_tiles*n_local_ctrl] (brow_ptr[I] << 24) | blocks in row I
+  std::vector<int32_t> emap;         // [n_tiles*M] >= 0: rank(J in row I) | rank(I in row J) << 16; < 0: -(slot+1)
+  int64_t n_multi = 0, n_slots = 0;  // blocks with > 1 contribution, and their contributions
+  std::vector<MultiBlock> mblk;      // [n_multi]
+  std::vector<int32_t> mslot0;       // [n_multi+1] first slot of each multi block
+  std::vector<uint8_t> slot_tr;      // [n_slots] 1 = slot holds the (J,I)-oriented block
+  // operand layouts (fragment-major, device_common.cuh fm_index)
+  int64_t Mpad = 0;                  // rows of d_tabA (multiple of IGA_K3_BM)
+  int64_t Npad = 0;                  // rows of d_coef (multiple of IGA_GEMM_BN)
+  int64_t k5_rows = 0;               // κ rows of d_tabAT (multiple of IGA_K3_BM)
+  int64_t Kp = 0;                    // K5a reduction length: table rows, each patch padded to 16
+  int max_patch_ctrl = 0;
+  std::vector<int32_t> pcol;         // [n_patches+1] first padded column of each patch
+  std::vector<int32_t> k5_pair;      // [Kp] patch-local (A | B << 16), -1 = padding
+  std::vector<int32_t> k5_col;       // [M] padded column of each table row
   bool on_device = false;
   // interpolation operator
   double interp_x[IGA_MAXQ + 1];
   double Pi1[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];   // V1^{-1}
   // device buffers
-  double *d_table = nullptr;     // [M][kstride]
-  double *d_tableT = nullptr;    // [kstride][M] (K5a A-operand)
-  double *d_coef = nullptr;      // [n_tiles*d*d][kstride]
-  double *d_local = nullptr;     // [M][N], N = n_tiles*d*d
+  double *d_table = nullptr;     // [M][kstride] row-major (K1 output, accessor)
+  double *d_tabA = nullptr;      // FM [Mpad][kstride], BR = IGA_K3_BM (K3 A operand)
+  double *d_tabAT = nullptr;     // FM [k5_rows][Kp], BR = IGA_K3_BM (K5a A operand)
+  double *d_coef = nullptr;      // FM [Npad][kstride], BR = IGA_GEMM_BN (K3 B operand)
+  double *d_side = nullptr;      // [n_slots][d*d] multi-contribution blocks (K3 -> K4)
   double *d_W = nullptr;         // [N][kstride]
+  double *d_X = nullptr;         // FM [Npad][Kp], BR = IGA_GEMM_BN (K5a B operand, from u, v)
   double *d_gpart = nullptr;     // [n_tiles][n_el_cp][d]
   int32_t *d_node_map = nullptr;
   int32_t *d_pairA = nullptr, *d_pairB = nullptr;
@@ -84,19 +108,25 @@ struct Handle {
   int32_t *d_col_idx = nullptr;
   int64_t *d_brow_ptr = nullptr;
   int32_t *d_bcol = nullptr;
-  uint8_t *d_bcnt = nullptr;
-  int64_t *d_cstart = nullptr;   // [n_nodes+1] start of each node's contributor list
-  uint32_t *d_contrib = nullptr; // packed (t, row, transposed)
+  int64_t *d_rowinfo = nullptr;
+  int32_t *d_emap = nullptr;
+  MultiBlock *d_mblk = nullptr;
+  int32_t *d_mslot0 = nullptr;
+  uint8_t *d_slot_tr = nullptr;
+  int32_t *d_k5_pair = nullptr;
+  int32_t *d_k5_col = nullptr;   // [M]
+  int32_t *d_patch_info = nullptr; // [n_patches][3]: first K5a chunk, ctrl_off, n_ctrl (+ sentinel chunk)
   double *d_mknots = nullptr;    // macro knots, 3 directions concatenated
   int32_t *d_mspan = nullptr;    // element -> knot span, 3 directions concatenated
   int *d_flag = nullptr;         // [0] error flag, [1] tile, [2] node
   // staging (host pointers in [any] arguments)
-  double *d_stage_ctrl = nullptr, *d_stage_young = nullptr, *d_stage_u = nullptr, *d_stage_v = nullptr;
-  double *d_stage_out = nullptr; size_t stage_out_bytes = 0;
+  static constexpr int N_STAGE = 6;
+  double *d_stage[N_STAGE] = {nullptr};   // grow-only device copies of host [any] arguments
+  size_t stage_cap[N_STAGE] = {0};
   // profiling
   bool profiling = false;
-  double prof_ms[8] = {0};
-  int64_t prof_launches[8] = {0};
+  double prof_ms[IGA_N_PROF] = {0};
+  int64_t prof_launches[IGA_N_PROF] = {0};
   std::vector<cudaEvent_t> ev_pool;
   ~Handle();
 };
@@ -112,13 +142,17 @@ struct InterpConst {
 cudaError_t launch_tables(const Handle &h, const DevPatch *dpatches, int n_patches,
                           const double *d_tile_ctrl, const double *d_tile_knots, const int *d_tile_elspan,
                           const double *d_gx, const double *d_gw, int total_pts, cudaStream_t s);
+// fm = true: FM layout into d_coef-shaped buffer; false: row-major coef[n][kstride]
 cudaError_t launch_interpolate(const Handle &h, const double *ctrl, const double *young, int young_per_tile,
-                               double nu, double *coef, cudaStream_t s);
-cudaError_t launch_contraction(const Handle &h, const double *A, const double *B, double *C,
-                               int64_t M, int64_t N, int K, int kstride, cudaStream_t s);
-cudaError_t launch_scatter(const Handle &h, const double *local, double *vals, cudaStream_t s);
+                               double nu, double *coef, bool fm, cudaStream_t s);
+cudaError_t launch_pack_tables(const Handle &h, cudaStream_t s);
+// K3: vals != nullptr -> fused CSR epilogue (+ side slots); local != nullptr -> local[M][N] output
+cudaError_t launch_contraction(const Handle &h, double *vals, double *local, cudaStream_t s);
+cudaError_t launch_scatter_multi(const Handle &h, double *vals, cudaStream_t s);
 cudaError_t launch_expand_pattern(const Handle &h, cudaStream_t s);
-cudaError_t launch_sens_W(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s);
+cudaError_t launch_sens_X(const Handle &h, const double *u, const double *v, cudaStream_t s);
+cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s);
+size_t k5x_smem_bytes(int d, int max_patch_ctrl);
 cudaError_t launch_sens_reverse(const Handle &h, const double *ctrl, const double *young, int young_per_tile,
                                 double nu, const double *W, double *gpart, cudaStream_t s);
 cudaError_t launch_sens_reduce(const Handle &h, const double *gpart, double *grad, cudaStream_t s);

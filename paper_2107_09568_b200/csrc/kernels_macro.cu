@@ -132,7 +132,7 @@ __device__ void tensor_pass(const InterpConst &c_ip, const double *in, double *o
 template <int D>
 __global__ void k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
                                const int *__restrict__ mspan, const double *__restrict__ young, int ypt,
-                               double nu, double *__restrict__ coef, int kstride, int *flag) {
+                               double nu, double *__restrict__ coef, int kstride, int fm, int *flag) {
   extern __shared__ double sm[];
   __shared__ MacroTile<D> mt;
   const int64_t t = blockIdx.x;
@@ -172,13 +172,15 @@ __global__ void k2_interpolate(const __grid_constant__ InterpConst c_ip, const d
     __syncthreads();
     double *tmp = in; in = out; out = tmp;
   }
-  // coef[(t*DD + ab)*kstride + (ij*npi + C)]
+  // coefficient row n = t*DD + ab, column κ = ij*npi + C: row-major coef[n*kstride + κ]
+  // (parity accessor) or the fragment-major K3 B operand (fm_index, BR = IGA_GEMM_BN)
   const int nk = DD * npi;
-  double *dst = coef + (size_t)t * DD * kstride;
   for (int idx = threadIdx.x; idx < DD * nk; idx += blockDim.x) {
     int ab = idx / nk, kap = idx % nk;
     int ij = kap / npi, C = kap % npi;
-    dst[(size_t)ab * kstride + kap] = in[C * NC + ij * DD + ab];
+    const int64_t n = t * DD + ab;
+    const int64_t o = fm ? fm_index(n, kap, IGA_GEMM_BN, kstride / IGA_KCHUNK) : n * kstride + kap;
+    coef[o] = in[C * NC + ij * DD + ab];
   }
 }
 
@@ -320,14 +322,14 @@ static size_t macro_smem(const Handle &h, int extra_per_node) {
 }
 
 cudaError_t launch_interpolate(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
-                               double *coef, cudaStream_t s) {
+                               double *coef, bool fm, cudaStream_t s) {
   size_t sm = macro_smem(h, 0);
   if (h.d == 2) {
     cudaFuncSetAttribute(k2_interpolate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k2_interpolate<2><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, coef, h.kstride, h.d_flag);
+    k2_interpolate<2><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, coef, h.kstride, (int)fm, h.d_flag);
   } else {
     cudaFuncSetAttribute(k2_interpolate<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k2_interpolate<3><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, coef, h.kstride, h.d_flag);
+    k2_interpolate<3><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, coef, h.kstride, (int)fm, h.d_flag);
   }
   return cudaGetLastError();
 }

@@ -1,77 +1,59 @@
-// kernels_scatter.cu — K4: local element blocks -> full symmetric CSR values
-// ("any scientific library ... sparse matrix data structures", §3.2.4
-// step 4 P:425; reading R9 for the symmetric storage).
+// kernels_scatter.cu — K4: the blocks of K that several (tile, local row) contributions
+// share ("any scientific library ... sparse matrix data structures",
+// §3.2.4 step 4 P:425; reading R9 for the symmetric storage).
 //
-// Owner computes, atomic-free and deterministic: one warp per global node row I.
-// Lane j owns block (I, J_j) of the block row; its contributor list (tile, local row,
-// transposed?) was built once on the host, sorted by (tile, row).  Each contributor is
-// a 9-double (3D) contiguous block of `local`; diagonal pairs (A = B) contribute their
-// upper triangle to both triangles so K is bitwise symmetric.  The node's d scalar
-// rows are one contiguous segment of the CSR value array: lane j writes d×d values at
-// row_base + a*d*nnzb + d*j + b.
+// Single-contribution blocks are written by the K3 epilogue directly.  A block with
+// several contributions — control points on tile faces shared by neighbouring tiles,
+// or on declared patch interfaces inside a tile — receives one side slot per
+// contribution from K3; here one thread per such block sums its slots in the fixed
+// order built on the host (sorted by (tile, row)), transposing the slots recorded in
+// the (J,I) orientation, and writes K(I,J) and K(J,I) = K(I,J)ᵀ.  Diagonal blocks take
+// the upper triangle for both triangles.  No atomics; bitwise deterministic.
 #include "device_common.cuh"
 
 namespace iga {
 
 template <int D>
 __global__ void __launch_bounds__(256)
-k4_scatter(const double *__restrict__ local, double *__restrict__ vals, const int64_t *__restrict__ brow_ptr,
-           const uint8_t *__restrict__ bcnt, const int64_t *__restrict__ cstart,
-           const uint32_t *__restrict__ contrib, const int *__restrict__ pairA, const int *__restrict__ pairB,
-           int64_t n_nodes, int64_t ldl, int rb) {
+k4_multi(const double *__restrict__ side, const MultiBlock *__restrict__ mblk, const int32_t *__restrict__ mslot0,
+         const uint8_t *__restrict__ slot_tr, int64_t n_multi, double *__restrict__ vals) {
   constexpr int DD = D * D;
-  const int lane = threadIdx.x & 31;
-  const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (I >= n_nodes) return;
-  const int64_t b0 = brow_ptr[I];
-  const int nb = (int)(brow_ptr[I + 1] - b0);
-  const int64_t rowbase = DD * b0, rowlen = (int64_t)D * nb;
-  int64_t cbase = cstart[I];
-  const uint32_t rmask = (1u << rb) - 1u;
-  for (int jb0 = 0; jb0 < nb; jb0 += 32) {
-    const int jb = jb0 + lane;
-    const int cnt = jb < nb ? bcnt[b0 + jb] : 0;
-    int incl = cnt;
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n_multi) return;
+  const MultiBlock mb = mblk[m];
+  const int s0 = mslot0[m], s1 = mslot0[m + 1];
+  double acc[DD];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int64_t c0 = cbase + incl - cnt;
-    double acc[DD];
+  for (int e = 0; e < DD; ++e) acc[e] = 0.0;
+  for (int sl = s0; sl < s1; ++sl) {
+    const double *L = side + (int64_t)sl * DD;
+    double l[DD];
 #pragma unroll
-    for (int e = 0; e < DD; ++e) acc[e] = 0.0;
-    for (int k = 0; k < cnt; ++k) {
-      const uint32_t pk = contrib[c0 + k];
-      const int64_t t = pk >> (rb + 1);
-      const int r = (int)((pk >> 1) & rmask);
-      const double *L = local + (int64_t)r * ldl + t * DD;
-      double l[DD];
-#pragma unroll
-      for (int e = 0; e < DD; ++e) l[e] = L[e];
-      if (pairA[r] == pairB[r]) {
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int b = 0; b < D; ++b) acc[a * D + b] += a <= b ? l[a * D + b] : l[b * D + a];
-      } else if (pk & 1u) {
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int b = 0; b < D; ++b) acc[a * D + b] += l[b * D + a];
-      } else {
-#pragma unroll
-        for (int e = 0; e < DD; ++e) acc[e] += l[e];
-      }
-    }
-    if (jb < nb) {
+    for (int e = 0; e < DD; ++e) l[e] = L[e];
+    if (slot_tr[sl]) {
 #pragma unroll
       for (int a = 0; a < D; ++a)
 #pragma unroll
-        for (int b = 0; b < D; ++b) vals[rowbase + a * rowlen + (int64_t)D * jb + b] = acc[a * D + b];
+        for (int b = 0; b < D; ++b) acc[a * D + b] += l[b * D + a];
+    } else {
+#pragma unroll
+      for (int e = 0; e < DD; ++e) acc[e] += l[e];
     }
-    cbase += __shfl_sync(0xffffffffu, incl, 31);
   }
+  if (mb.off_ij == mb.off_ji) {   // diagonal block
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) vals[mb.off_ij + a * mb.stride_i + b] = a <= b ? acc[a * D + b] : acc[b * D + a];
+    return;
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      vals[mb.off_ij + a * mb.stride_i + b] = acc[a * D + b];
+      vals[mb.off_ji + b * mb.stride_j + a] = acc[a * D + b];
+    }
 }
 
 // row_ptr / col_idx of the scalar CSR from the block CSR (interleaved DOFs, R9).
@@ -94,16 +76,13 @@ __global__ void k4_expand_pattern(const int64_t *__restrict__ brow_ptr, const in
   }
 }
 
-cudaError_t launch_scatter(const Handle &h, const double *local, double *vals, cudaStream_t s) {
-  int64_t threads = h.n_nodes * 32;
-  unsigned blocks = (unsigned)((threads + 255) / 256);
-  int64_t ldl = h.n_tiles * h.d * h.d;
+cudaError_t launch_scatter_multi(const Handle &h, double *vals, cudaStream_t s) {
+  if (h.n_multi == 0) return cudaSuccess;
+  unsigned blocks = (unsigned)((h.n_multi + 255) / 256);
   if (h.d == 2)
-    k4_scatter<2><<<blocks, 256, 0, s>>>(local, vals, h.d_brow_ptr, h.d_bcnt, h.d_cstart, h.d_contrib, h.d_pairA,
-                                         h.d_pairB, h.n_nodes, ldl, h.row_bits);
+    k4_multi<2><<<blocks, 256, 0, s>>>(h.d_side, h.d_mblk, h.d_mslot0, h.d_slot_tr, h.n_multi, vals);
   else
-    k4_scatter<3><<<blocks, 256, 0, s>>>(local, vals, h.d_brow_ptr, h.d_bcnt, h.d_cstart, h.d_contrib, h.d_pairA,
-                                         h.d_pairB, h.n_nodes, ldl, h.row_bits);
+    k4_multi<3><<<blocks, 256, 0, s>>>(h.d_side, h.d_mblk, h.d_mslot0, h.d_slot_tr, h.n_multi, vals);
   return cudaGetLastError();
 }
 

@@ -112,8 +112,7 @@ __global__ void k1_table_rows(int n_patches, int n_g, int p, int q, int nk, int 
                               const int *__restrict__ row_patch, const int *__restrict__ pairA,
                               const int *__restrict__ pairB, const int *__restrict__ elspan,
                               const double *__restrict__ wD, const double *__restrict__ G,
-                              const double *__restrict__ Nc, double *__restrict__ table,
-                              double *__restrict__ tableT) {
+                              const double *__restrict__ Nc, double *__restrict__ table) {
   int64_t row = blockIdx.x;
   int pi = row_patch[row];
   const DevPatch &P = c_patches[pi];
@@ -157,8 +156,30 @@ __global__ void k1_table_rows(int n_patches, int n_g, int p, int q, int nk, int 
           }
         }
     table[row * kstride + kap] = acc;
-    tableT[(int64_t)kap * ldT + row] = acc;
   }
+}
+
+// Offline re-layout of the row-major table into the two fragment-major GEMM operands
+// (device_common.cuh fm_index): K3's A (rows = table rows, BR = IGA_K3_BM) and K5a's A
+// (rows = κ, reduction columns = table rows with each patch padded to 16, BR = 32W).
+__global__ void k1_pack(const double *__restrict__ table, int64_t M, int nk, int kstride,
+                        const int32_t *__restrict__ k5_col, double *__restrict__ tabA, int nkcA,
+                        double *__restrict__ tabAT, int brT, int nkcT) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= M * nk) return;
+  const int64_t r = idx / nk;
+  const int kap = (int)(idx % nk);
+  const double v = table[r * kstride + kap];
+  tabA[fm_index(r, kap, IGA_K3_BM, nkcA)] = v;
+  tabAT[fm_index(kap, k5_col[r], brT, nkcT)] = v;
+}
+
+cudaError_t launch_pack_tables(const Handle &h, cudaStream_t s) {
+  const int64_t n = h.M * h.nk;
+  k1_pack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.d_table, h.M, h.nk, h.kstride, h.d_k5_col, h.d_tabA,
+                                                      h.kstride / IGA_KCHUNK, h.d_tabAT, IGA_K3_BM,
+                                                      (int)(h.Kp / IGA_KCHUNK));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tables(const Handle &h, const DevPatch *dpatches, int n_patches, const double *d_tile_ctrl,
@@ -191,10 +212,10 @@ cudaError_t launch_tables(const Handle &h, const DevPatch *dpatches, int n_patch
   int tpb = h.nk >= 256 ? 256 : 128;
   if (h.d == 2)
     k1_table_rows<2><<<(unsigned)h.M, tpb, 0, s>>>(n_patches, h.n_g, h.p, h.q, h.nk, h.kstride, h.M, (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK, row_patch,
-                                                   h.d_pairA, h.d_pairB, d_tile_elspan, wD, G, Nc, h.d_table, h.d_tableT);
+                                                   h.d_pairA, h.d_pairB, d_tile_elspan, wD, G, Nc, h.d_table);
   else
     k1_table_rows<3><<<(unsigned)h.M, tpb, 0, s>>>(n_patches, h.n_g, h.p, h.q, h.nk, h.kstride, h.M, (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK, row_patch,
-                                                   h.d_pairA, h.d_pairB, d_tile_elspan, wD, G, Nc, h.d_table, h.d_tableT);
+                                                   h.d_pairA, h.d_pairB, d_tile_elspan, wD, G, Nc, h.d_table);
   if ((e = cudaGetLastError())) return e;
   cudaFreeAsync(wD, s);
   cudaFreeAsync(G, s);
