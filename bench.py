@@ -9,7 +9,7 @@ the paper and reported separately (`offline`).
 
 Timing: W warm-up steps, then K steps bracketed by barrier + cuda synchronize, CUDA
 events on the launching stream, max over ranks.  The working set (CSR values 22.9 GB,
-local values 12 GB) is >> the 126 MB L2, so no explicit flush is needed.
+X 12 GB) is >> the 126 MB L2, so no explicit flush is needed.
 Per-kernel device times come from libiga's own CUDA events on the same stream
 (iga_set_profiling) over the timed region.
 
@@ -120,11 +120,19 @@ class ClockSampler:
 def algorithmic(prob, s, sens):
     """Algorithmic work per launch."""
     d = prob.d
-    N = s.n_tiles * d * d
+    dd = d * d
+    N = s.n_tiles * dd
     gemm = 2.0 * s.n_local_rows * s.n_k * N                       # unpadded K = d² n_pi
-    k2_bytes = 8.0 * (s.n_tiles * s.n_k * d * d + s.n_tiles + s.n_macro_cp * d)
-    k4_bytes = 8.0 * s.n_local_rows * N + 8.0 * s.nnz + 4.0 * s.n_contrib + 1.0 * s.n_blocks + 16.0 * s.n_nodes
-    return dict(k3_flops=gemm, k5a_flops=gemm if sens else 0.0, k2_bytes=k2_bytes, k4_bytes=k4_bytes)
+    k2_bytes = 8.0 * (s.n_tiles * s.n_k * dd + s.n_tiles + s.n_macro_cp * d)
+    # K3 epilogue: CSR writes of the single-contribution blocks, side-slot writes, rank map
+    multi_vals = 2.0 * s.n_multi_blocks * dd                      # (I,J) and (J,I) (diag: once, ignored)
+    k3_bytes = 8.0 * (s.nnz - multi_vals) + 8.0 * dd * s.n_side_slots + 4.0 * s.n_local_rows * s.n_tiles
+    # K4: side-slot reads + the multi blocks' CSR writes + their descriptors
+    k4_bytes = 8.0 * dd * s.n_side_slots + 8.0 * multi_vals + 28.0 * s.n_multi_blocks + 1.0 * s.n_side_slots
+    # K5x: X writes (rows x tiles x d²) + u, v reads
+    k5x_bytes = 8.0 * s.n_local_rows * N + 16.0 * s.n_dof
+    return dict(k3_flops=gemm, k5a_flops=gemm if sens else 0.0, k2_bytes=k2_bytes, k3_bytes=k3_bytes,
+                k4_bytes=k4_bytes, k5x_bytes=k5x_bytes if sens else 0.0)
 
 
 def load_traffic():
@@ -279,17 +287,20 @@ def run_ours(args, rank, world):
 
     alg = algorithmic(prob, s, sens)
     per = lambda slot: kms[slot] / max(kn[slot], 1)
-    k3_ms, k5a_ms, k2_ms, k4_ms = per(1), per(3), per(0), per(2)
+    k3_ms, k5a_ms, k2_ms, k4_ms, k5x_ms = per(1), per(3), per(0), per(2), per(7)
     traffic = load_traffic()
     rooflines = {
-        "K3_contraction": {"bound": "tensor", "achieved": alg["k3_flops"] / (k3_ms * 1e-3) / 1e12,
-                           "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "ms": k3_ms},
+        "K3_contraction_scatter": {"bound": "tensor", "achieved": alg["k3_flops"] / (k3_ms * 1e-3) / 1e12,
+                                   "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "ms": k3_ms,
+                                   "epilogue_hbm_gbs": alg["k3_bytes"] / (k3_ms * 1e-3) / 1e9},
         "K2_interpolation": {"bound": "hbm", "achieved": alg["k2_bytes"] / (k2_ms * 1e-3) / 1e9,
                              "peak": None, "unit": "GB/s", "ms": k2_ms},
-        "K4_scatter": {"bound": "hbm", "achieved": alg["k4_bytes"] / (k4_ms * 1e-3) / 1e9,
-                       "peak": None, "unit": "GB/s", "ms": k4_ms},
+        "K4_multi_gather": {"bound": "hbm", "achieved": alg["k4_bytes"] / (k4_ms * 1e-3) / 1e9,
+                            "peak": None, "unit": "GB/s", "ms": k4_ms},
     }
     if sens:
+        rooflines["K5x_generate_X"] = {"bound": "hbm", "achieved": alg["k5x_bytes"] / (k5x_ms * 1e-3) / 1e9,
+                                       "peak": None, "unit": "GB/s", "ms": k5x_ms}
         rooflines["K5a_W_gemm"] = {"bound": "tensor", "achieved": alg["k5a_flops"] / (k5a_ms * 1e-3) / 1e12,
                                    "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "ms": k5a_ms}
         rooflines["K5b_reverse"] = {"ms": per(4)}
@@ -300,13 +311,14 @@ def run_ours(args, rank, world):
     except Exception:
         hbm = None
     hbm = hbm or 6650.0
-    for k in ("K2_interpolation", "K4_scatter"):
-        rooflines[k]["peak"] = hbm
+    for k in ("K2_interpolation", "K4_multi_gather", "K5x_generate_X"):
+        if k in rooflines:
+            rooflines[k]["peak"] = hbm
     for k, r in rooflines.items():
         if r.get("peak"):
             r["frac"] = r["achieved"] / r["peak"]
-    dom = rooflines["K3_contraction"]
-    roofline = {"bound": "tensor", "kernel": "K3_contraction (FP64 DMMA)", "achieved": dom["achieved"],
+    dom = rooflines["K3_contraction_scatter"]
+    roofline = {"bound": "tensor", "kernel": "K3 contraction (FP64 DMMA) + fused CSR scatter", "achieved": dom["achieved"],
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": dom["frac"],
                 "traffic": traffic.get("K3_dram_bytes_per_launch"),
                 "peak_source": "measured DMMA ceiling, profiles/r01_fp64_ceiling.md (MEASURED_PEAKS.json has no FP64 entry)",
@@ -321,9 +333,10 @@ def run_ours(args, rank, world):
                        "l2": "working set >> 126 MB L2 (CSR values alone 8*nnz bytes); no explicit flush"},
             "nnz_per_s": nnz_per_s, "roofline": roofline, "rooflines_all": rooflines,
             "clocks": clk, "e2e": e2e,
-            "gpu_launches": int(args.steps * (3 + (3 if sens else 0))),
-            "kernel_ms_per_step": {"K2": k2_ms, "K3": k3_ms, "K4": k4_ms, "K5a": k5a_ms if sens else 0.0,
-                                   "K5b": per(4) if sens else 0.0, "K5c": per(5) if sens else 0.0},
+            "gpu_launches": int(args.steps * (3 + (4 if sens else 0))),
+            "kernel_ms_per_step": {"K2": k2_ms, "K3": k3_ms, "K4": k4_ms, "K5x": k5x_ms if sens else 0.0,
+                                   "K5a": k5a_ms if sens else 0.0, "K5b": per(4) if sens else 0.0,
+                                   "K5c": per(5) if sens else 0.0},
             "offline": {"build_s (host topology + K1 tables + pattern)": build_s}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_t, dt, cores, nnz = cpu_baseline_oracle(sens=sens)

@@ -23,7 +23,8 @@
 // K3: persistent (one CTA per SM), CTA tile 128 rows × 72 columns (8 tiles in 3D),
 //   8 MMA warps of 16×72 (2×9 DMMA tiles), 4 epilogue warps that scatter the previous
 //   tile while the MMA warps compute the next; MMA warp 0 refills the 4-stage ring with
-//   bulk copies once all MMA warps released a stage.  Work order M-blocks fastest: the
+//   bulk copies once all MMA warps released a stage (an mbarrier wait: measured faster
+//   here than letting the last releasing warp refill, which K5a uses).  Work order M-blocks fastest: the
 //   resident CTAs share one coefficient block and the table stays L2-resident.
 // K5a: CTA 128 κ-rows × 72 columns, 8 MMA warps of 16×72, 4 warps generating X into a
 //   4-stage ring (one of their lanes streams the table); long reduction over all rows.
@@ -294,19 +295,22 @@ cudaError_t launch_contraction(const Handle &h, double *vals, double *local, cud
 // (measured: 27.9 ms vs 22.7 ms for the GEMM alone at cfg5, profiles/r01_*).
 
 // X[col][(t,a,b)] for the tile patch of grid.x and the 72 columns of N-block grid.y;
-// chunk kc of the patch is written as one contiguous FM chunk (coalesced).
+// chunk kc of the patch is written as one contiguous FM chunk (coalesced).  Thread
+// (warp w, lane) owns row k = 4w + lane%4 of every chunk and the 9 columns
+// n_j = 8j + lane/4, i.e. FM elements e = 128j + 32w + lane: one pair per chunk, the
+// per-column offsets are loop invariants.
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, const int32_t *__restrict__ node_map,
         int nl, const double *__restrict__ u, const double *__restrict__ v, int64_t n_tiles, int nkc,
         double *__restrict__ X) {
   constexpr int DD = D * D, TPC = BN / DD;
   extern __shared__ __align__(16) double smem[];
-  const int p = blockIdx.x;
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const int64_t nb = blockIdx.y, t0 = nb * TPC;
   const int kc0 = pinfo[3 * p], kc1 = pinfo[3 * (p + 1)], off = pinfo[3 * p + 1], nc = pinfo[3 * p + 2];
   double *us = smem, *vs = smem + TPC * nc * D;
-  for (int i = threadIdx.x; i < TPC * nc; i += blockDim.x) {
+  for (int i = tid; i < TPC * nc; i += 128) {
     const int tl = i / nc, A = i % nc;
     const int64_t t = t0 + tl;
     double *uo = us + i * D, *vo = vs + i * D;
@@ -319,23 +323,37 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
       for (int a = 0; a < D; ++a) { uo[a] = 0.0; vo[a] = 0.0; }
     }
   }
+  const int k = 4 * (tid >> 5) + (lane & 3);
+  int cA[NI], cB[NI];
+  double fdiag[NI];
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    const int n = 8 * j + (lane >> 2), tl = n / DD, ab = n % DD, a = ab / D, b = ab % D;
+    cA[j] = tl * nc * D + a;
+    cB[j] = tl * nc * D + b;
+    fdiag[j] = a < b ? 1.0 : (a == b ? 0.5 : 0.0);
+  }
   __syncthreads();
+  int32_t pr = k5_pair[(int64_t)kc0 * BK + k];
   for (int kc = kc0; kc < kc1; ++kc) {
-    double *dst = X + (nb * nkc + kc) * (int64_t)K5_X_CHUNK_;
-    for (int e = threadIdx.x; e < K5_X_CHUNK_; e += blockDim.x) {
-      const int g = e >> 7, kk = (e >> 5) & 3, l = e & 31;
-      const int n = g * 8 + (l >> 2), k = kk * 4 + (l & 3);
-      const int tl = n / DD, ab = n % DD, a = ab / D, b = ab % D;
-      const int32_t pr = k5_pair[(int64_t)kc * BK + k];
-      double x = 0.0;
-      if (pr >= 0) {
-        const int A = pr & 0xffff, B = pr >> 16;
-        const double *ub = us + tl * nc * D, *vb = vs + tl * nc * D;
-        x = fma(ub[B * D + b], vb[A * D + a], ub[A * D + a] * vb[B * D + b]);
-        if (A == B) x = a < b ? x : (a == b ? 0.5 * x : 0.0);
+    const int32_t pr_next = kc + 1 < kc1 ? k5_pair[(int64_t)(kc + 1) * BK + k] : -1;
+    double *dst = X + (nb * nkc + kc) * (int64_t)K5_X_CHUNK_ + tid;
+    double x[NI];
+    if (pr >= 0) {
+      const int A = (pr & 0xffff) * D, B = (pr >> 16) * D;
+#pragma unroll
+      for (int j = 0; j < NI; ++j) x[j] = fma(us[cB[j] + B], vs[cA[j] + A], us[cA[j] + A] * vs[cB[j] + B]);
+      if (A == B) {
+#pragma unroll
+        for (int j = 0; j < NI; ++j) x[j] *= fdiag[j];
       }
-      dst[e] = x;
+    } else {
+#pragma unroll
+      for (int j = 0; j < NI; ++j) x[j] = 0.0;
     }
+#pragma unroll
+    for (int j = 0; j < NI; ++j) dst[128 * j] = x[j];
+    pr = pr_next;
   }
 }
 
@@ -344,7 +362,7 @@ constexpr int K5_A_CHUNK = BM * BK, K5_B_CHUNK = BN * BK;   // doubles
 constexpr int K5_WP = BM + 1;                                // W staging pitch
 constexpr int K5_THREADS = 32 * N_MMA_WARPS;
 constexpr size_t K5_OFF_BAR = sizeof(double) * (size_t)K5_STAGES * (K5_A_CHUNK + K5_B_CHUNK);
-constexpr size_t K5_SMEM = K5_OFF_BAR + 2 * K5_STAGES * sizeof(uint64_t);
+constexpr size_t K5_SMEM = K5_OFF_BAR + K5_STAGES * (sizeof(uint64_t) + sizeof(int));
 static_assert(sizeof(double) * BN * K5_WP <= K5_OFF_BAR, "W staging must fit in the stages");
 
 // W[n][κ] = Σ_col tabAT[κ][col] X[col][n]: CTA = 128 κ rows × 72 columns, 8 MMA warps of
@@ -355,21 +373,20 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K5_STAGES * K5_A_CHUNK;
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5_OFF_BAR);
-  uint64_t *empty = full + K5_STAGES;
+  int *released = reinterpret_cast<int *>(full + K5_STAGES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t kb = blockIdx.x, nb = blockIdx.y;
   const double *gA = tabAT + kb * (int64_t)nkc * K5_A_CHUNK, *gB = X + nb * (int64_t)nkc * K5_B_CHUNK;
   if (tid == 0) {
     for (int s = 0; s < K5_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], N_MMA_WARPS);
+      released[s] = 0;
     }
     mbar_fence_init();
   }
   __syncthreads();
-  auto produce = [&](int kc) {
+  auto produce = [&](int kc) {   // the last MMA warp to release a stage refills it
     const int st = kc % K5_STAGES;
-    if (kc >= K5_STAGES) mbar_wait(&empty[st], ((kc / K5_STAGES) & 1) ^ 1);
     mbar_expect_tx(&full[st], (K5_A_CHUNK + K5_B_CHUNK) * 8);
     bulk_g2s(sA + st * K5_A_CHUNK, gA + (int64_t)kc * K5_A_CHUNK, K5_A_CHUNK * 8, &full[st]);
     bulk_g2s(sB + st * K5_B_CHUNK, gB + (int64_t)kc * K5_B_CHUNK, K5_B_CHUNK * 8, &full[st]);
@@ -386,8 +403,14 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
     mbar_wait(&full[st], (kc / K5_STAGES) & 1);
     mma_chunk_fm<BK / 4>(sA + st * K5_A_CHUNK, sB + st * K5_B_CHUNK, warp * MI, lane, acc);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-    if (tid == 0 && kc + K5_STAGES < nkc) produce(kc + K5_STAGES);
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&released[st], 1) == N_MMA_WARPS - 1) {
+        released[st] = 0;
+        __threadfence_block();
+        if (kc + K5_STAGES < nkc) produce(kc + K5_STAGES);
+      }
+    }
   }
   __syncthreads();   // all stages consumed: stage W[n][κ] in shared memory
   double *sW = smem;
@@ -419,7 +442,7 @@ static cudaError_t launch_k5x(const Handle &h, const double *u, const double *v,
   if (e) return e;
   dim3 grid((unsigned)h.n_patches, (unsigned)(h.Npad / BN));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k5x_gen<D><<<grid, 256, smem, s>>>(h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, u, v, h.n_tiles,
+  k5x_gen<D><<<grid, 128, smem, s>>>(h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, u, v, h.n_tiles,
                                      (int)(h.Kp / BK), h.d_X);
   return cudaGetLastError();
 }

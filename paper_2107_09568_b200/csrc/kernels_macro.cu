@@ -38,20 +38,20 @@ InterpConst make_interp_const(const Handle &h) {
 // Shared per-tile macro data: 1D basis at the nodes and the active control points.
 template <int D>
 struct MacroTile {
-  double B1[3][IGA_MAXQ + 1][IGA_MAXP + 1];
-  double D1[3][IGA_MAXQ + 1][IGA_MAXP + 1];   // derivative w.r.t. ξ_k (includes span length)
-  double P[(IGA_MAXP + 1) * (IGA_MAXP + 1) * (IGA_MAXP + 1) * 3];
+  double B1[D][IGA_MAXQ + 1][IGA_MAXP + 1];
+  double D1[D][IGA_MAXQ + 1][IGA_MAXP + 1];   // derivative w.r.t. ξ_k (includes span length)
+  double P[(D == 2 ? (IGA_MAXP + 1) * (IGA_MAXP + 1) : (IGA_MAXP + 1) * (IGA_MAXP + 1) * (IGA_MAXP + 1)) * D];
   int nact;
 };
 
 template <int D>
 __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64_t t, const double *__restrict__ ctrl,
-                                const double *__restrict__ mknots, const int *__restrict__ mspan) {
+                                const double *__restrict__ mknots, const int *__restrict__ mspan,
+                                int tid = threadIdx.x, int nthr = blockDim.x) {
   const int q = c_ip.q;
   int e[3] = {0, 0, 0};
   int64_t tmp = t;
   for (int k = 0; k < D; ++k) { e[k] = (int)(tmp % c_ip.mel[k]); tmp /= c_ip.mel[k]; }
-  int tid = threadIdx.x;
   if (tid < D * (q + 1)) {
     int k = tid / (q + 1), m = tid % (q + 1);
     const double *U = mknots + c_ip.moff[k];
@@ -67,7 +67,7 @@ __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   int nact = n1[0] * n1[1] * n1[2];
   if (tid == 0) mt.nact = nact;
-  for (int idx = tid; idx < nact * D; idx += blockDim.x) {
+  for (int idx = tid; idx < nact * D; idx += nthr) {
     int ra = idx / D, a = idx % D;
     int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
     int64_t cp = 0;
@@ -107,156 +107,260 @@ __device__ __forceinline__ void lame(double E, double nu, double &lam, double &m
   mu = E / (2.0 * (1.0 + nu));
 }
 
-// apply the 1D operator Op (row c, col m: out[c] = Σ_m Op[c][m] in[m], or its transpose)
-// along direction `dir` of an (q+1)^D × ncomp array in shared memory.
-template <int D>
-__device__ void tensor_pass(const InterpConst &c_ip, const double *in, double *out, int dir, int ncomp, bool transpose) {
-  const int q1 = c_ip.q + 1;
-  int npi = 1;
-  for (int k = 0; k < D; ++k) npi *= q1;
-  int stride = 1;
-  for (int k = 0; k < dir; ++k) stride *= q1;
-  for (int idx = threadIdx.x; idx < npi * ncomp; idx += blockDim.x) {
-    int C = idx / ncomp, comp = idx % ncomp;
-    int c = (C / stride) % q1;
-    int base = C - c * stride;
+// apply the 1D operator Π1 = V1⁻¹ (or its transpose) along direction DIR of an
+// (Q+1)^D × NCOMP array in shared memory; every index is a compile-time constant.
+template <int D, int Q, int DIR, bool TRANSPOSE, int NCOMP>
+__device__ __forceinline__ void tensor_pass(const InterpConst &c_ip, const double *in, double *out) {
+  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
+  constexpr int STRIDE = DIR == 0 ? 1 : (DIR == 1 ? Q1 : Q1 * Q1);
+  for (int idx = threadIdx.x; idx < NPI * NCOMP; idx += blockDim.x) {
+    const int C = idx / NCOMP, comp = idx - C * NCOMP;
+    const int c = (C / STRIDE) % Q1;
+    const double *src = in + (C - c * STRIDE) * NCOMP + comp;
     double acc = 0.0;
-    for (int m = 0; m < q1; ++m) {
-      double op = transpose ? c_ip.Pi1[m * q1 + c] : c_ip.Pi1[c * q1 + m];
-      acc += op * in[(base + m * stride) * ncomp + comp];
-    }
+#pragma unroll
+    for (int m = 0; m < Q1; ++m)
+      acc = fma(TRANSPOSE ? c_ip.Pi1[m * Q1 + c] : c_ip.Pi1[c * Q1 + m], src[m * STRIDE * NCOMP], acc);
     out[idx] = acc;
   }
 }
 
-template <int D>
-__global__ void k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
-                               const int *__restrict__ mspan, const double *__restrict__ young, int ypt,
-                               double nu, double *__restrict__ coef, int kstride, int fm, int *flag) {
-  extern __shared__ double sm[];
-  __shared__ MacroTile<D> mt;
-  const int64_t t = blockIdx.x;
-  const int q1 = c_ip.q + 1;
-  int npi = 1;
-  for (int k = 0; k < D; ++k) npi *= q1;
-  constexpr int DD = D * D, NC = DD * DD;
-  double *S0 = sm, *S1 = sm + npi * NC;
-  load_macro_tile<D>(c_ip, mt, t, ctrl, mknots, mspan);
+template <int D, int Q, bool TRANSPOSE, int NCOMP>
+__device__ __forceinline__ const double *tensor_apply(const InterpConst &c_ip, double *a, double *b) {
+  tensor_pass<D, Q, 0, TRANSPOSE, NCOMP>(c_ip, a, b);
   __syncthreads();
-  double E = young[ypt ? t : 0], lam, mu;
-  lame(E, nu, lam, mu);
-  for (int m = threadIdx.x; m < npi; m += blockDim.x) {
+  tensor_pass<D, Q, 1, TRANSPOSE, NCOMP>(c_ip, b, a);
+  __syncthreads();
+  if (D == 2) return a;
+  tensor_pass<D, Q, 2, TRANSPOSE, NCOMP>(c_ip, a, b);
+  __syncthreads();
+  return b;
+}
+
+// per-node geometry: G = J⁻¹ (rows ǧ_i), det J, gg = G Gᵀ
+template <int D>
+struct NodeGeo {
+  double G[D][D], gg[D][D], det;
+};
+
+template <int D, int Q>
+__device__ __forceinline__ void node_geometry(const InterpConst &c_ip, const MacroTile<D> &mt, NodeGeo<D> *geo,
+                                              int64_t t, int *flag) {
+  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
+  for (int m = threadIdx.x; m < NPI; m += blockDim.x) {
     double J[D][D], G[D][D];
     macro_J<D>(c_ip, mt, m, J);
-    double det = det_inv<D>(J, G);
+    const double det = det_inv<D>(J, G);
     if (!(det > 0.0)) raise_flag(flag, 2, (int)t, m);
-    double gg[D][D];
+    NodeGeo<D> &o = geo[m];
     for (int i = 0; i < D; ++i)
       for (int j = 0; j < D; ++j) {
+        o.G[i][j] = G[i][j];
         double v = 0.0;
         for (int c = 0; c < D; ++c) v += G[i][c] * G[j][c];
-        gg[i][j] = v;
+        o.gg[i][j] = v;
       }
-    double *o = S0 + m * NC;
-    for (int i = 0; i < D; ++i)
-      for (int j = 0; j < D; ++j)
-        for (int a = 0; a < D; ++a)
-          for (int b = 0; b < D; ++b)
-            o[(i * D + j) * DD + a * D + b] =
-                det * (lam * G[i][a] * G[j][b] + mu * G[j][a] * G[i][b] + (a == b ? mu * gg[i][j] : 0.0));
-  }
-  __syncthreads();
-  double *in = S0, *out = S1;
-  for (int dir = 0; dir < D; ++dir) {
-    tensor_pass<D>(c_ip, in, out, dir, NC, false);
-    __syncthreads();
-    double *tmp = in; in = out; out = tmp;
-  }
-  // coefficient row n = t*DD + ab, column κ = ij*npi + C: row-major coef[n*kstride + κ]
-  // (parity accessor) or the fragment-major K3 B operand (fm_index, BR = IGA_GEMM_BN)
-  const int nk = DD * npi;
-  for (int idx = threadIdx.x; idx < DD * nk; idx += blockDim.x) {
-    int ab = idx / nk, kap = idx % nk;
-    int ij = kap / npi, C = kap % npi;
-    const int64_t n = t * DD + ab;
-    const int64_t o = fm ? fm_index(n, kap, IGA_GEMM_BN, kstride / IGA_KCHUNK) : n * kstride + kap;
-    coef[o] = in[C * NC + ij * DD + ab];
+    o.det = det;
   }
 }
 
-template <int D>
-__global__ void k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
-                            const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
-                            const double *__restrict__ W, int kstride, double *__restrict__ gpart, int *flag) {
-  extern __shared__ double sm[];
+// K2: thread = (tile, Ā component (i,j,a,b)); TPB tiles per CTA.  Phases: macro data
+// per tile -> node geometry (one thread per node) -> each thread evaluates its component
+// of Ā (Eq. 37, closed form) at the (q+1)^d nodes into registers, applies (V1⁻¹)^{⊗d}
+// by D 1D passes in registers (all indices compile-time) and writes its (q+1)^d
+// interpolation coefficients.
+template <int D, int Q>
+struct K2Shape {
+  static constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, DD = D * D, NC = DD * DD;
+  static constexpr int TPB = D == 2 ? 16 : 4;   // tiles per CTA: 256 / 324 threads
+  static constexpr int THREADS = TPB * NC;
+  static constexpr bool REG = NPI <= 27;        // register path; larger q: shared-memory passes
+};
+
+template <int D, int Q>
+__global__ void __launch_bounds__(K2Shape<D, Q>::THREADS)
+k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
+               const int *__restrict__ mspan, const double *__restrict__ young, int ypt,
+               double nu, double *__restrict__ coef, int kstride, int fm, int64_t n_tiles, int *flag) {
+  using S = K2Shape<D, Q>;
+  static_assert(S::REG, "register path only for (q+1)^d <= 27");
+  constexpr int Q1 = S::Q1, NPI = S::NPI, DD = S::DD, NC = S::NC, TPB = S::TPB;
+  __shared__ MacroTile<D> mt[TPB];
+  __shared__ NodeGeo<D> geo[TPB][NPI];
+  const int tl = threadIdx.x / NC, comp = threadIdx.x % NC;
+  const int64_t t = (int64_t)blockIdx.x * TPB + tl;
+  const bool live = t < n_tiles;
+  if (live) load_macro_tile<D>(c_ip, mt[tl], t, ctrl, mknots, mspan, comp, NC);
+  __syncthreads();
+  if (live)
+    for (int m = comp; m < NPI; m += NC) {
+      double J[D][D], G[D][D];
+      macro_J<D>(c_ip, mt[tl], m, J);
+      const double det = det_inv<D>(J, G);
+      if (!(det > 0.0)) raise_flag(flag, 2, (int)t, m);
+      NodeGeo<D> &o = geo[tl][m];
+      for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+          o.G[i][j] = G[i][j];
+          double v = 0.0;
+          for (int c = 0; c < D; ++c) v += G[i][c] * G[j][c];
+          o.gg[i][j] = v;
+        }
+      o.det = det;
+    }
+  __syncthreads();
+  if (!live) return;
+  double lam, mu;
+  lame(young[ypt ? t : 0], nu, lam, mu);
+  const int ij = comp / DD, ab = comp % DD, i = ij / D, j = ij % D, a = ab / D, b = ab % D;
+  double x[NPI], y[NPI];
+#pragma unroll
+  for (int m = 0; m < NPI; ++m) {
+    const NodeGeo<D> &g = geo[tl][m];
+    x[m] = g.det * (lam * g.G[i][a] * g.G[j][b] + mu * g.G[j][a] * g.G[i][b] + (a == b ? mu * g.gg[i][j] : 0.0));
+  }
+  // direction 0, 1 (, 2): out[c] = Σ_m Π1[c][m] in[m] along the direction
+#pragma unroll
+  for (int C = 0; C < NPI; ++C) {
+    const int c = C % Q1, base = C - c;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[c * Q1 + m], x[base + m], acc);
+    y[C] = acc;
+  }
+#pragma unroll
+  for (int C = 0; C < NPI; ++C) {
+    const int c = (C / Q1) % Q1, base = C - c * Q1;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[c * Q1 + m], y[base + m * Q1], acc);
+    x[C] = acc;
+  }
+  if (D == 3) {
+#pragma unroll
+    for (int C = 0; C < NPI; ++C) {
+      const int c = C / (Q1 * Q1), base = C - c * Q1 * Q1;
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[c * Q1 + m], x[base + m * Q1 * Q1], acc);
+      y[C] = acc;
+    }
+  }
+  const double *res = D == 3 ? y : x;
+  // coefficient row n = t*DD + ab, column κ = ij*npi + C: row-major coef[n*kstride + κ]
+  // (parity accessor) or the fragment-major K3 B operand (fm_index, BR = IGA_GEMM_BN)
+  const int64_t n = t * DD + ab;
+#pragma unroll
+  for (int C = 0; C < NPI; ++C) {
+    const int kap = ij * NPI + C;
+    coef[fm ? fm_index(n, kap, IGA_GEMM_BN, kstride / IGA_KCHUNK) : n * kstride + kap] = res[C];
+  }
+}
+
+// K2 for (q+1)^d > 27 (3D, q >= 3): one CTA per tile, component arrays in shared memory.
+template <int D, int Q>
+__global__ void __launch_bounds__(256)
+k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl,
+                    const double *__restrict__ mknots, const int *__restrict__ mspan, const double *__restrict__ young,
+                    int ypt, double nu, double *__restrict__ coef, int kstride, int fm, int64_t n_tiles, int *flag) {
+  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
+  constexpr int DD = D * D, NC = DD * DD, NK = DD * NPI;
+  extern __shared__ double dyn[];
+  double *S0 = dyn, *S1 = dyn + NPI * NC;
   __shared__ MacroTile<D> mt;
+  __shared__ NodeGeo<D> geo[NPI];
   const int64_t t = blockIdx.x;
-  const int q1 = c_ip.q + 1;
-  int npi = 1;
-  for (int k = 0; k < D; ++k) npi *= q1;
-  constexpr int DD = D * D, NC = DD * DD;
-  double *S0 = sm, *S1 = sm + npi * NC, *dSdJ = sm + 2 * npi * NC;
   load_macro_tile<D>(c_ip, mt, t, ctrl, mknots, mspan);
-  const int nk = DD * npi;
+  __syncthreads();
+  node_geometry<D, Q>(c_ip, mt, geo, t, flag);
+  double lam, mu;
+  lame(young[ypt ? t : 0], nu, lam, mu);
+  __syncthreads();
+  for (int it = threadIdx.x; it < NPI * DD; it += blockDim.x) {   // Ā (Eq. 37, closed form)
+    const int m = it / DD, ij = it % DD, i = ij / D, j = ij % D;
+    const NodeGeo<D> &g = geo[m];
+    double *o = S0 + m * NC + ij * DD;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        o[a * D + b] = g.det * (lam * g.G[i][a] * g.G[j][b] + mu * g.G[j][a] * g.G[i][b] + (a == b ? mu * g.gg[i][j] : 0.0));
+  }
+  __syncthreads();
+  const double *res = tensor_apply<D, Q, false, NC>(c_ip, S0, S1);
+  for (int idx = threadIdx.x; idx < DD * NK; idx += blockDim.x) {
+    const int ab = idx / NK, kap = idx % NK, ij = kap / NPI, C = kap % NPI;
+    const int64_t n = t * DD + ab;
+    const int64_t o = fm ? fm_index(n, kap, IGA_GEMM_BN, kstride / IGA_KCHUNK) : n * kstride + kap;
+    coef[o] = res[C * NC + ij * DD + ab];
+  }
+}
+
+// K5b: one CTA per tile: Ŵ = Πᵀ W, reverse mode of S = ⟨Ŵ, Ā(J)⟩ per node, chain to the
+// active macro control points.
+template <int D, int Q>
+__global__ void __launch_bounds__(256)
+k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
+            const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
+            const double *__restrict__ W, int kstride, double *__restrict__ gpart, int *flag) {
+  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
+  constexpr int DD = D * D, NC = DD * DD, NK = DD * NPI;
+  extern __shared__ double dyn[];
+  double *S0 = dyn, *S1 = dyn + NPI * NC, *dSdJ = dyn + 2 * NPI * NC;
+  __shared__ MacroTile<D> mt;
+  __shared__ NodeGeo<D> geo[NPI];
+  const int64_t t = blockIdx.x;
+  load_macro_tile<D>(c_ip, mt, t, ctrl, mknots, mspan);
   const double *src = W + (size_t)t * DD * kstride;
-  for (int idx = threadIdx.x; idx < DD * nk; idx += blockDim.x) {
-    int ab = idx / nk, kap = idx % nk;
-    int ij = kap / npi, C = kap % npi;
+  for (int idx = threadIdx.x; idx < DD * NK; idx += blockDim.x) {
+    const int ab = idx / NK, kap = idx % NK, ij = kap / NPI, C = kap % NPI;
     S0[C * NC + ij * DD + ab] = src[(size_t)ab * kstride + kap];
   }
   __syncthreads();
-  double *in = S0, *out = S1;
-  for (int dir = 0; dir < D; ++dir) {   // Ŵ = Πᵀ W (transposed 1D operator per direction)
-    tensor_pass<D>(c_ip, in, out, dir, NC, true);
-    __syncthreads();
-    double *tmp = in; in = out; out = tmp;
-  }
-  double E = young[ypt ? t : 0], lam, mu;
-  lame(E, nu, lam, mu);
-  for (int m = threadIdx.x; m < npi; m += blockDim.x) {
-    const double *Wh = in + m * NC;   // Ŵ[ij*DD + ab]
-    double J[D][D], G[D][D];
-    macro_J<D>(c_ip, mt, m, J);
-    double det = det_inv<D>(J, G);
-    if (!(det > 0.0)) raise_flag(flag, 2, (int)t, m);
-    double T1 = 0, T2 = 0, T3 = 0, w[D][D], gg[D][D];
+  node_geometry<D, Q>(c_ip, mt, geo, t, flag);
+  const double *Wh_all = tensor_apply<D, Q, true, NC>(c_ip, S0, S1);   // Ŵ = Πᵀ W (also syncs geo)
+  double lam, mu;
+  lame(young[ypt ? t : 0], nu, lam, mu);
+  for (int m = threadIdx.x; m < NPI; m += blockDim.x) {
+    const double *Wh = Wh_all + m * NC;   // Ŵ[ij*DD + ab]
+    const NodeGeo<D> &g = geo[m];
+    const double det = g.det;
+    double T1 = 0, T2 = 0, T3 = 0, w[D][D];
     for (int i = 0; i < D; ++i)
       for (int j = 0; j < D; ++j) {
-        double s = 0.0, v = 0.0;
-        for (int a = 0; a < D; ++a) s += Wh[(i * D + j) * DD + a * D + a];
-        for (int c = 0; c < D; ++c) v += G[i][c] * G[j][c];
-        w[i][j] = s;
-        gg[i][j] = v;
-        T3 += s * v;
+        double sd = 0.0;
+        for (int a = 0; a < D; ++a) sd += Wh[(i * D + j) * DD + a * D + a];
+        w[i][j] = sd;
+        T3 += sd * g.gg[i][j];
         for (int a = 0; a < D; ++a)
           for (int b = 0; b < D; ++b) {
-            double x = Wh[(i * D + j) * DD + a * D + b];
-            T1 += x * G[i][a] * G[j][b];
-            T2 += x * G[j][a] * G[i][b];
+            const double x = Wh[(i * D + j) * DD + a * D + b];
+            T1 += x * g.G[i][a] * g.G[j][b];
+            T2 += x * g.G[j][a] * g.G[i][b];
           }
       }
-    double S = det * (lam * T1 + mu * T2 + mu * T3);
-    double Q[D][D];
+    const double S = det * (lam * T1 + mu * T2 + mu * T3);
+    double Q_[D][D];
     for (int mi = 0; mi < D; ++mi)
       for (int n = 0; n < D; ++n) {
         double d1 = 0, d2 = 0, d3 = 0;
         for (int j = 0; j < D; ++j)
           for (int b = 0; b < D; ++b) {
-            d1 += Wh[(mi * D + j) * DD + n * D + b] * G[j][b];   // Σ_{j,b} Ŵ_{mj,nb} G_jb
-            d1 += Wh[(j * D + mi) * DD + b * D + n] * G[j][b];   // Σ_{i,a} Ŵ_{im,an} G_ia
-            d2 += Wh[(j * D + mi) * DD + n * D + b] * G[j][b];   // Σ_{i,b} Ŵ_{im,nb} G_ib
-            d2 += Wh[(mi * D + j) * DD + b * D + n] * G[j][b];   // Σ_{j,a} Ŵ_{mj,an} G_ja
+            d1 += Wh[(mi * D + j) * DD + n * D + b] * g.G[j][b];   // Σ_{j,b} Ŵ_{mj,nb} G_jb
+            d1 += Wh[(j * D + mi) * DD + b * D + n] * g.G[j][b];   // Σ_{i,a} Ŵ_{im,an} G_ia
+            d2 += Wh[(j * D + mi) * DD + n * D + b] * g.G[j][b];   // Σ_{i,b} Ŵ_{im,nb} G_ib
+            d2 += Wh[(mi * D + j) * DD + b * D + n] * g.G[j][b];   // Σ_{j,a} Ŵ_{mj,an} G_ja
           }
-        for (int j = 0; j < D; ++j) d3 += (w[mi][j] + w[j][mi]) * G[j][n];
-        Q[mi][n] = det * (lam * d1 + mu * d2 + mu * d3);
+        for (int j = 0; j < D; ++j) d3 += (w[mi][j] + w[j][mi]) * g.G[j][n];
+        Q_[mi][n] = det * (lam * d1 + mu * d2 + mu * d3);
       }
     // ∂S/∂J[a][β] = S G[β][a] - Σ_{i,n} G[i][a] Q[i][n] G[β][n]
     double *o = dSdJ + m * DD;
     for (int a = 0; a < D; ++a)
       for (int be = 0; be < D; ++be) {
-        double v = S * G[be][a];
+        double v = S * g.G[be][a];
         for (int i = 0; i < D; ++i)
-          for (int n = 0; n < D; ++n) v -= G[i][a] * Q[i][n] * G[be][n];
+          for (int n = 0; n < D; ++n) v -= g.G[i][a] * Q_[i][n] * g.G[be][n];
         o[a * D + be] = v;
       }
   }
@@ -264,11 +368,11 @@ __global__ void k5b_reverse(const __grid_constant__ InterpConst c_ip, const doub
   // chain to the active control points: g[r][a] = Σ_m Σ_β ∂S/∂J[a][β] ∂_β N_r(ξ_m)
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   for (int idx = threadIdx.x; idx < mt.nact * D; idx += blockDim.x) {
-    int ra = idx / D, a = idx % D;
-    int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
+    const int ra = idx / D, a = idx % D;
+    const int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
     double acc = 0.0;
-    for (int m = 0; m < npi; ++m) {
-      int mm[3] = {m % q1, (m / q1) % q1, m / (q1 * q1)};
+    for (int m = 0; m < NPI; ++m) {
+      const int mm[3] = {m % Q1, (m / Q1) % Q1, m / (Q1 * Q1)};
       for (int be = 0; be < D; ++be) {
         double v = 1.0;
         for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
@@ -316,35 +420,61 @@ __global__ void k5c_reduce(const __grid_constant__ InterpConst c_ip, const int *
   grad[idx] = acc;
 }
 
-static size_t macro_smem(const Handle &h, int extra_per_node) {
-  int npi = h.npi, dd = h.d * h.d;
-  return sizeof(double) * ((size_t)2 * npi * dd * dd + (size_t)npi * extra_per_node);
+template <int D, int Q>
+static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
+                             double *coef, bool fm, cudaStream_t s) {
+  using S = K2Shape<D, Q>;
+  if constexpr (S::REG) {
+    const unsigned grid = (unsigned)((h.n_tiles + S::TPB - 1) / S::TPB);
+    k2_interpolate<D, Q><<<grid, S::THREADS, 0, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt,
+                                                     nu, coef, h.kstride, (int)fm, h.n_tiles, h.d_flag);
+  } else {
+    const size_t sm = sizeof(double) * 2 * S::NPI * S::NC;
+    cudaError_t e = cudaFuncSetAttribute(k2_interpolate_smem<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+    k2_interpolate_smem<D, Q><<<(unsigned)h.n_tiles, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan,
+                                                                   young, ypt, nu, coef, h.kstride, (int)fm,
+                                                                   h.n_tiles, h.d_flag);
+  }
+  return cudaGetLastError();
 }
+
+template <int D, int Q>
+static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
+                              const double *W, double *gpart, cudaStream_t s) {
+  constexpr int NPI = D == 2 ? (Q + 1) * (Q + 1) : (Q + 1) * (Q + 1) * (Q + 1);
+  const size_t sm = sizeof(double) * (2 * NPI * D * D * D * D + NPI * D * D);
+  cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e) return e;
+  k5b_reverse<D, Q><<<(unsigned)h.n_tiles, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
+                                                        ypt, nu, W, h.kstride, gpart, h.d_flag);
+  return cudaGetLastError();
+}
+
+// dispatch on (d, q): every index of the macro kernels is a compile-time constant
+#define IGA_DISPATCH_DQ(F, ...)                                                          \
+  switch (h.d * 10 + h.q) {                                                               \
+    case 20: return F<2, 0>(__VA_ARGS__);                                                 \
+    case 21: return F<2, 1>(__VA_ARGS__);                                                 \
+    case 22: return F<2, 2>(__VA_ARGS__);                                                 \
+    case 23: return F<2, 3>(__VA_ARGS__);                                                 \
+    case 24: return F<2, 4>(__VA_ARGS__);                                                 \
+    case 30: return F<3, 0>(__VA_ARGS__);                                                 \
+    case 31: return F<3, 1>(__VA_ARGS__);                                                 \
+    case 32: return F<3, 2>(__VA_ARGS__);                                                 \
+    case 33: return F<3, 3>(__VA_ARGS__);                                                 \
+    case 34: return F<3, 4>(__VA_ARGS__);                                                 \
+    default: return cudaErrorInvalidValue;                                                \
+  }
 
 cudaError_t launch_interpolate(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
                                double *coef, bool fm, cudaStream_t s) {
-  size_t sm = macro_smem(h, 0);
-  if (h.d == 2) {
-    cudaFuncSetAttribute(k2_interpolate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k2_interpolate<2><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, coef, h.kstride, (int)fm, h.d_flag);
-  } else {
-    cudaFuncSetAttribute(k2_interpolate<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k2_interpolate<3><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, coef, h.kstride, (int)fm, h.d_flag);
-  }
-  return cudaGetLastError();
+  IGA_DISPATCH_DQ(launch_k2, h, ctrl, young, ypt, nu, coef, fm, s)
 }
 
 cudaError_t launch_sens_reverse(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
                                 const double *W, double *gpart, cudaStream_t s) {
-  size_t sm = macro_smem(h, h.d * h.d);
-  if (h.d == 2) {
-    cudaFuncSetAttribute(k5b_reverse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k5b_reverse<2><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, W, h.kstride, gpart, h.d_flag);
-  } else {
-    cudaFuncSetAttribute(k5b_reverse<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k5b_reverse<3><<<(unsigned)h.n_tiles, 128, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, W, h.kstride, gpart, h.d_flag);
-  }
-  return cudaGetLastError();
+  IGA_DISPATCH_DQ(launch_k5b, h, ctrl, young, ypt, nu, W, gpart, s)
 }
 
 cudaError_t launch_sens_reduce(const Handle &h, const double *gpart, double *grad, cudaStream_t s) {

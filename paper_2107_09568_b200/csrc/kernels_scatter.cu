@@ -25,19 +25,23 @@ k4_multi(const double *__restrict__ side, const MultiBlock *__restrict__ mblk, c
   double acc[DD];
 #pragma unroll
   for (int e = 0; e < DD; ++e) acc[e] = 0.0;
-  for (int sl = s0; sl < s1; ++sl) {
-    const double *L = side + (int64_t)sl * DD;
-    double l[DD];
+  // slots two at a time, all loads issued before the sums (most blocks have exactly two)
+  for (int sl = s0; sl < s1; sl += 2) {
+    const bool two = sl + 1 < s1;
+    const double *L0 = side + (int64_t)sl * DD, *L1 = side + (int64_t)(two ? sl + 1 : sl) * DD;
+    double l0[DD], l1[DD];
 #pragma unroll
-    for (int e = 0; e < DD; ++e) l[e] = L[e];
-    if (slot_tr[sl]) {
+    for (int e = 0; e < DD; ++e) { l0[e] = L0[e]; l1[e] = L1[e]; }
+    const bool t0 = slot_tr[sl], t1 = two && slot_tr[sl + 1];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) acc[a * D + b] += t0 ? l0[b * D + a] : l0[a * D + b];
+    if (two) {
 #pragma unroll
       for (int a = 0; a < D; ++a)
 #pragma unroll
-        for (int b = 0; b < D; ++b) acc[a * D + b] += l[b * D + a];
-    } else {
-#pragma unroll
-      for (int e = 0; e < DD; ++e) acc[e] += l[e];
+        for (int b = 0; b < D; ++b) acc[a * D + b] += t1 ? l1[b * D + a] : l1[a * D + b];
     }
   }
   if (mb.off_ij == mb.off_ji) {   // diagonal block
