@@ -50,6 +50,7 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_slot_tr, h.slot_tr.data(), h.slot_tr.size()) ||
       !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
       !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
+      !up((void **)&h.d_tperm, h.tperm.data(), h.tperm.size()) ||
       !up((void **)&h.d_patch_info, pinfo.data(), pinfo.size() * 4))
     return IGA_ENOMEM;
   if (cudaMalloc((void **)&h.d_side, std::max<size_t>(8, (size_t)h.n_slots * h.d * h.d * 8)) != cudaSuccess) {
@@ -481,6 +482,19 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   }
   if (h.max_patch_ctrl >= 32768) { set_error("tile patch with >= 32768 control points"); return IGA_ELIMIT; }
   h.Kp = h.pcol[n_patches];
+  // K3 epilogue, transposed pass: within each 128-row block, rows ordered by (B, A) so
+  // that neighbouring threads write neighbouring blocks of CSR row node(B)
+  h.tperm.assign(h.Mpad, 0);
+  for (int64_t m0 = 0; m0 < h.Mpad; m0 += IGA_K3_BM) {
+    std::vector<int> idx(IGA_K3_BM);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) {
+      const int64_t rx = m0 + x, ry = m0 + y;
+      if (rx >= h.M || ry >= h.M) return rx < h.M && ry >= h.M;
+      return h.pairB[rx] != h.pairB[ry] ? h.pairB[rx] < h.pairB[ry] : h.pairA[rx] < h.pairA[ry];
+    });
+    for (int k = 0; k < IGA_K3_BM; ++k) h.tperm[m0 + k] = (uint8_t)idx[k];
+  }
   h.k5_pair.assign(h.Kp, -1);
   h.k5_col.assign(h.M, 0);
   for (int pi = 0; pi < n_patches; ++pi) {

@@ -89,6 +89,7 @@ struct Handle {
   std::vector<int32_t> pcol;         // [n_patches+1] first padded column of each patch
   std::vector<int32_t> k5_pair;      // [Kp] patch-local (A | B << 16), -1 = padding
   std::vector<int32_t> k5_col;       // [M] padded column of each table row
+  std::vector<uint8_t> tperm;        // [Mpad] K3 transposed-pass row order within each 128-row block
   bool on_device = false;
   // interpolation operator
   double interp_x[IGA_MAXQ + 1];
@@ -115,6 +116,7 @@ struct Handle {
   uint8_t *d_slot_tr = nullptr;
   int32_t *d_k5_pair = nullptr;
   int32_t *d_k5_col = nullptr;   // [M]
+  uint8_t *d_tperm = nullptr;    // [Mpad]
   int32_t *d_patch_info = nullptr; // [n_patches][3]: first K5a chunk, ctrl_off, n_ctrl (+ sentinel chunk)
   double *d_mknots = nullptr;    // macro knots, 3 directions concatenated
   int32_t *d_mspan = nullptr;    // element -> knot span, 3 directions concatenated

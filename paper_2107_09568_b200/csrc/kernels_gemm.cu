@@ -36,7 +36,7 @@ constexpr int BK = IGA_KCHUNK;     // 16
 constexpr int BN = IGA_GEMM_BN;    // 72
 constexpr int NI = BN / 8;         // 9 DMMA column tiles per warp
 constexpr int MI = 2;              // 2 DMMA row tiles per warp (16 rows)
-constexpr int N_MMA_WARPS = 8, WS_THREADS = 32 * (N_MMA_WARPS + 4);   // + 4 helper warps (12 warps: 168 regs)
+constexpr int N_MMA_WARPS = 8;
 constexpr int BM = 16 * N_MMA_WARPS;                                        // 128
 constexpr int K5_X_CHUNK_ = BN * BK;                                        // doubles per X chunk
 
@@ -95,187 +95,192 @@ __device__ __forceinline__ void store_row(double *p, double x0, double x1, doubl
 }
 
 // ---------------------------------------------------------------------------------
-// K3 (persistent, warp-specialised)
+// K3: one CTA per 128×72 output tile, 8 MMA warps of 16×72, 4-stage bulk-copy ring
+// refilled by the last warp to release a stage, 2 CTAs per SM (16 MMA warps: the DMMA
+// pipe stays fed while the co-resident CTA runs its epilogue).  After the main loop
+// the same warps stage the tile in shared memory and scatter it.
 constexpr int K3_STAGES = 4;
 constexpr int K3_A_CHUNK = BM * BK, K3_B_CHUNK = BN * BK;             // doubles
 constexpr int K3_CROW = BN + 1;                                        // epilogue pitch (odd)
-constexpr size_t K3_OFF_C = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
-constexpr size_t K3_OFF_BAR = K3_OFF_C + sizeof(double) * (size_t)BM * K3_CROW;
-constexpr size_t K3_SMEM = K3_OFF_BAR + (2 * K3_STAGES + 2) * sizeof(uint64_t);
+constexpr int K3_THREADS = 32 * N_MMA_WARPS;
+constexpr size_t K3_OFF_BAR = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
+constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int));
+static_assert(sizeof(double) * BM * K3_CROW <= K3_OFF_BAR, "epilogue staging must fit in the stages");
 static_assert(BM == IGA_K3_BM, "K3 CTA rows");
+
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
 // EPI = 0: local[M][N] (nzdata, Eq. 58) ; EPI = 1: fused CSR scatter (+ side slots)
 template <int D, int EPI>
-__global__ void __launch_bounds__(WS_THREADS, 1)
+__global__ void __launch_bounds__(K3_THREADS, 2)
 k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int64_t M,
-            int64_t n_tiles, int n_mb, int64_t n_work, double *__restrict__ out, const int32_t *__restrict__ pairA,
+            int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
-            int nl, double *__restrict__ side) {
-  constexpr int DD = D * D, TPC = BN / DD;
+            int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm) {
+  constexpr int DD = D * D, TPC = BN / DD, TPT = TPC / 2;   // tiles per CTA, per epilogue thread
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K3_STAGES * K3_A_CHUNK;
-  double *sC = reinterpret_cast<double *>(reinterpret_cast<char *>(smem) + K3_OFF_C);
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K3_OFF_BAR);
-  uint64_t *empty = full + K3_STAGES, *cfull = empty + K3_STAGES, *cempty = cfull + 1;
+  int *released = reinterpret_cast<int *>(full + K3_STAGES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t mb = blockIdx.x, nb = blockIdx.y, m0 = mb * BM, t0 = nb * TPC;
+  const double *gA = tabA + mb * nkc * K3_A_CHUNK, *gB = coef + nb * nkc * K3_B_CHUNK;
+  // epilogue ownership: row er of the tile, tiles [et0, et0 + TPT) of the CTA
+  const int er = tid & (BM - 1), et0 = (tid >> 7) * TPT;
+  const int64_t r = m0 + er;
   if (tid == 0) {
     for (int s = 0; s < K3_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], N_MMA_WARPS);
+      released[s] = 0;
     }
-    mbar_init(cfull, 32 * N_MMA_WARPS);
-    mbar_init(cempty, 128);
     mbar_fence_init();
   }
+  if (EPI == 1 && r < M)   // warm L2 with the epilogue's maps while the main loop runs
+    for (int tl = et0; tl < et0 + TPT && t0 + tl < n_tiles; ++tl) prefetch_l2(emap + (t0 + tl) * M + r);
   __syncthreads();
-
-  if (warp < N_MMA_WARPS) {   // ---- MMA warps
-    uint32_t g = 0, it = 0;
-    const int fr = lane >> 2, fc = lane & 3;
-    // producer cursor (MMA warp 0, lane 0): next chunk to load, K3_STAGES ahead
-    int64_t pw = blockIdx.x;
-    int pkc = 0;
-    uint32_t pg = 0;
-    auto produce = [&]() {
-      if (pw >= n_work) return;
-      const int st = pg % K3_STAGES;
-      if (pg >= K3_STAGES) mbar_wait(&empty[st], ((pg / K3_STAGES) & 1) ^ 1);
-      const int64_t mb = pw % n_mb, nb = pw / n_mb;
-      mbar_expect_tx(&full[st], (K3_A_CHUNK + K3_B_CHUNK) * 8);
-      bulk_g2s(sA + st * K3_A_CHUNK, tabA + (mb * nkc + pkc) * K3_A_CHUNK, K3_A_CHUNK * 8, &full[st]);
-      bulk_g2s(sB + st * K3_B_CHUNK, coef + (nb * nkc + pkc) * K3_B_CHUNK, K3_B_CHUNK * 8, &full[st]);
-      ++pg;
-      if (++pkc == nkc) { pkc = 0; pw += gridDim.x; }
-    };
-    if (tid == 0)
-      for (int s = 0; s < K3_STAGES; ++s) produce();
-    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-      double acc[MI][NI][2];
+  auto produce = [&](int kc) {
+    const int st = kc % K3_STAGES;
+    mbar_expect_tx(&full[st], (K3_A_CHUNK + K3_B_CHUNK) * 8);
+    bulk_g2s(sA + st * K3_A_CHUNK, gA + (int64_t)kc * K3_A_CHUNK, K3_A_CHUNK * 8, &full[st]);
+    bulk_g2s(sB + st * K3_B_CHUNK, gB + (int64_t)kc * K3_B_CHUNK, K3_B_CHUNK * 8, &full[st]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < K3_STAGES && s < nkc; ++s) produce(s);
+  double acc[MI][NI][2];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-      for (int kc = 0; kc < nkc; ++kc, ++g) {
-        const int st = g % K3_STAGES;
-        mbar_wait(&full[st], (g / K3_STAGES) & 1);
-        if (kc + 1 < nkc)
-          mma_chunk_fm<BK / 4>(sA + st * K3_A_CHUNK, sB + st * K3_B_CHUNK, warp * MI, lane, acc);
-        else
-          mma_chunk_tail(sA + st * K3_A_CHUNK, sB + st * K3_B_CHUNK, warp * MI, lane, ksteps - kc * (BK / 4), acc);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-        if (tid == 0) produce();   // waits until all MMA warps released chunk g's stage
+    for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  for (int kc = 0; kc < nkc; ++kc) {
+    const int st = kc % K3_STAGES;
+    mbar_wait(&full[st], (kc / K3_STAGES) & 1);
+    if (kc + 1 < nkc)
+      mma_chunk_fm<BK / 4>(sA + st * K3_A_CHUNK, sB + st * K3_B_CHUNK, warp * MI, lane, acc);
+    else
+      mma_chunk_tail(sA + st * K3_A_CHUNK, sB + st * K3_B_CHUNK, warp * MI, lane, ksteps - kc * (BK / 4), acc);
+    __syncwarp();
+    if (lane == 0) {   // the last warp to release a stage refills it
+      __threadfence_block();
+      if (atomicAdd(&released[st], 1) == N_MMA_WARPS - 1) {
+        released[st] = 0;
+        __threadfence_block();
+        if (kc + K3_STAGES < nkc) produce(kc + K3_STAGES);
       }
-      mbar_wait(cempty, (it & 1) ^ 1);   // the epilogue has drained the previous tile
+    }
+  }
+  __syncthreads();   // all stages consumed: stage the tile in shared memory
+  double *sC = smem;
+  {
+    const int fr = lane >> 2, fc = lane & 3;
+#ifdef IGA_EXPERIMENT_K3_BARE
+    double sum = 0.0;
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          const int r = warp * 16 + mi * 8 + fr, c = ni * 8 + 2 * fc;
-          sC[r * K3_CROW + c] = acc[mi][ni][0];
-          sC[r * K3_CROW + c + 1] = acc[mi][ni][1];
-        }
-      mbar_arrive(cfull);
+      for (int ni = 0; ni < NI; ++ni) sum += acc[mi][ni][0] + acc[mi][ni][1];
+    if (sum == 1.2345) out[0] = sum;
+    return;
+#endif
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const int rr = warp * 16 + mi * 8 + fr, c = ni * 8 + 2 * fc;
+        sC[rr * K3_CROW + c] = acc[mi][ni][0];
+        sC[rr * K3_CROW + c + 1] = acc[mi][ni][1];
+      }
+  }
+  __syncthreads();
+  if (EPI == 0) {
+    const int64_t N = n_tiles * DD, n0 = nb * BN;
+    for (int i = tid; i < BM * BN; i += K3_THREADS) {
+      const int rr = i / BN, c = i % BN;
+      const int64_t gr = m0 + rr, gc = n0 + c;
+      if (gr < M && gc < N) out[gr * N + gc] = sC[rr * K3_CROW + c];
     }
     return;
   }
-
-  // ---- epilogue warps: thread e owns row e of the tile, for the CTA's tiles
-  const int e = tid - 32 * N_MMA_WARPS;
-  uint32_t it = 0;
-  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-    const int64_t mb = w % n_mb, nb = w / n_mb;
-    const int64_t m0 = mb * BM, r = m0 + e, t0 = nb * TPC;
-    if (EPI == 0) {
-      mbar_wait(cfull, it & 1);
-      const int64_t N = n_tiles * DD, n0 = nb * BN;
-      for (int i = e; i < BM * BN; i += 128) {
-        const int rr = i / BN, c = i % BN;
-        const int64_t gr = m0 + rr, gc = n0 + c;
-        if (gr < M && gc < N) out[gr * N + gc] = sC[rr * K3_CROW + c];
-      }
-      mbar_arrive(cempty);
+  // fused scatter (R9).  Pass 1: row er, blocks (I,J) (and diagonal / side-slot blocks);
+  // pass 2: row tperm[er] of the (B, A)-ordered block, blocks (J,I) = L^T, so that
+  // neighbouring threads write neighbouring blocks of the same CSR rows in both passes.
+  const int et = tperm[m0 + er];
+  const int64_t rt = m0 + et;
+  const bool live = r < M, live_t = rt < M;
+  const int A = live ? pairA[r] : 0, B = live ? pairB[r] : 0;
+  const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
+  int32_t em[TPT], emt[TPT];
+  int64_t riA[TPT], riB[TPT];
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int64_t t = t0 + et0 + k < n_tiles ? t0 + et0 + k : n_tiles - 1;
+    em[k] = live ? emap[t * M + r] : -1;
+    riA[k] = live ? rowinfo[t * nl + A] : 0;
+    emt[k] = live_t ? emap[t * M + rt] : -1;
+    riB[k] = live_t ? rowinfo[t * nl + Bt] : 0;
+  }
+  const double *Lrow = sC + er * K3_CROW, *Ltrow = sC + et * K3_CROW;
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int tl = et0 + k;
+    if (!live || t0 + tl >= n_tiles) break;
+    const double *L = Lrow + tl * DD;
+    double l[DD];
+#pragma unroll
+    for (int q = 0; q < DD; ++q) l[q] = L[q];
+    const int32_t ev = em[k];
+#ifdef IGA_EXPERIMENT_NO_SCATTER
+    if (ev != 12345) { if (l[0] == 1.2345) out[0] = l[1]; continue; }
+#endif
+    if (ev < 0) {   // one of several contributions: side slot, summed by K4
+      double *o = side + (int64_t)(-ev - 1) * DD;
+#pragma unroll
+      for (int q = 0; q < DD; ++q) o[q] = l[q];
       continue;
     }
-    // prefetch the maps of this row before the accumulators are ready
-    int A = 0, B = 0;
-    int32_t em[TPC];
-    int64_t riA[TPC], riB[TPC];
-    const bool live = r < M;
-    if (live) {
-      A = pairA[r];
-      B = pairB[r];
+    const int64_t offI = DD * (riA[k] >> 24) + D * (ev & 0xffff);
+    const int64_t strI = D * (riA[k] & 0xffffff);
+    auto L_ = [&](int a, int b) { return a < D && b < D ? l[a * D + b] : 0.0; };
+    if (A == B) {   // diagonal block: upper triangle mirrored (R9)
 #pragma unroll
-      for (int tl = 0; tl < TPC; ++tl) {
-        const int64_t t = t0 + tl < n_tiles ? t0 + tl : n_tiles - 1;
-        em[tl] = emap[t * M + r];
-        riA[tl] = rowinfo[t * nl + A];
-        riB[tl] = rowinfo[t * nl + B];
-      }
-    }
-    mbar_wait(cfull, it & 1);
-    if (live) {
-      const double *Lrow = sC + e * K3_CROW;
+      for (int a = 0; a < D; ++a)
+        store_row<D>(out + offI + a * strI, a <= 0 ? L_(a, 0) : L_(0, a), a <= 1 ? L_(a, 1) : L_(1, a),
+                     a <= 2 ? L_(a, 2) : L_(2, a));
+    } else {
+#ifndef IGA_EXPERIMENT_NO_DIRECT
 #pragma unroll
-      for (int tl = 0; tl < TPC; ++tl) {
-        if (t0 + tl >= n_tiles) break;
-        const double *L = Lrow + tl * DD;
-        double l[DD];
-#pragma unroll
-        for (int k = 0; k < DD; ++k) l[k] = L[k];
-        const int32_t ev = em[tl];
-#ifdef IGA_EXPERIMENT_NO_SCATTER
-        if (ev != 12345) { if (l[0] == 1.2345) out[0] = l[1]; continue; }
+      for (int a = 0; a < D; ++a) store_row<D>(out + offI + a * strI, L_(a, 0), L_(a, 1), L_(a, 2));
 #endif
-        if (ev < 0) {   // one of several contributions: side slot, summed by K4
-          double *o = side + (int64_t)(-ev - 1) * DD;
-#pragma unroll
-          for (int k = 0; k < DD; ++k) o[k] = l[k];
-          continue;
-        }
-        const int64_t offI = DD * (riA[tl] >> 24) + D * (ev & 0xffff);
-        const int64_t strI = D * (riA[tl] & 0xffffff);
-        auto L_ = [&](int a, int b) { return a < D && b < D ? l[a * D + b] : 0.0; };
-        if (A == B) {   // diagonal block: upper triangle mirrored (R9)
-#pragma unroll
-          for (int a = 0; a < D; ++a)
-            store_row<D>(out + offI + a * strI, a <= 0 ? L_(a, 0) : L_(0, a), a <= 1 ? L_(a, 1) : L_(1, a),
-                         a <= 2 ? L_(a, 2) : L_(2, a));
-        } else {
-          const int64_t offJ = DD * (riB[tl] >> 24) + D * (ev >> 16);
-          const int64_t strJ = D * (riB[tl] & 0xffffff);
-#pragma unroll
-          for (int a = 0; a < D; ++a) store_row<D>(out + offI + a * strI, L_(a, 0), L_(a, 1), L_(a, 2));
-#pragma unroll
-          for (int b = 0; b < D; ++b) store_row<D>(out + offJ + b * strJ, L_(0, b), L_(1, b), L_(2, b));
-        }
-      }
     }
-    mbar_arrive(cempty);
   }
-}
-
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+#ifndef IGA_EXPERIMENT_NO_TRANSPOSED
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int tl = et0 + k;
+    if (!live_t || t0 + tl >= n_tiles) break;
+    const int32_t ev = emt[k];
+    if (ev < 0 || At == Bt) continue;   // side slot / diagonal: done in pass 1
+    const double *L = Ltrow + tl * DD;
+    double l[DD];
+#pragma unroll
+    for (int q = 0; q < DD; ++q) l[q] = L[q];
+    auto L_ = [&](int a, int b) { return a < D && b < D ? l[a * D + b] : 0.0; };
+    const int64_t offJ = DD * (riB[k] >> 24) + D * (ev >> 16);
+    const int64_t strJ = D * (riB[k] & 0xffffff);
+#pragma unroll
+    for (int b = 0; b < D; ++b) store_row<D>(out + offJ + b * strJ, L_(0, b), L_(1, b), L_(2, b));
   }
-  return n;
+#endif
 }
 
 template <int D, int EPI>
 static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k3_contract<D, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM);
   if (e) return e;
-  const int n_mb = (int)(h.Mpad / BM);
-  const int64_t n_work = (int64_t)n_mb * (h.Npad / BN);
-  const unsigned grid = (unsigned)std::min<int64_t>(n_work, num_sms());
-  k3_contract<D, EPI><<<grid, WS_THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.kstride / BK, (h.nk + 3) / 4, h.M,
-                                                        h.n_tiles, n_mb, n_work, out, h.d_pairA, h.d_pairB,
-                                                        h.d_emap, h.d_rowinfo, h.n_local_ctrl, h.d_side);
+  dim3 grid((unsigned)(h.Mpad / BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
+  if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+  k3_contract<D, EPI><<<grid, K3_THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.kstride / BK, (h.nk + 3) / 4, h.M,
+                                                        h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,
+                                                        h.n_local_ctrl, h.d_side, h.d_tperm);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,247 @@
+"""GPU parity at BASELINE.json's full sizes (cfg4: 1024 tiles, p = q = 3, per-tile E;
+cfg5: 8192 tiles, the bench workload), in the launch configuration bench.py times.
+
+The oracle cannot form K at these sizes, so it is compared on sampled outputs it can
+compute one by one (north star; task ③):
+  * element matrices of sampled tiles (incl. the first and last) — oracle local_lookup;
+  * complete CSR rows of sampled nodes — the oracle's element matrices of every tile
+    containing the node, assembled per reading R9, placed by the library's pattern;
+    nodes are drawn among tile-face / patch-interface points too, so rows that go
+    through K4's multi-contribution gather are covered;
+  * sensitivity entries g[k, α] at sampled macro control points (oracle complex step);
+  * properties at full size: pattern structure (sorted, node rows share their column
+    sets, structural symmetry of sampled rows), bitwise symmetry of sampled blocks,
+    K·translation = 0 row-wise, translation invariance Σ_k g[k] = 0 and Euler
+    homogeneity Σ P·g = (d-2)·uᵀKv (uᵀKv from the GPU's own K).
+The global node numbering at these sizes comes from the library (it is checked bit for
+bit against the oracle's DofMap on cfg1-3, test_gpu_parity.py); here it is checked by
+property: coincident control points of neighbouring tiles share a node id.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TOL_ELEM = 1e-12
+TOL_K = 1e-11
+TOL_SENS = 1e-11
+
+_cases = {}
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def case(c):
+    if c in _cases:
+        return _cases[c]
+    from paper_2107_09568_b200 import Assembler
+    from synth import make_config
+    from oracle.assemble import Tables
+    prob = make_config(c)
+    A = Assembler(prob)
+    s = A.sizes
+    d = prob.d
+    dev = torch.device("cuda:0")
+    ctrl = torch.tensor(prob.macro.ctrl, dtype=torch.float64, device=dev)
+    young = torch.tensor(prob.young, dtype=torch.float64, device=dev)
+    vals = torch.empty(s.nnz, dtype=torch.float64, device=dev)
+    local = torch.empty(s.n_local_rows * s.n_tiles * d * d, dtype=torch.float64, device=dev)
+    A.assemble(ctrl, young, prob.nu, vals, local)
+    rp = torch.empty(s.n_dof + 1, dtype=torch.int64, device=dev)
+    ci = torch.empty(s.nnz, dtype=torch.int32, device=dev)
+    A.pattern(rp, ci)
+    torch.cuda.synchronize()
+    nl = sum(p.n_ctrl for p in prob.tile)
+    nm = A.node_map_for(nl)
+    offs = np.cumsum([0] + [p.n_ctrl for p in prob.tile])
+    tabs = Tables(prob)
+    pairs = A.pairs()
+    assert np.array_equal(pairs, np.concatenate(tabs.pairs))
+    patch_of_row = np.concatenate([np.full(len(pr), k) for k, pr in enumerate(tabs.pairs)])
+    pa = pairs[:, 0] + offs[patch_of_row]
+    pb = pairs[:, 1] + offs[patch_of_row]
+    out = dict(prob=prob, A=A, s=s, ctrl=ctrl, young=young, vals=vals, local=local, rp=rp, ci=ci,
+               rp_h=rp.cpu().numpy(), nm=nm, pa=pa, pb=pb, tabs=tabs)
+    _cases[c] = out
+    return out
+
+
+def sample_nodes(g, n, seed):
+    """Nodes of sampled (tile, control point) pairs; half of them on tile faces / patch
+    interfaces (nodes shared by several tiles or patches)."""
+    nm = g["nm"]
+    rng = np.random.default_rng(seed)
+    counts = np.bincount(nm.ravel())
+    shared = np.flatnonzero(counts > 1)
+    nodes = list(rng.choice(nm.shape[0] * nm.shape[1], n // 2, replace=False))
+    nodes = [int(nm.ravel()[f]) for f in nodes] + [int(x) for x in rng.choice(shared, n - n // 2, replace=False)]
+    return sorted(set(nodes))
+
+
+def oracle_row_blocks(g, I):
+    """{J: d×d block K(I,J)} from the oracle's element matrices (reading R9)."""
+    from oracle import assemble as As
+    prob, nm, pa, pb, tabs = g["prob"], g["nm"], g["pa"], g["pb"], g["tabs"]
+    d = prob.d
+    tiles = np.unique(np.nonzero(nm == I)[0])
+    L = As.local_lookup(prob, tabs, prob.macro.ctrl, [int(t) for t in tiles])
+    blocks = {}
+    for n, t in enumerate(tiles):
+        nI, nJ = nm[t][pa], nm[t][pb]
+        for r in np.flatnonzero(nI == I):
+            J = int(nJ[r])
+            blk = L[n, r] if J != I else np.array([[L[n, r, min(a, b), max(a, b)] for b in range(d)] for a in range(d)])
+            blocks[J] = blocks.get(J, 0.0) + blk
+        for r in np.flatnonzero((nJ == I) & (nI != I)):
+            J = int(nI[r])
+            blocks[J] = blocks.get(J, 0.0) + L[n, r].T
+    return blocks
+
+
+def gpu_row_blocks(g, I):
+    d = g["prob"].d
+    rp = g["rp_h"]
+    cols = g["ci"][rp[I * d]:rp[I * d + 1]].cpu().numpy()
+    Js = cols[::d] // d
+    out = np.zeros((len(Js), d, d))
+    for a in range(d):
+        v = g["vals"][rp[I * d + a]:rp[I * d + a + 1]].cpu().numpy().reshape(-1, d)
+        c = g["ci"][rp[I * d + a]:rp[I * d + a + 1]].cpu().numpy().reshape(-1, d)
+        assert np.array_equal(c, Js[:, None] * d + np.arange(d)), "node rows must share their column sets"
+        out[:, a, :] = v
+    return Js, out
+
+
+@pytest.mark.parametrize("c", [4, 5])
+def test_fullsize_element_matrices(c):
+    from oracle import assemble as As
+    g = case(c)
+    prob, s = g["prob"], g["s"]
+    d = prob.d
+    rng = np.random.default_rng(100 + c)
+    tiles = sorted(set(rng.choice(prob.n_tiles, 6, replace=False).tolist() + [0, prob.n_tiles - 1]))
+    ref = As.local_lookup(prob, g["tabs"], prob.macro.ctrl, tiles)
+    Lg = g["local"].view(s.n_local_rows, s.n_tiles, d, d)
+    for n, t in enumerate(tiles):
+        got = Lg[:, t].cpu().numpy()
+        assert rel(got, ref[n]) < TOL_ELEM, (t, rel(got, ref[n]))
+
+
+@pytest.mark.parametrize("c", [4, 5])
+def test_fullsize_csr_rows(c):
+    g = case(c)
+    for I in sample_nodes(g, 10, 200 + c):
+        ref = oracle_row_blocks(g, I)
+        Js, got = gpu_row_blocks(g, I)
+        assert list(Js) == sorted(ref), I                               # block columns of row I
+        R = np.stack([ref[int(J)] for J in Js])
+        assert rel(got, R) < TOL_K, (I, rel(got, R))
+
+
+@pytest.mark.parametrize("c", [4, 5])
+def test_fullsize_properties(c):
+    g = case(c)
+    prob, s = g["prob"], g["s"]
+    d = prob.d
+    rp = g["rp_h"]
+    assert rp[0] == 0 and rp[-1] == s.nnz and np.all(np.diff(rp) > 0)
+    # node rows: d scalar rows of equal length; K(I,J) = K(J,I)^T bitwise on sampled rows;
+    # translations in the kernel row-wise
+    for I in sample_nodes(g, 8, 300 + c):
+        Js, blk = gpu_row_blocks(g, I)
+        assert np.all(np.diff(Js) > 0)
+        for a in range(d):
+            assert abs(blk[:, a, :].sum(axis=0)).max() < 1e-12 * abs(blk).max() * 10   # Σ_J K(I,J)·e_b = 0
+        for n, J in enumerate(Js[:6]):
+            Ji, bj = gpu_row_blocks(g, int(J))
+            k = int(np.searchsorted(Ji, I))
+            assert Ji[k] == I and np.array_equal(bj[k], blk[n].T)
+    # DofMap property: face points of neighbouring tiles share node ids, and every node id
+    # of a tile patch is distinct
+    nm = g["nm"]
+    assert nm.max() + 1 == s.n_nodes
+    offs = np.cumsum([0] + [p.n_ctrl for p in prob.tile])
+    for t in np.random.default_rng(c).choice(prob.n_tiles, 16, replace=False):
+        for k in range(len(prob.tile)):
+            ids = nm[t, offs[k]:offs[k + 1]]
+            assert len(np.unique(ids)) == len(ids)
+    P = np.concatenate([p.ctrl for p in prob.tile])
+    lo = np.flatnonzero(np.abs(P[:, 0]) < 1e-10)
+    hi = np.flatnonzero(np.abs(P[:, 0] - 1.0) < 1e-10)
+    match = {int(a): int(b) for a in hi for b in lo if np.abs(P[a, 1:] - P[b, 1:]).max() < 1e-10}
+    n0 = prob.n_el[0]
+    for t in range(0, prob.n_tiles - 1, max(1, prob.n_tiles // 16)):
+        if (t % n0) == n0 - 1:
+            continue
+        for a, b in match.items():
+            assert nm[t, a] == nm[t + 1, b]
+
+
+def spmv_dot(g, u, v, max_nnz=1 << 30):
+    """uᵀKv with the GPU's CSR K, in row slices of < 2^30 non-zeros (torch's sparse mv
+    indexes with int32 beyond that)."""
+    rp = g["rp_h"]
+    n = len(rp) - 1
+    total, r0 = 0.0, 0
+    while r0 < n:
+        r1 = int(np.searchsorted(rp, rp[r0] + max_nnz, side="right")) - 1
+        r1 = max(r1, r0 + 1)
+        a, b = int(rp[r0]), int(rp[r1])
+        sub = torch.sparse_csr_tensor(g["rp"][r0:r1 + 1] - a, g["ci"][a:b].to(torch.int64), g["vals"][a:b],
+                                      size=(r1 - r0, n))
+        total += torch.dot(u[r0:r1], torch.mv(sub, v)).item()
+        r0 = r1
+    return total
+
+
+class _LibPattern:
+    """I[t], J[t] of the oracle sensitivity, from the library's node map."""
+
+    def __init__(self, g):
+        self.g = g
+
+    @property
+    def I(self):
+        g = self.g
+        return _Rows(g["nm"], g["pa"])
+
+    @property
+    def J(self):
+        g = self.g
+        return _Rows(g["nm"], g["pb"])
+
+
+class _Rows:
+    def __init__(self, nm, idx):
+        self.nm, self.idx = nm, idx
+
+    def __getitem__(self, t):
+        return self.nm[t][self.idx]
+
+
+@pytest.mark.parametrize("c", [4, 5])
+def test_fullsize_sensitivity(c):
+    from oracle import sensitivity as S
+    from synth import draw_uv_seeded
+    g = case(c)
+    prob, A, s = g["prob"], g["A"], g["s"]
+    d = prob.d
+    u, v = draw_uv_seeded(c, s.n_dof)
+    ut, vt = torch.tensor(u, device="cuda"), torch.tensor(v, device="cuda")
+    grad = torch.empty(s.n_macro_cp * d, dtype=torch.float64, device="cuda")
+    A.sensitivity(g["ctrl"], g["young"], prob.nu, ut, vt, grad)
+    got = grad.cpu().numpy().reshape(-1, d)
+    scale = np.abs(got).max()
+    assert np.abs(got.sum(0)).max() < 1e-10 * scale                      # translation invariance
+    uKv = spmv_dot(g, ut, vt)
+    euler = float(np.sum(prob.macro.ctrl * got))
+    assert abs(euler - (d - 2) * uKv) < 1e-9 * max(abs(uKv), scale)      # Σ P·g = (d-2) uᵀKv
+    rng = np.random.default_rng(400 + c)
+    ent = [(int(k), int(a)) for k, a in zip(rng.integers(0, len(got), 4), rng.integers(0, d, 4))]
+    ref = S.sensitivity(prob, g["tabs"], _LibPattern(g), u, v, entries=ent)
+    for k, a in ent:
+        assert abs(got[k, a] - ref[k, a]) < TOL_SENS * scale * 10, (k, a, got[k, a], ref[k, a])
