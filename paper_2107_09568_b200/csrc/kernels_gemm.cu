@@ -200,9 +200,12 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     }
     return;
   }
-  // fused scatter (R9).  Pass 1: row er, blocks (I,J) (and diagonal / side-slot blocks);
-  // pass 2: row tperm[er] of the (B, A)-ordered block, blocks (J,I) = L^T, so that
-  // neighbouring threads write neighbouring blocks of the same CSR rows in both passes.
+  // fused scatter (R9).  Pass 1: row er, blocks (I,J) (diagonal blocks mirrored from
+  // their upper triangle); pass 2: row tperm[er] of the (B, A)-ordered block, blocks
+  // (J,I) = Lᵀ.  Both orders put neighbouring blocks of one CSR row in neighbouring lanes;
+  // the d-double row segments of a warp's 32 blocks are then stored cooperatively — lane
+  // l writes words l, l+32, ... of the warp's 32·d words — so runs of adjacent blocks leave
+  // as whole 32-B sectors instead of 8/16-B pieces per lane.
   const int et = tperm[m0 + er];
   const int64_t rt = m0 + et;
   const bool live = r < M, live_t = rt < M;
@@ -213,63 +216,51 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
     const int64_t t = t0 + et0 + k < n_tiles ? t0 + et0 + k : n_tiles - 1;
-    em[k] = live ? emap[t * M + r] : -1;
+    em[k] = live ? emap[t * M + r] : 0;
     riA[k] = live ? rowinfo[t * nl + A] : 0;
-    emt[k] = live_t ? emap[t * M + rt] : -1;
+    emt[k] = live_t ? emap[t * M + rt] : 0;
     riB[k] = live_t ? rowinfo[t * nl + Bt] : 0;
   }
-  const double *Lrow = sC + er * K3_CROW, *Ltrow = sC + et * K3_CROW;
+  // lanes hold (o = CSR offset of their row segment or -1, smem row, diagonal?); word w of
+  // the warp comes from lane w/D, column w%D; value L[ra][cb] of that lane's block
+  auto coop = [&](int64_t o, int srow, bool dg, int tl, int idx, bool transposed) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int w = 32 * j + lane, src = w / D, c = w - src * D;
+      const int64_t ob = __shfl_sync(0xffffffffu, o, src);
+      const int sb = __shfl_sync(0xffffffffu, srow, src);
+      const bool db = __shfl_sync(0xffffffffu, (int)dg, src) != 0;
+      if (ob >= 0) {
+        int ra = transposed ? c : idx, cb = transposed ? idx : c;
+        if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+        out[ob + c] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+      }
+    }
+  };
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
     const int tl = et0 + k;
-    if (!live || t0 + tl >= n_tiles) break;
-    const double *L = Lrow + tl * DD;
-    double l[DD];
-#pragma unroll
-    for (int q = 0; q < DD; ++q) l[q] = L[q];
+    if (t0 + tl >= n_tiles) break;   // warp-uniform
     const int32_t ev = em[k];
 #ifdef IGA_EXPERIMENT_NO_SCATTER
-    if (ev != 12345) { if (l[0] == 1.2345) out[0] = l[1]; continue; }
+    if (ev != 12345) continue;
 #endif
-    if (ev < 0) {   // one of several contributions: side slot, summed by K4
+    if (live && ev < 0) {   // one of several contributions: side slot, summed by K4
+      const double *L = sC + er * K3_CROW + tl * DD;
       double *o = side + (int64_t)(-ev - 1) * DD;
 #pragma unroll
-      for (int q = 0; q < DD; ++q) o[q] = l[q];
-      continue;
+      for (int q = 0; q < DD; ++q) o[q] = L[q];
     }
-    const int64_t offI = DD * (riA[k] >> 24) + D * (ev & 0xffff);
-    const int64_t strI = D * (riA[k] & 0xffffff);
-    auto L_ = [&](int a, int b) { return a < D && b < D ? l[a * D + b] : 0.0; };
-    if (A == B) {   // diagonal block: upper triangle mirrored (R9)
+    const bool w1 = live && ev >= 0;
+    const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff), str1 = D * (riA[k] & 0xffffff);
 #pragma unroll
-      for (int a = 0; a < D; ++a)
-        store_row<D>(out + offI + a * strI, a <= 0 ? L_(a, 0) : L_(0, a), a <= 1 ? L_(a, 1) : L_(1, a),
-                     a <= 2 ? L_(a, 2) : L_(2, a));
-    } else {
-#ifndef IGA_EXPERIMENT_NO_DIRECT
+    for (int a = 0; a < D; ++a) coop(w1 ? off1 + a * str1 : -1, er, A == B, tl, a, false);
+    const int32_t evt = emt[k];
+    const bool w2 = live_t && evt >= 0 && At != Bt;
+    const int64_t off2 = DD * (riB[k] >> 24) + D * (evt >> 16), str2 = D * (riB[k] & 0xffffff);
 #pragma unroll
-      for (int a = 0; a < D; ++a) store_row<D>(out + offI + a * strI, L_(a, 0), L_(a, 1), L_(a, 2));
-#endif
-    }
+    for (int b = 0; b < D; ++b) coop(w2 ? off2 + b * str2 : -1, et, false, tl, b, true);
   }
-#ifndef IGA_EXPERIMENT_NO_TRANSPOSED
-#pragma unroll
-  for (int k = 0; k < TPT; ++k) {
-    const int tl = et0 + k;
-    if (!live_t || t0 + tl >= n_tiles) break;
-    const int32_t ev = emt[k];
-    if (ev < 0 || At == Bt) continue;   // side slot / diagonal: done in pass 1
-    const double *L = Ltrow + tl * DD;
-    double l[DD];
-#pragma unroll
-    for (int q = 0; q < DD; ++q) l[q] = L[q];
-    auto L_ = [&](int a, int b) { return a < D && b < D ? l[a * D + b] : 0.0; };
-    const int64_t offJ = DD * (riB[k] >> 24) + D * (ev >> 16);
-    const int64_t strJ = D * (riB[k] & 0xffffff);
-#pragma unroll
-    for (int b = 0; b < D; ++b) store_row<D>(out + offJ + b * strJ, L_(0, b), L_(1, b), L_(2, b));
-  }
-#endif
 }
 
 template <int D, int EPI>
