@@ -47,6 +47,7 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_emap, h.emap.data(), h.emap.size() * 4) ||
       !up((void **)&h.d_mblk, h.mblk.data(), h.mblk.size() * sizeof(MultiBlock)) ||
       !up((void **)&h.d_mslot0, h.mslot0.data(), h.mslot0.size() * 4) ||
+      !up((void **)&h.d_mperm, h.mperm.data(), h.mperm.size() * 4) ||
       !up((void **)&h.d_slot_tr, h.slot_tr.data(), h.slot_tr.size()) ||
       !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
       !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
@@ -62,6 +63,7 @@ iga_status upload_topology(Handle &h) {
   std::vector<int32_t>().swap(h.emap);
   std::vector<MultiBlock>().swap(h.mblk);
   std::vector<int32_t>().swap(h.mslot0);
+  std::vector<int32_t>().swap(h.mperm);
   std::vector<uint8_t>().swap(h.slot_tr);
   return IGA_OK;
 }
@@ -464,6 +466,23 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   }
   std::vector<uint64_t>().swap(keys);
   std::vector<uint64_t>().swap(kcol);
+  {   // K4 transposed pass order: multi blocks sorted by (J, I) = (row of K(J,I), its column)
+    std::vector<int64_t> rowJ(h.n_multi), colI(h.n_multi);
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < h.n_multi; ++m) {
+      const MultiBlock &mb = h.mblk[m];
+      // off_ji = d²·brow_ptr[J] + d·rank: recover J by binary search in brow_ptr
+      const int64_t b = (mb.off_ji / d) / d;   // block index lower bound of row J
+      const int64_t J = std::upper_bound(h.brow_ptr.begin(), h.brow_ptr.end(), b) - h.brow_ptr.begin() - 1;
+      rowJ[m] = J;
+      colI[m] = mb.off_ij;   // (I, J) order already sorts by I within row J
+    }
+    h.mperm.resize(h.n_multi);
+    std::iota(h.mperm.begin(), h.mperm.end(), 0);
+    std::stable_sort(h.mperm.begin(), h.mperm.end(), [&](int32_t x, int32_t y) {
+      return rowJ[x] != rowJ[y] ? rowJ[x] < rowJ[y] : colI[x] < colI[y];
+    });
+  }
   h.rowinfo.assign(nt * nl, 0);
 #pragma omp parallel for schedule(static)
   for (int64_t f = 0; f < nt * nl; ++f) {

@@ -79,6 +79,7 @@ struct Handle {
   int64_t n_multi = 0, n_slots = 0;  // blocks with > 1 contribution, and their contributions
   std::vector<MultiBlock> mblk;      // [n_multi]
   std::vector<int32_t> mslot0;       // [n_multi+1] first slot of each multi block
+  std::vector<int32_t> mperm;        // [n_multi] multi blocks in (J, I) order (K4 transposed pass)
   std::vector<uint8_t> slot_tr;      // [n_slots] 1 = slot holds the (J,I)-oriented block
   // operand layouts (fragment-major, device_common.cuh fm_index)
   int64_t Mpad = 0;                  // rows of d_tabA (multiple of IGA_K3_BM)
@@ -113,6 +114,7 @@ struct Handle {
   int32_t *d_emap = nullptr;
   MultiBlock *d_mblk = nullptr;
   int32_t *d_mslot0 = nullptr;
+  int32_t *d_mperm = nullptr;
   uint8_t *d_slot_tr = nullptr;
   int32_t *d_k5_pair = nullptr;
   int32_t *d_k5_col = nullptr;   // [M]
