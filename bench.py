@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-sensitivity", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: shard ONE problem over the ranks (slabs + halo, gradient all-reduce; "
+                         "strong scaling) instead of one independent problem per rank (weak scaling)")
     return ap.parse_args()
 
 
@@ -69,6 +72,17 @@ def reduce_max(x, world):
     dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(x, world):
+    if world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -212,10 +226,13 @@ def run_ours(args, rank, world):
     dev = torch.device("cuda", local_rank)
     sens = not args.no_sensitivity
     prob = make_config(args.config)
+    shard = args.shard and world > 1
     t0 = time.perf_counter()
-    A = Assembler(prob)
+    A = Assembler(prob, shard=(world, rank) if shard else None)
     build_s = time.perf_counter() - t0
     s = A.sizes
+    if shard:
+        from paper_2107_09568_b200.shard import allreduce_grad
     d = prob.d
     ctrl = torch.tensor(prob.macro.ctrl, dtype=torch.float64, device=dev)
     young = torch.tensor(prob.young, dtype=torch.float64, device=dev)
@@ -230,6 +247,8 @@ def run_ours(args, rank, world):
         A.assemble(ctrl, young, prob.nu, vals, stream=stream)
         if sens:
             A.sensitivity(ctrl, young, prob.nu, u, v, grad, stream=stream)
+            if shard:
+                allreduce_grad(grad, world)   # the sharded step's one collective (NCCL)
 
     for _ in range(args.warmup):
         step()
@@ -250,9 +269,10 @@ def run_ours(args, rank, world):
     kms, kn = A.kernel_times()
     A.set_profiling(False)
     ms = reduce_max(ms_local, world)
-    tiles_total = s.n_tiles * world
+    tiles_total = s.n_tiles if shard else s.n_tiles * world   # shard: the ranks share one problem
+    nnz_total = reduce_sum(s.nnz, world) if shard else s.nnz * world
     value = tiles_total / (ms * 1e-3)
-    nnz_per_s = s.nnz * world / (ms * 1e-3)
+    nnz_per_s = nnz_total / (ms * 1e-3)
 
     # ---- e2e: host (pinned) inputs through the C ABI, gradient read back ---------
     e2e = None
@@ -325,10 +345,14 @@ def run_ours(args, rank, world):
                 "algorithmic_flops_per_launch": alg["k3_flops"]}
 
     line = {"metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg{args.config}" + ("" if sens else " (K only)"),
-                       "n_tiles_per_gpu": int(s.n_tiles), "nnz": int(s.nnz), "n_dof": int(s.n_dof), "p": prob.p,
+                       "parallelism": (f"slab{world} (one problem: slabs + halo, gradient all-reduce)" if shard
+                                       else f"replica{world} (one independent problem per GPU)"),
+                       "n_tiles_per_gpu": int(s.n_tiles_owned if shard else s.n_tiles), "nnz": int(nnz_total),
+                       "n_dof": int(s.n_dof), "p": prob.p,
                        "q": prob.q, "sensitivity": sens,
                        "l2": "working set >> 126 MB L2 (CSR values alone 8*nnz bytes); no explicit flush"},
             "nnz_per_s": nnz_per_s, "roofline": roofline, "rooflines_all": rooflines,

@@ -71,6 +71,19 @@ typedef struct {
 
 typedef struct iga_handle iga_handle;
 
+/* Slab partition of ONE problem over n_shards processes.  The macro
+ * elements are split into n_shards contiguous slabs of element layers along the slowest
+ * direction (direction d-1); shard s owns the tiles of its slab and the CSR rows of the
+ * nodes that first appear in it (a contiguous range of global node ids), and also forms
+ * the tiles of one halo layer of the next slab so that its rows are complete.  K needs no
+ * communication; iga_sensitivity returns this shard's partial gradient (its owned tiles
+ * only), which the caller sums over shards (one all-reduce of n_macro_cp*d doubles).
+ * NULL or n_shards = 1: the whole problem. */
+typedef struct {
+  int32_t n_shards;
+  int32_t shard;
+} iga_shard;
+
 typedef struct {
   int32_t dim;            /* d */
   int32_t q;              /* interpolation degree p_π */
@@ -80,16 +93,22 @@ typedef struct {
   int32_t n_patches;
   int32_t n_gauss;        /* Gauss points per direction per tile knot span (R3) */
   int32_t reserved;
-  int64_t n_tiles;        /* m_M = macro elements (Eq. 5) */
+  int64_t n_tiles;        /* m_M = macro elements (Eq. 5), whole problem; per-tile E has this length */
   int64_t n_local_rows;   /* Σ_p n_nz,p = rows of the stacked mat𝔎 (Eqs. 56-57) */
   int64_t n_macro_cp;     /* macro control points (Eq. 4) */
-  int64_t n_nodes;        /* global nodes after merging (R10) */
-  int64_t n_dof;          /* n_nodes * d, interleaved DOF = node*d + a (R9) */
-  int64_t nnz;            /* scalar CSR non-zeros of K (both triangles, R9) */
-  int64_t n_blocks;       /* d×d structural blocks */
-  int64_t n_contrib;      /* (tile, local row) -> block contributions, both triangles */
-  int64_t n_multi_blocks; /* blocks (I <= J) with more than one contribution (K4 gathers them) */
+  int64_t n_nodes;        /* global nodes after merging (R10), whole problem */
+  int64_t n_dof;          /* n_nodes * d, interleaved DOF = node*d + a (R9): length of u, v */
+  int64_t nnz;            /* scalar CSR non-zeros of the rows this handle forms (both triangles, R9) */
+  int64_t n_blocks;       /* d×d structural blocks of those rows */
+  int64_t n_contrib;      /* (tile, local row) -> block contributions to those rows */
+  int64_t n_multi_blocks; /* blocks with more than one contribution (K4 gathers them) */
   int64_t n_side_slots;   /* contributions to those blocks (K3 side slots, d² doubles each) */
+  /* shard (iga_shard; whole problem: 0, n_tiles, n_tiles, 0, n_dof) */
+  int64_t tile_begin;     /* first tile of the slab (global id) */
+  int64_t n_tiles_local;  /* tiles formed: slab + halo layer (local_values / coefficient rows) */
+  int64_t n_tiles_owned;  /* tiles of the slab (the sensitivity's partial sum) */
+  int64_t row_begin;      /* first CSR row (global scalar row = node*d + a) of this handle */
+  int64_t n_rows;         /* CSR rows of this handle: row_ptr has n_rows + 1 entries */
 } iga_sizes;
 
 /* ---------------------------------------------------------------------------
@@ -100,6 +119,7 @@ typedef struct {
  *  macro_topology           degree and knots of F (ctrl ignored) [host].
  *  q                        interpolation degree (0..4).
  *  n_gauss                  Gauss points per direction per span; 0 = p + ceil((q+1)/2) (R3).
+ *  shard                    NULL (whole problem) or the slab this handle forms (iga_shard).
  *  stream                   cudaStream_t used for the device work.
  *  out                      receives a new handle (owned by the caller; free with iga_free).
  * Device work: K1 (lookup tables 𝔎_p by micro Gauss quadrature, Eq. 52).
@@ -111,7 +131,7 @@ typedef struct {
 iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches,
                             const iga_interface *interfaces, int32_t n_interfaces,
                             const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
-                            void *stream, iga_handle **out);
+                            const iga_shard *shard, void *stream, iga_handle **out);
 
 /* iga_build_topology — host-only variant of iga_build_tables: validation, I_coo,
  * DofMap and the CSR pattern, no device work and no tables.  The handle answers
@@ -121,16 +141,17 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches,
 iga_status iga_build_topology(const iga_spline *tile_patches, int32_t n_patches,
                               const iga_interface *interfaces, int32_t n_interfaces,
                               const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
-                              iga_handle **out);
+                              const iga_shard *shard, iga_handle **out);
 
 /* ---------------------------------------------------------------------------
  * iga_assemble — form K^π (Eq. 50) into CSR values: the hot path (§3.2.4 steps 1-4).
  *  macro_ctrl   [any] n_macro_cp*d doubles: the control net of F (Eq. 4).
  *  young        [any] E: one double (young_per_tile = 0) or n_tiles doubles (= 1).
  *  nu           Poisson ratio, -1 < ν < 0.5.
- *  csr_values   [any] nnz doubles, overwritten, ordered as the pattern of iga_get_pattern.
- *  local_values [any] optional (NULL = skip): n_local_rows*n_tiles*d² doubles receiving
- *               nzdata (Eq. 58) as local[row][t*d² + a*d + b].
+ *  csr_values   [any] nnz doubles, overwritten, ordered as the pattern of iga_get_pattern
+ *               (the rows [row_begin, row_begin + n_rows) of K for a shard).
+ *  local_values [any] optional (NULL = skip): n_local_rows*n_tiles_local*d² doubles receiving
+ *               nzdata (Eq. 58) as local[row][t*d² + a*d + b], t = local tile index.
  * Kernels: K2 (per-tile ∇F at the (q+1)^d Gauss nodes -> Ā (Eq. 37) -> interpolation
  * coefficients, R1), K3 (FP64 DMMA contraction nzdata = mat𝔎·mat⟨Ā⟩, Eq. 58),
  * K4 (atomic-free owner-computes gather into the full symmetric CSR, R9).
@@ -143,7 +164,8 @@ iga_status iga_assemble(const iga_handle *h, const double *macro_ctrl, const dou
 /* ---------------------------------------------------------------------------
  * iga_sensitivity — g[k*d + α] = uᵀ (∂K^π/∂P_{k,α}) v for every macro control-point
  * coordinate (Eqs. 70-73; R13: u ≠ v allowed, K^π as assembled by R9).
- *  u, v  [any] n_dof doubles (interleaved DOF).   grad [any] n_macro_cp*d, overwritten.
+ *  u, v  [any] n_dof doubles (interleaved DOF).   grad [any] n_macro_cp*d, overwritten
+ *        (a shard: the sum over its owned tiles only; sum the shards' grads).
  * Kernels: K5a (W_t = mat𝔎ᵀ X_t, FP64 DMMA, X_t generated from u, v on the fly),
  * K5b (Ŵ = Πᵀ W, analytic reverse mode of Ā(J), chain to P), K5c (deterministic
  * reduction over the tiles sharing a control point).
@@ -160,16 +182,17 @@ iga_status iga_interpolate(const iga_handle *h, const double *macro_ctrl, const 
 /* Accessors.  iga_get_sizes: [host] out. */
 iga_status iga_get_sizes(const iga_handle *h, iga_sizes *out);
 
-/* iga_get_pattern — row_ptr (n_dof+1 int64), col_idx (nnz int32); either may be NULL.
- * [any] pointers. */
+/* iga_get_pattern — row_ptr (n_rows+1 int64, starting at 0), col_idx (nnz int32, global
+ * columns); either may be NULL.  [any] pointers. */
 iga_status iga_get_pattern(const iga_handle *h, int64_t *row_ptr, int32_t *col_idx);
 
-/* iga_get_block_map — for tiles [t_begin, t_end): (pos(I*d,J*d), pos(J*d,I*d)) per
- * (tile, local row) as 2 int64 each, tile-major (R9). [host] out. */
+/* iga_get_block_map — for local tiles [t_begin, t_end): (pos(I*d,J*d), pos(J*d,I*d)) per
+ * (tile, local row) as 2 int64 each, tile-major (R9); -1 where the row is not this
+ * handle's. [host] out. */
 iga_status iga_get_block_map(const iga_handle *h, int64_t t_begin, int64_t t_end, int64_t *out);
 
-/* iga_get_node_map — node[t*n_local_ctrl + off_p + A] for all tiles (R10). [host] out
- * (n_tiles * Σ_p n_ctrl,p int32).  */
+/* iga_get_node_map — global node[t*n_local_ctrl + off_p + A] for the local tiles (R10).
+ * [host] out (n_tiles_local * Σ_p n_ctrl,p int32).  */
 iga_status iga_get_node_map(const iga_handle *h, int32_t *out);
 
 /* iga_get_tables — the stacked table mat𝔎 (n_local_rows × n_k, row-major, unpadded). [any] */

@@ -59,13 +59,14 @@ def macro_active(prob, t):
     return M._active(prob.macro, M.tile_element(prob.macro, t))
 
 
-def sensitivity(prob, tabs, pattern, u, v, ctrl=None, entries=None):
-    """g (n_cp, d).  `entries`: optional list of (k, α) to compute (others left 0)."""
+def sensitivity(prob, tabs, pattern, u, v, ctrl=None, entries=None, tiles=None):
+    """g (n_cp, d).  `entries`: optional list of (k, α) to compute (others left 0);
+    `tiles`: optional subset of tiles whose terms of Eq. 73's sum over t are taken."""
     ctrl = prob.macro.ctrl if ctrl is None else ctrl
     d = prob.d
     g = np.zeros_like(ctrl, dtype=np.float64)
     want = None if entries is None else set((int(k), int(a)) for k, a in entries)
-    for t in range(prob.n_tiles):
+    for t in (range(prob.n_tiles) if tiles is None else tiles):
         act = macro_active(prob, t)
         if want is not None and not any((k, a) in want for k in act for a in range(d)):
             continue

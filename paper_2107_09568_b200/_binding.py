@@ -40,7 +40,13 @@ class iga_sizes(C.Structure):
                 ("k_stride", C.c_int32), ("n_patches", C.c_int32), ("n_gauss", C.c_int32), ("reserved", C.c_int32),
                 ("n_tiles", C.c_int64), ("n_local_rows", C.c_int64), ("n_macro_cp", C.c_int64),
                 ("n_nodes", C.c_int64), ("n_dof", C.c_int64), ("nnz", C.c_int64), ("n_blocks", C.c_int64),
-                ("n_contrib", C.c_int64), ("n_multi_blocks", C.c_int64), ("n_side_slots", C.c_int64)]
+                ("n_contrib", C.c_int64), ("n_multi_blocks", C.c_int64), ("n_side_slots", C.c_int64),
+                ("tile_begin", C.c_int64), ("n_tiles_local", C.c_int64), ("n_tiles_owned", C.c_int64),
+                ("row_begin", C.c_int64), ("n_rows", C.c_int64)]
+
+
+class iga_shard(C.Structure):
+    _fields_ = [("n_shards", C.c_int32), ("shard", C.c_int32)]
 
 
 N_PROF = 10   # IGA_N_PROF: 0 K2, 1 K3(+scatter), 2 K4, 3 K5a, 4 K5b, 5 K5c, 6 staging, 7 K5x, 8 K3 nzdata
@@ -60,9 +66,9 @@ def load():
     lib = C.CDLL(LIB_PATH)
     vp, i32, i64, d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     lib.iga_build_tables.argtypes = [C.POINTER(iga_spline), i32, C.POINTER(iga_interface), i32,
-                                     C.POINTER(iga_spline), i32, i32, vp, C.POINTER(vp)]
+                                     C.POINTER(iga_spline), i32, i32, C.POINTER(iga_shard), vp, C.POINTER(vp)]
     lib.iga_build_topology.argtypes = [C.POINTER(iga_spline), i32, C.POINTER(iga_interface), i32,
-                                       C.POINTER(iga_spline), i32, i32, C.POINTER(vp)]
+                                       C.POINTER(iga_spline), i32, i32, C.POINTER(iga_shard), C.POINTER(vp)]
     lib.iga_assemble.argtypes = [vp, vp, vp, i32, d, vp, vp, vp]
     lib.iga_sensitivity.argtypes = [vp, vp, vp, i32, d, vp, vp, vp, vp]
     lib.iga_interpolate.argtypes = [vp, vp, vp, i32, d, vp, vp]
@@ -132,9 +138,10 @@ def _spline(s, keep):
 
 class Assembler:
     """Handle around iga_build_tables for a problem description (synth.Problem-like:
-    .tile (patches), .interfaces, .macro (degree/knots), .q, .n_gauss)."""
+    .tile (patches), .interfaces, .macro (degree/knots), .q, .n_gauss).
+    shard=(n_shards, shard): form only that slab of the problem (iga_shard)."""
 
-    def __init__(self, prob, n_gauss=0, stream=None, topology_only=False):
+    def __init__(self, prob, n_gauss=0, stream=None, topology_only=False, shard=None):
         lib = load()
         keep = []
         arr = (iga_spline * len(prob.tile))(*[_spline(s, keep) for s in prob.tile])
@@ -142,13 +149,14 @@ class Assembler:
         for n, f in enumerate(prob.interfaces):
             ifs[n] = iga_interface(f.patch_a, f.dir_a, f.side_a, f.patch_b, f.dir_b, f.side_b)
         mac = _spline(prob.macro, keep)
+        sh = C.byref(iga_shard(int(shard[0]), int(shard[1]))) if shard is not None else None
         h = C.c_void_p()
         if topology_only:
             _check(lib.iga_build_topology(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), prob.q,
-                                          n_gauss, C.byref(h)))
+                                          n_gauss, sh, C.byref(h)))
         else:
             _check(lib.iga_build_tables(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), prob.q,
-                                        n_gauss, _stream_ptr(stream), C.byref(h)))
+                                        n_gauss, sh, _stream_ptr(stream), C.byref(h)))
         self._h = h
         self.sizes = iga_sizes()
         _check(lib.iga_get_sizes(h, C.byref(self.sizes)))
@@ -176,15 +184,15 @@ class Assembler:
         _check(load().iga_get_pattern(self._h, _ptr(row_ptr), _ptr(col_idx)))
 
     def block_map(self, t_begin=0, t_end=None):
-        t_end = self.sizes.n_tiles if t_end is None else t_end
+        t_end = self.sizes.n_tiles_local if t_end is None else t_end
         out = np.empty(((t_end - t_begin) * self.sizes.n_local_rows, 2), dtype=np.int64)
         _check(load().iga_get_block_map(self._h, t_begin, t_end, out.ctypes.data))
         return out
 
     def node_map_for(self, n_local_ctrl):
-        out = np.empty(self.sizes.n_tiles * n_local_ctrl, dtype=np.int32)
+        out = np.empty(self.sizes.n_tiles_local * n_local_ctrl, dtype=np.int32)
         _check(load().iga_get_node_map(self._h, out.ctypes.data))
-        return out.reshape(self.sizes.n_tiles, n_local_ctrl)
+        return out.reshape(self.sizes.n_tiles_local, n_local_ctrl)
 
     def tables(self):
         out = np.empty((self.sizes.n_local_rows, self.sizes.n_k), dtype=np.float64)

@@ -163,7 +163,7 @@ struct UF {
 };
 
 iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const iga_interface *ifc,
-                      int n_ifc, const iga_spline *macro, int q, int n_gauss) {
+                      int n_ifc, const iga_spline *macro, int q, int n_gauss, const iga_shard *shard) {
   if (!tile || n_patches <= 0 || !macro) { set_error("no tile patches or no macro topology"); return IGA_EINVAL; }
   const int d = tile[0].dim;
   if (d != 2 && d != 3) { set_error("dim must be 2 or 3 (got %d)", d); return IGA_EINVAL; }
@@ -340,23 +340,63 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
         if (ids[i] == ids[i - 1]) { set_error("tile %lld patch %d: two control points merged", (long long)t, pi); return IGA_ENONCONFORMING; }
     }
 
+  // ---- shard: slab of macro-element layers along the slowest direction
+  // plus one halo layer; owned rows = nodes first appearing in the slab (a contiguous
+  // id range, since ids follow first appearance over tiles).  Every tile containing an
+  // owned node lies in the slab or the halo layer, so owned rows are complete.
+  h.n_tiles_glob = nt;
+  h.n_nodes_glob = h.n_nodes;
+  {
+    int64_t tb = 0, te_own = nt, te = nt, n0 = 0, n1 = h.n_nodes;
+    if (shard && shard->n_shards > 1) {
+      const int kd = d - 1;
+      const int64_t layers = h.mel[kd], layer = nt / layers;
+      if (shard->shard < 0 || shard->shard >= shard->n_shards || shard->n_shards > layers) {
+        set_error("shard %d of %d: need 0 <= shard < n_shards <= %lld element layers", shard->shard, shard->n_shards,
+                  (long long)layers);
+        return IGA_EINVAL;
+      }
+      const int64_t l0 = shard->shard * layers / shard->n_shards, l1 = (shard->shard + 1) * layers / shard->n_shards;
+      tb = l0 * layer;
+      te_own = l1 * layer;
+      te = std::min(nt, te_own + layer);
+      int32_t mx = -1;
+      for (int64_t f = 0; f < tb * nl; ++f) mx = std::max(mx, h.node_map[f]);
+      n0 = mx + 1;
+      for (int64_t f = tb * nl; f < te_own * nl; ++f) mx = std::max(mx, h.node_map[f]);
+      n1 = mx + 1;
+      h.n_shards = shard->n_shards;
+      h.shard = shard->shard;
+    }
+    h.t_base = tb;
+    h.n_tiles_own = te_own - tb;
+    h.n_tiles = te - tb;
+    h.node_base = n0;
+    h.n_nodes = n1 - n0;
+    if (tb != 0 || te != nt)
+      h.node_map = std::vector<int32_t>(h.node_map.begin() + tb * nl, h.node_map.begin() + te * nl);
+  }
+
   // ---- pattern (R9) and the K3 fused-epilogue maps ------------------------------
   // Every (tile t, table row r) with I = node(A_r), J = node(B_r) contributes the local
   // block L to K(I,J) and Lᵀ to K(J,I).  Blocks with exactly one contribution are
   // written straight from the K3 epilogue (emap holds rank(J in row I) | rank(I in row
   // J) << 16); blocks with several contributions (tile faces, patch interfaces) get
   // one side slot per contribution and are summed in a fixed order by K4.
-  if (nt * h.M >= (int64_t(1) << 40)) { set_error("n_tiles * table rows exceeds 2^40"); return IGA_ELIMIT; }
+  // (local tiles lt = t - t_base; owned rows i = I - node_base; columns stay global)
+  const int64_t lnt = h.n_tiles, n0 = h.node_base;
+  if (lnt * h.M >= (int64_t(1) << 40)) { set_error("n_tiles * table rows exceeds 2^40"); return IGA_ELIMIT; }
   const int64_t nn = h.n_nodes;
+  auto own = [&](int64_t I) { return I >= n0 && I < n0 + nn; };
   std::vector<int64_t> cnt(nn + 1, 0);
   std::vector<std::atomic<int64_t>> acnt(nn);
   for (auto &a : acnt) a.store(0, std::memory_order_relaxed);
 #pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < nt; ++t)
+  for (int64_t t = 0; t < lnt; ++t)
     for (int64_t r = 0; r < h.M; ++r) {
       int32_t I = h.node_map[t * nl + h.pairA[r]], J = h.node_map[t * nl + h.pairB[r]];
-      acnt[I].fetch_add(1, std::memory_order_relaxed);
-      if (I != J) acnt[J].fetch_add(1, std::memory_order_relaxed);
+      if (own(I)) acnt[I - n0].fetch_add(1, std::memory_order_relaxed);
+      if (I != J && own(J)) acnt[J - n0].fetch_add(1, std::memory_order_relaxed);
     }
   for (int64_t i = 0; i < nn; ++i) cnt[i + 1] = cnt[i] + acnt[i].load(std::memory_order_relaxed);
   h.n_contrib = cnt[nn];
@@ -365,15 +405,17 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   for (int64_t i = 0; i < nn; ++i) acnt[i].store(cnt[i], std::memory_order_relaxed);
   std::vector<uint64_t> kcol(h.n_contrib);   // J per key (sort by (J, code))
 #pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < nt; ++t)
+  for (int64_t t = 0; t < lnt; ++t)
     for (int64_t r = 0; r < h.M; ++r) {
       int32_t I = h.node_map[t * nl + h.pairA[r]], J = h.node_map[t * nl + h.pairB[r]];
       uint64_t code = (uint64_t)(t * h.M + r) << 1;
-      int64_t k = acnt[I].fetch_add(1, std::memory_order_relaxed);
-      keys[k] = code;
-      kcol[k] = (uint64_t)J;
-      if (I != J) {
-        k = acnt[J].fetch_add(1, std::memory_order_relaxed);
+      if (own(I)) {
+        const int64_t k = acnt[I - n0].fetch_add(1, std::memory_order_relaxed);
+        keys[k] = code;
+        kcol[k] = (uint64_t)J;
+      }
+      if (I != J && own(J)) {
+        const int64_t k = acnt[J - n0].fetch_add(1, std::memory_order_relaxed);
         keys[k] = code | 1u;
         kcol[k] = (uint64_t)I;
       }
@@ -404,7 +446,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   h.nnz = h.n_blocks * d * d;
   if (h.n_blocks >= (int64_t(1) << 39)) { set_error("too many blocks"); return IGA_ELIMIT; }
   h.bcol.assign(h.n_blocks, 0);
-  h.emap.assign(nt * h.M, 0);
+  h.emap.assign(lnt * h.M, 0);
   uint16_t *e16 = reinterpret_cast<uint16_t *>(h.emap.data());
   std::vector<int64_t> mcount(nn + 1, 0), scount(nn + 1, 0);
   // pass 1: block columns, direct ranks, multi-block counts (canonical I <= J)
@@ -420,7 +462,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       if (k1 - k == 1) {
         const uint64_t code = keys[k] >> 1;
         e16[2 * code + (keys[k] & 1u)] = (uint16_t)(b - h.brow_ptr[i]);
-      } else if (J >= i) {
+      } else if (J >= i + n0 || !own(J)) {   // canonical row of a shared block
         mcount[i + 1] += 1;
         scount[i + 1] += k1 - k;
       }
@@ -448,12 +490,18 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       while (k1 < cnt[i + 1] && kcol[k1] == kcol[k]) ++k1;
       ++b;
       const int64_t J = (int64_t)kcol[k];
-      if (k1 - k > 1 && J >= i) {
+      if (k1 - k > 1 && (J >= i + n0 || !own(J))) {
         MultiBlock &mb = h.mblk[m];
         mb.off_ij = (int64_t)d * d * h.brow_ptr[i] + (int64_t)d * (b - h.brow_ptr[i]);
-        mb.off_ji = (int64_t)d * d * h.brow_ptr[J] + (int64_t)d * rank_in_row(J, i);
         mb.stride_i = (int32_t)(d * (h.brow_ptr[i + 1] - h.brow_ptr[i]));
-        mb.stride_j = (int32_t)(d * (h.brow_ptr[J + 1] - h.brow_ptr[J]));
+        if (own(J)) {
+          const int64_t j = J - n0;
+          mb.off_ji = (int64_t)d * d * h.brow_ptr[j] + (int64_t)d * rank_in_row(j, i + n0);
+          mb.stride_j = (int32_t)(d * (h.brow_ptr[j + 1] - h.brow_ptr[j]));
+        } else {   // row J belongs to another shard
+          mb.off_ji = -1;
+          mb.stride_j = 0;
+        }
         h.mslot0[m] = (int32_t)sl;
         for (int64_t kk = k; kk < k1; ++kk, ++sl) {
           h.slot_tr[sl] = (uint8_t)(keys[kk] & 1u);
@@ -473,7 +521,8 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       const MultiBlock &mb = h.mblk[m];
       // off_ji = d²·brow_ptr[J] + d·rank: recover J by binary search in brow_ptr
       const int64_t b = (mb.off_ji / d) / d;   // block index lower bound of row J
-      const int64_t J = std::upper_bound(h.brow_ptr.begin(), h.brow_ptr.end(), b) - h.brow_ptr.begin() - 1;
+      const int64_t J = mb.off_ji < 0 ? INT64_MAX
+                                      : std::upper_bound(h.brow_ptr.begin(), h.brow_ptr.end(), b) - h.brow_ptr.begin() - 1;
       rowJ[m] = J;
       colI[m] = mb.off_ij;   // (I, J) order already sorts by I within row J
     }
@@ -483,16 +532,16 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       return rowJ[x] != rowJ[y] ? rowJ[x] < rowJ[y] : colI[x] < colI[y];
     });
   }
-  h.rowinfo.assign(nt * nl, 0);
+  h.rowinfo.assign(lnt * nl, 0);
 #pragma omp parallel for schedule(static)
-  for (int64_t f = 0; f < nt * nl; ++f) {
+  for (int64_t f = 0; f < lnt * nl; ++f) {
     const int64_t I = h.node_map[f];
-    h.rowinfo[f] = (h.brow_ptr[I] << 24) | (h.brow_ptr[I + 1] - h.brow_ptr[I]);
+    h.rowinfo[f] = own(I) ? (h.brow_ptr[I - n0] << 24) | (h.brow_ptr[I - n0 + 1] - h.brow_ptr[I - n0]) : -1;
   }
 
   // ---- operand layouts: K3 A rows, coefficient rows, K5a padded reduction columns --
   h.Mpad = (h.M + IGA_K3_BM - 1) / IGA_K3_BM * IGA_K3_BM;
-  h.Npad = (nt * d * d + IGA_GEMM_BN - 1) / IGA_GEMM_BN * IGA_GEMM_BN;
+  h.Npad = (lnt * d * d + IGA_GEMM_BN - 1) / IGA_GEMM_BN * IGA_GEMM_BN;
   h.pcol.assign(n_patches + 1, 0);
   h.max_patch_ctrl = 0;
   for (int pi = 0; pi < n_patches; ++pi) {

@@ -163,7 +163,7 @@ const char *iga_version(void) { return "libiga 0.1 (sm_100a, FP64 DMMA)"; }
 
 iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
                             int32_t n_interfaces, const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
-                            void *stream, iga_handle **out) {
+                            const iga_shard *shard, void *stream, iga_handle **out) {
   if (!out) { set_error("out is NULL"); return IGA_EINVAL; }
   *out = nullptr;
   if (n_patches > 64) { set_error("at most 64 tile patches"); return IGA_EINVAL; }
@@ -174,7 +174,7 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, c
   cudaStream_t s = (cudaStream_t)stream;
   iga_status st;
   try {
-    st = build_host(h, tile_patches, n_patches, interfaces, n_interfaces, macro_topology, q, n_gauss);
+    st = build_host(h, tile_patches, n_patches, interfaces, n_interfaces, macro_topology, q, n_gauss, shard);
   } catch (std::bad_alloc &) {
     set_error("out of host memory during the host build");
     st = IGA_ENOMEM;
@@ -210,7 +210,7 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, c
   int nact_m = 1;
   for (int k = 0; k < d; ++k) nact_m *= h.pm[k] + 1;
   CUB(cudaMalloc((void **)&h.d_gpart, sizeof(double) * h.n_tiles * nact_m * d));
-  CUB(cudaMalloc((void **)&h.d_row_ptr, sizeof(int64_t) * (h.n_dof + 1)));
+  CUB(cudaMalloc((void **)&h.d_row_ptr, sizeof(int64_t) * (h.n_nodes * d + 1)));
   CUB(cudaMalloc((void **)&h.d_col_idx, sizeof(int32_t) * std::max<int64_t>(h.nnz, 1)));
   // macro knots / element spans
   std::vector<double> mk;
@@ -277,14 +277,14 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, c
 
 iga_status iga_build_topology(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
                               int32_t n_interfaces, const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
-                              iga_handle **out) {
+                              const iga_shard *shard, iga_handle **out) {
   if (!out) { set_error("out is NULL"); return IGA_EINVAL; }
   *out = nullptr;
   iga_handle *H = new (std::nothrow) iga_handle();
   if (!H) { set_error("out of host memory"); return IGA_ENOMEM; }
   iga_status st;
   try {
-    st = build_host(H->h, tile_patches, n_patches, interfaces, n_interfaces, macro_topology, q, n_gauss);
+    st = build_host(H->h, tile_patches, n_patches, interfaces, n_interfaces, macro_topology, q, n_gauss, shard);
   } catch (std::bad_alloc &) {
     set_error("out of host memory during the host build");
     st = IGA_ENOMEM;
@@ -307,16 +307,21 @@ iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
   o->k_stride = h.kstride;
   o->n_patches = h.n_patches;
   o->n_gauss = h.n_g;
-  o->n_tiles = h.n_tiles;
+  o->n_tiles = h.n_tiles_glob;
   o->n_local_rows = h.M;
   o->n_macro_cp = h.n_cp;
-  o->n_nodes = h.n_nodes;
+  o->n_nodes = h.n_nodes_glob;
   o->n_dof = h.n_dof;
   o->nnz = h.nnz;
   o->n_blocks = h.n_blocks;
   o->n_contrib = h.n_contrib;
   o->n_multi_blocks = h.n_multi;
   o->n_side_slots = h.n_slots;
+  o->tile_begin = h.t_base;
+  o->n_tiles_local = h.n_tiles;
+  o->n_tiles_owned = h.n_tiles_own;
+  o->row_begin = h.node_base * h.d;
+  o->n_rows = h.n_nodes * h.d;
   return IGA_OK;
 }
 
@@ -334,7 +339,7 @@ iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const do
   CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
   const double *dctrl, *dyoung;
   if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
-      !sg.in(young, young_per_tile ? (size_t)h.n_tiles : 1, &dyoung)) {
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles_glob : 1, &dyoung)) {
     set_error("staging of host inputs failed");
     return IGA_ENOMEM;
   }
@@ -382,7 +387,7 @@ iga_status iga_interpolate(const iga_handle *Hc, const double *macro_ctrl, const
   double *dcoef;
   const size_t ncoef = (size_t)h.n_tiles * h.d * h.d * h.kstride;
   if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
-      !sg.in(young, young_per_tile ? (size_t)h.n_tiles : 1, &dyoung) || !sg.out(coef, ncoef, &dcoef)) {
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles_glob : 1, &dyoung) || !sg.out(coef, ncoef, &dcoef)) {
     set_error("staging failed");
     return IGA_ENOMEM;
   }
@@ -412,7 +417,7 @@ iga_status iga_sensitivity(const iga_handle *Hc, const double *macro_ctrl, const
   const double *dctrl, *dyoung, *du, *dv;
   double *dgrad;
   if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
-      !sg.in(young, young_per_tile ? (size_t)h.n_tiles : 1, &dyoung) || !sg.in(u, (size_t)h.n_dof, &du) ||
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles_glob : 1, &dyoung) || !sg.in(u, (size_t)h.n_dof, &du) ||
       !sg.in(v, (size_t)h.n_dof, &dv) || !sg.out(grad, (size_t)(h.n_cp * h.d), &dgrad)) {
     set_error("staging failed");
     return IGA_ENOMEM;
@@ -442,7 +447,7 @@ iga_status iga_get_pattern(const iga_handle *Hc, int64_t *row_ptr, int32_t *col_
   if (!Hc) { set_error("NULL handle"); return IGA_EINVAL; }
   const Handle &h = Hc->h;
   if (h.on_device) {
-    if (row_ptr) CU(cudaMemcpy(row_ptr, h.d_row_ptr, sizeof(int64_t) * (h.n_dof + 1), cudaMemcpyDefault));
+    if (row_ptr) CU(cudaMemcpy(row_ptr, h.d_row_ptr, sizeof(int64_t) * (h.n_nodes * h.d + 1), cudaMemcpyDefault));
     if (col_idx) CU(cudaMemcpy(col_idx, h.d_col_idx, sizeof(int32_t) * h.nnz, cudaMemcpyDefault));
     return IGA_OK;
   }
@@ -458,7 +463,7 @@ iga_status iga_get_pattern(const iga_handle *Hc, int64_t *row_ptr, int32_t *col_
           for (int b = 0; b < d; ++b) col_idx[base + d * j + b] = h.bcol[b0 + j] * d + b;
     }
   }
-  if (row_ptr) row_ptr[h.n_dof] = h.nnz;
+  if (row_ptr) row_ptr[h.n_nodes * d] = h.nnz;
   return IGA_OK;
 }
 
@@ -469,9 +474,11 @@ iga_status iga_get_block_map(const iga_handle *Hc, int64_t t_begin, int64_t t_en
   const int d = h.d;
   const int64_t nl = h.n_local_ctrl;
   auto pos = [&](int64_t I, int64_t J) -> int64_t {
-    const int32_t *b = h.bcol.data() + h.brow_ptr[I], *e = h.bcol.data() + h.brow_ptr[I + 1];
+    const int64_t i = I - h.node_base;
+    if (i < 0 || i >= h.n_nodes) return -1;   // row of another shard
+    const int32_t *b = h.bcol.data() + h.brow_ptr[i], *e = h.bcol.data() + h.brow_ptr[i + 1];
     const int32_t *f = std::lower_bound(b, e, (int32_t)J);
-    return (int64_t)d * d * h.brow_ptr[I] + (int64_t)d * (f - b);
+    return (int64_t)d * d * h.brow_ptr[i] + (int64_t)d * (f - b);
   };
 #pragma omp parallel for schedule(static)
   for (int64_t t = t_begin; t < t_end; ++t)

@@ -67,9 +67,15 @@ struct Handle {
   int mel[3] = {1, 1, 1};        // macro elements per dir
   std::vector<double> mknots[3];
   std::vector<int> mel_span[3];
-  int64_t n_cp = 0, n_tiles = 0;
+  int64_t n_cp = 0;
+  // tiles: global count; this handle's local tiles [t_base, t_base + n_tiles) of which the
+  // first n_tiles_own are owned (the rest is the halo layer of a shard)
+  int64_t n_tiles_glob = 0, t_base = 0, n_tiles = 0, n_tiles_own = 0;
+  int32_t n_shards = 1, shard = 0;
   // global numbering / pattern
-  int64_t n_nodes = 0, n_dof = 0, nnz = 0, n_blocks = 0, n_contrib = 0;
+  // nodes: global count; owned (CSR) rows are nodes [node_base, node_base + n_nodes);
+  // n_dof = global DOF count (length of u, v); nnz / n_blocks are the owned rows'
+  int64_t n_nodes_glob = 0, node_base = 0, n_nodes = 0, n_dof = 0, nnz = 0, n_blocks = 0, n_contrib = 0;
   std::vector<int32_t> node_map;     // [n_tiles][n_local_ctrl]
   std::vector<int64_t> brow_ptr;     // [n_nodes+1]
   std::vector<int32_t> bcol;         // [n_blocks]
@@ -138,6 +144,8 @@ struct Handle {
 // --- device constants shared by kernels (set by api) ---
 struct InterpConst {
   int d, q, pm[3], mn[3], mel[3], moff[3], soff[3];   // offsets of direction k in d_mknots / d_mspan
+  int64_t t_base;        // global id of local tile 0
+  int64_t n_own;         // owned local tiles (sensitivity reduction)
   double Pi1[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
   double x[IGA_MAXQ + 1];
 };
@@ -164,7 +172,7 @@ InterpConst make_interp_const(const Handle &h);
 
 // host build steps (host_build.cpp)
 iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const iga_interface *ifc,
-                      int n_ifc, const iga_spline *macro, int q, int n_gauss);
+                      int n_ifc, const iga_spline *macro, int q, int n_gauss, const iga_shard *shard);
 void gauss_legendre01(int n, double *x, double *w);
 iga_status upload_topology(Handle &h);
 

@@ -251,12 +251,12 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
 #pragma unroll
       for (int q = 0; q < DD; ++q) o[q] = L[q];
     }
-    const bool w1 = live && ev >= 0;
+    const bool w1 = live && ev >= 0 && riA[k] >= 0;   // riA < 0: row of another shard
     const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff), str1 = D * (riA[k] & 0xffffff);
 #pragma unroll
     for (int a = 0; a < D; ++a) coop(w1 ? off1 + a * str1 : -1, er, A == B, tl, a, false);
     const int32_t evt = emt[k];
-    const bool w2 = live_t && evt >= 0 && At != Bt;
+    const bool w2 = live_t && evt >= 0 && At != Bt && riB[k] >= 0;
     const int64_t off2 = DD * (riB[k] >> 24) + D * (evt >> 16), str2 = D * (riB[k] & 0xffffff);
 #pragma unroll
     for (int b = 0; b < D; ++b) coop(w2 ? off2 + b * str2 : -1, et, false, tl, b, true);
@@ -436,9 +436,10 @@ static cudaError_t launch_k5x(const Handle &h, const double *u, const double *v,
   const size_t smem = k5x_smem_bytes(D, h.max_patch_ctrl);
   cudaError_t e = cudaFuncSetAttribute(k5x_gen<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
-  dim3 grid((unsigned)h.n_patches, (unsigned)(h.Npad / BN));
+  // the sensitivity runs over the owned tiles (the first n_tiles_own local tiles)
+  dim3 grid((unsigned)h.n_patches, (unsigned)((h.n_tiles_own * D * D + BN - 1) / BN));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k5x_gen<D><<<grid, 128, smem, s>>>(h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, u, v, h.n_tiles,
+  k5x_gen<D><<<grid, 128, smem, s>>>(h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, u, v, h.n_tiles_own,
                                      (int)(h.Kp / BK), h.d_X);
   return cudaGetLastError();
 }
@@ -450,9 +451,9 @@ cudaError_t launch_sens_X(const Handle &h, const double *u, const double *v, cud
 cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k5a_wgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM);
   if (e) return e;
-  dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)(h.Npad / BN));
+  dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)((h.n_tiles_own * h.d * h.d + BN - 1) / BN));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k5a_wgemm<<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), h.n_tiles * h.d * h.d, W,
+  k5a_wgemm<<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), h.n_tiles_own * h.d * h.d, W,
                                               h.kstride);
   return cudaGetLastError();
 }

@@ -30,6 +30,8 @@ InterpConst make_interp_const(const Handle &h) {
     off += (k < h.d) ? (int)h.mknots[k].size() : 0;
     soff += (k < h.d) ? (int)h.mel_span[k].size() : 0;
   }
+  ic.t_base = h.t_base;
+  ic.n_own = h.n_tiles_own;
   for (int i = 0; i < (IGA_MAXQ + 1) * (IGA_MAXQ + 1); ++i) ic.Pi1[i] = h.Pi1[i];
   for (int i = 0; i <= IGA_MAXQ; ++i) ic.x[i] = h.interp_x[i];
   return ic;
@@ -190,14 +192,15 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   const int tl = threadIdx.x / NC, comp = threadIdx.x % NC;
   const int64_t t = (int64_t)blockIdx.x * TPB + tl;
   const bool live = t < n_tiles;
-  if (live) load_macro_tile<D>(c_ip, mt[tl], t, ctrl, mknots, mspan, comp, NC);
+  const int64_t tg = t + c_ip.t_base;   // global tile id (macro element, E, error report)
+  if (live) load_macro_tile<D>(c_ip, mt[tl], tg, ctrl, mknots, mspan, comp, NC);
   __syncthreads();
   if (live)
     for (int m = comp; m < NPI; m += NC) {
       double J[D][D], G[D][D];
       macro_J<D>(c_ip, mt[tl], m, J);
       const double det = det_inv<D>(J, G);
-      if (!(det > 0.0)) raise_flag(flag, 2, (int)t, m);
+      if (!(det > 0.0)) raise_flag(flag, 2, (int)tg, m);
       NodeGeo<D> &o = geo[tl][m];
       for (int i = 0; i < D; ++i)
         for (int j = 0; j < D; ++j) {
@@ -211,7 +214,7 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   __syncthreads();
   if (!live) return;
   double lam, mu;
-  lame(young[ypt ? t : 0], nu, lam, mu);
+  lame(young[ypt ? tg : 0], nu, lam, mu);
   const int ij = comp / DD, ab = comp % DD, i = ij / D, j = ij % D, a = ab / D, b = ab % D;
   double x[NPI], y[NPI];
 #pragma unroll
@@ -269,12 +272,12 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
   double *S0 = dyn, *S1 = dyn + NPI * NC;
   __shared__ MacroTile<D> mt;
   __shared__ NodeGeo<D> geo[NPI];
-  const int64_t t = blockIdx.x;
-  load_macro_tile<D>(c_ip, mt, t, ctrl, mknots, mspan);
+  const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
+  load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
   __syncthreads();
-  node_geometry<D, Q>(c_ip, mt, geo, t, flag);
+  node_geometry<D, Q>(c_ip, mt, geo, tg, flag);
   double lam, mu;
-  lame(young[ypt ? t : 0], nu, lam, mu);
+  lame(young[ypt ? tg : 0], nu, lam, mu);
   __syncthreads();
   for (int it = threadIdx.x; it < NPI * DD; it += blockDim.x) {   // Ā (Eq. 37, closed form)
     const int m = it / DD, ij = it % DD, i = ij / D, j = ij % D;
@@ -309,18 +312,18 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
   double *S0 = dyn, *S1 = dyn + NPI * NC, *dSdJ = dyn + 2 * NPI * NC;
   __shared__ MacroTile<D> mt;
   __shared__ NodeGeo<D> geo[NPI];
-  const int64_t t = blockIdx.x;
-  load_macro_tile<D>(c_ip, mt, t, ctrl, mknots, mspan);
+  const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
+  load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
   const double *src = W + (size_t)t * DD * kstride;
   for (int idx = threadIdx.x; idx < DD * NK; idx += blockDim.x) {
     const int ab = idx / NK, kap = idx % NK, ij = kap / NPI, C = kap % NPI;
     S0[C * NC + ij * DD + ab] = src[(size_t)ab * kstride + kap];
   }
   __syncthreads();
-  node_geometry<D, Q>(c_ip, mt, geo, t, flag);
+  node_geometry<D, Q>(c_ip, mt, geo, tg, flag);
   const double *Wh_all = tensor_apply<D, Q, true, NC>(c_ip, S0, S1);   // Ŵ = Πᵀ W (also syncs geo)
   double lam, mu;
-  lame(young[ypt ? t : 0], nu, lam, mu);
+  lame(young[ypt ? tg : 0], nu, lam, mu);
   for (int m = threadIdx.x; m < NPI; m += blockDim.x) {
     const double *Wh = Wh_all + m * NC;   // Ŵ[ij*DD + ab]
     const NodeGeo<D> &g = geo[m];
@@ -411,7 +414,8 @@ __global__ void k5c_reduce(const __grid_constant__ InterpConst c_ip, const int *
         int s0 = mspan[c_ip.soff[0] + e0];
         int r0 = ii[0] - (s0 - c_ip.pm[0]);
         if (r0 < 0 || r0 > c_ip.pm[0]) continue;
-        int64_t t = e0 + (int64_t)c_ip.mel[0] * (e1 + (int64_t)c_ip.mel[1] * e2);
+        const int64_t t = e0 + (int64_t)c_ip.mel[0] * (e1 + (int64_t)c_ip.mel[1] * e2) - c_ip.t_base;
+        if (t < 0 || t >= c_ip.n_own) continue;   // tile of another shard (or this shard's halo)
         int ra = r0 + n1[0] * (r1 + n1[1] * r2);
         acc += gpart[((size_t)t * nact + ra) * D + a];
       }
@@ -446,7 +450,7 @@ static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double 
   const size_t sm = sizeof(double) * (2 * NPI * D * D * D * D + NPI * D * D);
   cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
-  k5b_reverse<D, Q><<<(unsigned)h.n_tiles, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
+  k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
                                                         ypt, nu, W, h.kstride, gpart, h.d_flag);
   return cudaGetLastError();
 }

@@ -88,7 +88,8 @@ k4_multi(const double *__restrict__ side, const MultiBlock *__restrict__ mblk, c
   const bool dg1 = b1.off_ij == b1.off_ji;
 #pragma unroll
   for (int a = 0; a < D; ++a) coop(live ? b1.off_ij + a * b1.stride_i : -1, dg1, 0, a);
-  const bool w2 = live && b2.off_ij != b2.off_ji;   // diagonal blocks are complete after pass 1
+  // diagonal blocks are complete after pass 1; off_ji < 0: row J belongs to another shard
+  const bool w2 = live && b2.off_ji >= 0 && b2.off_ij != b2.off_ji;
 #pragma unroll
   for (int b = 0; b < D; ++b) coop(w2 ? b2.off_ji + b * b2.stride_j : -1, false, 1, b);
 }

@@ -268,3 +268,35 @@ def test_invalid_arguments_raise():
     p3.tile[0].ctrl[14] = p3.tile[0].ctrl[15] + np.array([0.3, 0.0])   # folds the tile
     with pytest.raises(IgaError, match="EDEGENERATE|EINVAL"):
         Assembler(p3)
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("c,n", [(2, 2), (3, 3)])
+def test_sharded_assembly_and_gradient(c, n):
+    """One problem in n slabs (iga_shard): each shard's CSR rows are
+    bit-identical to the whole problem's rows, and the shards' partial gradients sum to
+    the whole gradient (the all-reduce of the multi-GPU step, done here on one GPU)."""
+    from paper_2107_09568_b200 import Assembler
+    from synth import draw_uv_seeded
+    g = gpu_case(c)
+    prob, A = g["prob"], g["A"]
+    s = A.sizes
+    rp = torch.empty(s.n_dof + 1, dtype=torch.int64, device="cuda")
+    A.pattern(rp, None)
+    rp = rp.cpu().numpy()
+    u, v = draw_uv_seeded(c, s.n_dof)
+    ut, vt = torch.tensor(u, device="cuda"), torch.tensor(v, device="cuda")
+    gfull = torch.empty(s.n_macro_cp * prob.d, dtype=torch.float64, device="cuda")
+    A.sensitivity(g["ctrl"], g["young"], prob.nu, ut, vt, gfull)
+    gsum = torch.zeros_like(gfull)
+    for k in range(n):
+        B = Assembler(prob, shard=(n, k))
+        z = B.sizes
+        vals = torch.empty(z.nnz, dtype=torch.float64, device="cuda")
+        B.assemble(g["ctrl"], g["young"], prob.nu, vals)
+        a, b = rp[z.row_begin], rp[z.row_begin + z.n_rows]
+        assert torch.equal(vals, g["vals"][a:b]), k
+        gk = torch.empty_like(gfull)
+        B.sensitivity(g["ctrl"], g["young"], prob.nu, ut, vt, gk)
+        gsum += gk
+    assert (torch.linalg.norm(gsum - gfull) / torch.linalg.norm(gfull)).item() < 1e-13

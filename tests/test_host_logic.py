@@ -113,3 +113,100 @@ def test_reference_arm_json():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["unit"] == "tiles/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+# ---------------------------------------------------------------------------
+# sharding one problem (include/iga.h iga_shard): host topology
+
+@pytest.mark.parametrize("c,n", [(2, 2), (3, 3)])
+def test_shard_topology_partitions_rows_and_tiles(c, n):
+    """Each shard's CSR rows are exactly the corresponding rows of the whole problem's
+    pattern; row ranges and owned tiles partition the problem."""
+    from paper_2107_09568_b200 import Assembler
+    from synth import make_config
+    prob = make_config(c)
+    full = Assembler(prob, topology_only=True)
+    fs = full.sizes
+    rp = np.empty(fs.n_dof + 1, np.int64)
+    ci = np.empty(fs.nnz, np.int32)
+    full.pattern(rp, ci)
+    nl = sum(p.n_ctrl for p in prob.tile)
+    nm_full = full.node_map_for(nl)
+    row, tile = 0, 0
+    for s in range(n):
+        A = Assembler(prob, topology_only=True, shard=(n, s))
+        z = A.sizes
+        assert (z.n_dof, z.n_tiles, z.n_nodes) == (fs.n_dof, fs.n_tiles, fs.n_nodes)
+        assert z.row_begin == row and z.tile_begin == tile
+        r1 = row + z.n_rows
+        srp = np.empty(z.n_rows + 1, np.int64)
+        sci = np.empty(z.nnz, np.int32)
+        A.pattern(srp, sci)
+        assert np.array_equal(srp, rp[row:r1 + 1] - rp[row])
+        assert np.array_equal(sci, ci[rp[row]:rp[r1]])
+        assert np.array_equal(A.node_map_for(nl), nm_full[tile:tile + z.n_tiles_local])
+        assert z.n_tiles_local - z.n_tiles_owned in (0, prob.n_tiles // prob.n_el[-1])   # one halo layer
+        # block map: positions of owned rows shifted by the shard's first value, -1 elsewhere
+        bm = A.block_map(0, 2)
+        bf = full.block_map(tile, tile + 2)
+        shift = rp[row]
+        ok = bm >= 0
+        assert np.array_equal(bm[ok], bf[ok] - shift)
+        assert np.all((bf[~ok] < shift) | (bf[~ok] >= rp[r1]))
+        row, tile = r1, tile + z.n_tiles_owned
+    assert row == fs.n_dof and tile == fs.n_tiles
+
+
+def _shard_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    from paper_2107_09568_b200 import Assembler
+    from paper_2107_09568_b200.shard import allreduce_grad, shard_of
+    from synth import make_config, draw_uv_seeded
+    from oracle.assemble import Tables
+    from oracle.dofmap import DofMap, Pattern
+    from oracle import sensitivity as S
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    prob = make_config(2, n_el=(2, 2, 2))
+    z = Assembler(prob, topology_only=True, shard=shard_of(rank, world)).sizes
+    ranges = [None] * world
+    dist.all_gather_object(ranges, (z.row_begin, z.n_rows, z.tile_begin, z.n_tiles_owned, z.nnz))
+    # the data-path collective of the sharded step: partial gradients over owned tiles
+    dm = DofMap(prob)
+    tabs = Tables(prob)
+    pt = Pattern(prob, dm, tabs.pairs)
+    u, v = draw_uv_seeded(2, dm.n_dof)
+    own = range(z.tile_begin, z.tile_begin + z.n_tiles_owned)
+    g = torch.tensor(S.sensitivity(prob, tabs, pt, u, v, tiles=own))
+    allreduce_grad(g, world)
+    full = S.sensitivity(prob, tabs, pt, u, v) if rank == 0 else None
+    q.put((rank, ranges, g.numpy(), full))
+    dist.destroy_process_group()
+
+
+def test_shard_gradient_allreduce_gloo():
+    """world_size 2 (gloo, CPU): shards partition rows and tiles, and the all-reduce of the
+    per-shard partial gradients (oracle arithmetic over each rank's owned tiles) equals
+    the whole problem's gradient."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000)
+    ps = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, ranges, g, full = q.get(timeout=600)
+        res[r] = (ranges, g, full)
+    for p in ps:
+        p.join(60)
+    ranges = res[0][0]
+    assert ranges == res[1][0]
+    (rb0, nr0, tb0, nt0, _), (rb1, nr1, tb1, nt1, _) = ranges
+    assert rb0 == 0 and rb1 == nr0 and tb0 == 0 and tb1 == nt0 and nt0 + nt1 == 8
+    full = res[0][2]
+    for r in range(2):
+        assert np.abs(res[r][1] - full).max() < 1e-13 * np.abs(full).max()
