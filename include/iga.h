@@ -174,6 +174,20 @@ iga_status iga_sensitivity(const iga_handle *h, const double *macro_ctrl, const 
                            int32_t young_per_tile, double nu, const double *u, const double *v,
                            double *grad, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * iga_apply — matrix-free y = K^π u (Eq. 74: "the multiplication of a vector
+ * with the system matrix with only the lookup table and the projection coefficients at
+ * hand").  K is never stored: K2, then the K3 contraction whose epilogue
+ * multiplies every element block with u and sums the products of each run of equal local
+ * row / column index into a partial slot, then a gather of the partials per node in a
+ * fixed order (deterministic, no atomics).  Equals the CSR product of iga_assemble's K.
+ *  u  [any] n_dof doubles (global).   y [any] n_rows doubles (this handle's rows), overwritten.
+ * Device memory: n_tiles_local * P * d doubles of partials, allocated by the first call.
+ * Errors: EINVAL, EDEGENERATE, ENOMEM, ECUDA.
+ * ------------------------------------------------------------------------- */
+iga_status iga_apply(const iga_handle *h, const double *macro_ctrl, const double *young,
+                     int32_t young_per_tile, double nu, const double *u, double *y, void *stream);
+
 /* iga_interpolate — K2 only (parity): coefficients ⟨Ā_ij⟩_C of every tile, written as
  * coef[(t*d² + a*d + b)*k_stride + κ] with κ = (i*d + j)*n_pi + C.  [any] pointers. */
 iga_status iga_interpolate(const iga_handle *h, const double *macro_ctrl, const double *young,
@@ -205,7 +219,8 @@ iga_status iga_get_pairs(const iga_handle *h, int32_t *out);
  * profiling is enabled (CUDA events on the caller's stream).  IGA_N_PROF slots:
  * 0 K2 interpolate, 1 K3 contraction + fused scatter, 2 K4 multi-contribution gather,
  * 3 K5a W-GEMM, 4 K5b reverse, 5 K5c reduce, 6 host<->device staging, 7 K5x X generation,
- * 8 K3 nzdata output (local_values).  enable != 0 resets the accumulators. */
+ * 8 K3 nzdata output (local_values), 9 matrix-free apply (K3 apply epilogue + gather).
+ * enable != 0 resets the accumulators. */
 #define IGA_N_PROF 10
 iga_status iga_set_profiling(iga_handle *h, int32_t enable);
 iga_status iga_get_kernel_times(const iga_handle *h, double *ms_out /* IGA_N_PROF */,

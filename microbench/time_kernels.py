@@ -7,6 +7,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--apply", action="store_true")
     args = ap.parse_args()
     import torch
     from paper_2107_09568_b200 import Assembler
@@ -21,14 +22,17 @@ def main():
     u, v = draw_uv_seeded(args.config, s.n_dof)
     u, v = torch.tensor(u, device=dev), torch.tensor(v, device=dev)
     grad = torch.empty(s.n_macro_cp * prob.d, dtype=torch.float64, device=dev)
+    y = torch.empty(s.n_dof, dtype=torch.float64, device=dev)
     for it in range(2):
         A.set_profiling(it == 1)
         for _ in range(args.reps if it else 2):
             A.assemble(ctrl, young, prob.nu, vals)
             A.sensitivity(ctrl, young, prob.nu, u, v, grad)
+            if args.apply:
+                A.apply(ctrl, young, prob.nu, u, y)
         torch.cuda.synchronize()
     ms, n = A.kernel_times()
-    names = ["K2", "K3", "K4", "K5a", "K5b", "K5c", "stage", "K5x", "K3local", "-"]
+    names = ["K2", "K3", "K4", "K5a", "K5b", "K5c", "stage", "K5x", "K3local", "apply"]
     flops = 2.0 * s.n_local_rows * s.n_k * s.n_tiles * prob.d ** 2
     out = {nm: round(ms[i] / max(n[i], 1), 4) for i, nm in enumerate(names) if n[i]}
     out["K3_tflops"] = round(flops / (out["K3"] * 1e-3) / 1e12, 2)

@@ -52,6 +52,14 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
       !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
       !up((void **)&h.d_tperm, h.tperm.data(), h.tperm.size()) ||
+      !up((void **)&h.d_g1len, h.g1len.data(), h.g1len.size() * 2) ||
+      !up((void **)&h.d_g2len, h.g2len.data(), h.g2len.size() * 2) ||
+      !up((void **)&h.d_g1slot, h.g1slot.data(), h.g1slot.size() * 4) ||
+      !up((void **)&h.d_g2slot, h.g2slot.data(), h.g2slot.size() * 4) ||
+      !up((void **)&h.d_sA_ptr, h.sA_ptr.data(), h.sA_ptr.size() * 4) ||
+      !up((void **)&h.d_sA_slot, h.sA_slot.data(), h.sA_slot.size() * 4) ||
+      !up((void **)&h.d_inv_ptr, h.inv_ptr.data(), h.inv_ptr.size() * 8) ||
+      !up((void **)&h.d_inv_ent, h.inv_ent.data(), h.inv_ent.size() * 4) ||
       !up((void **)&h.d_patch_info, pinfo.data(), pinfo.size() * 4))
     return IGA_ENOMEM;
   if (cudaMalloc((void **)&h.d_side, std::max<size_t>(8, (size_t)h.n_slots * h.d * h.d * 8)) != cudaSuccess) {
@@ -64,6 +72,8 @@ iga_status upload_topology(Handle &h) {
   std::vector<MultiBlock>().swap(h.mblk);
   std::vector<int32_t>().swap(h.mslot0);
   std::vector<int32_t>().swap(h.mperm);
+  std::vector<int64_t>().swap(h.inv_ptr);
+  std::vector<int32_t>().swap(h.inv_ent);
   std::vector<uint8_t>().swap(h.slot_tr);
   return IGA_OK;
 }
@@ -562,6 +572,50 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       return h.pairB[rx] != h.pairB[ry] ? h.pairB[rx] < h.pairB[ry] : h.pairA[rx] < h.pairA[ry];
     });
     for (int k = 0; k < IGA_K3_BM; ++k) h.tperm[m0 + k] = (uint8_t)idx[k];
+  }
+  // matrix-free apply maps (tile-independent, NEXT N1)
+  {
+    h.g1len.assign(h.Mpad, 0);
+    h.g2len.assign(h.Mpad, 0);
+    h.g1slot.assign(h.Mpad, -1);
+    h.g2slot.assign(h.Mpad, -1);
+    std::vector<int32_t> key;   // local control point receiving each slot
+    for (int64_t m0 = 0; m0 < h.Mpad; m0 += IGA_K3_BM) {
+      for (int e = 0; e < IGA_K3_BM && m0 + e < h.M;) {   // runs of equal A in row order
+        int f = e + 1;
+        while (f < IGA_K3_BM && m0 + f < h.M && h.pairA[m0 + f] == h.pairA[m0 + e]) ++f;
+        h.g1len[m0 + e] = (uint16_t)(f - e);
+        h.g1slot[m0 + e] = (int32_t)key.size();
+        key.push_back(h.pairA[m0 + e]);
+        e = f;
+      }
+      for (int q = 0; q < IGA_K3_BM;) {   // runs of equal B in tperm order (diagonal rows add 0)
+        const int64_t r = m0 + h.tperm[m0 + q];
+        if (r >= h.M) break;
+        int f = q + 1;
+        while (f < IGA_K3_BM && m0 + h.tperm[m0 + f] < h.M && h.pairB[m0 + h.tperm[m0 + f]] == h.pairB[r]) ++f;
+        h.g2len[m0 + q] = (uint16_t)(f - q);
+        h.g2slot[m0 + q] = (int32_t)key.size();
+        key.push_back(h.pairB[r]);
+        q = f;
+      }
+    }
+    h.P = (int64_t)key.size();
+    h.sA_ptr.assign(nl + 1, 0);
+    for (int32_t k : key) h.sA_ptr[k + 1]++;
+    for (int64_t a = 0; a < nl; ++a) h.sA_ptr[a + 1] += h.sA_ptr[a];
+    h.sA_slot.assign(h.P, 0);
+    std::vector<int32_t> fill(h.sA_ptr.begin(), h.sA_ptr.end() - 1);
+    for (int64_t p = 0; p < h.P; ++p) h.sA_slot[fill[key[p]]++] = (int32_t)p;
+    // owned node -> (local tile, A) occurrences, sorted by (tile, A)
+    h.inv_ptr.assign(nn + 1, 0);
+    for (int64_t f = 0; f < lnt * nl; ++f)
+      if (own(h.node_map[f])) h.inv_ptr[h.node_map[f] - n0 + 1]++;
+    for (int64_t i = 0; i < nn; ++i) h.inv_ptr[i + 1] += h.inv_ptr[i];
+    h.inv_ent.assign(h.inv_ptr[nn], 0);
+    std::vector<int64_t> fi(h.inv_ptr.begin(), h.inv_ptr.end() - 1);
+    for (int64_t f = 0; f < lnt * nl; ++f)
+      if (own(h.node_map[f])) h.inv_ent[fi[h.node_map[f] - n0]++] = (int32_t)f;
   }
   h.k5_pair.assign(h.Kp, -1);
   h.k5_col.assign(h.M, 0);

@@ -12,7 +12,8 @@ const char *get_error();
 Handle::~Handle() {
   void *bufs[] = {d_table, d_tabA, d_tabAT, d_coef, d_side, d_W, d_X, d_gpart, d_node_map, d_pairA, d_pairB,
                   d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_mperm, d_slot_tr,
-                  d_k5_pair, d_k5_col, d_tperm, d_patch_info, d_mknots, d_mspan, d_flag};
+                  d_k5_pair, d_k5_col, d_tperm, d_g1len, d_g2len, d_g1slot, d_g2slot, d_sA_ptr, d_sA_slot,
+                  d_inv_ptr, d_inv_ent, d_part, d_patch_info, d_mknots, d_mspan, d_flag};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (int i = 0; i < N_STAGE; ++i)
@@ -366,6 +367,49 @@ iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const do
   }
   idst = pf.begin(6);
   if (!sg.flush()) { set_error("D2H copy of outputs failed"); return IGA_ECUDA; }
+  pf.end(idst);
+  st = check_flag(h, s);
+  pf.collect();
+  return st;
+}
+
+iga_status iga_apply(const iga_handle *Hc, const double *macro_ctrl, const double *young, int32_t young_per_tile,
+                     double nu, const double *u, double *y, void *stream) {
+  if (!Hc || !macro_ctrl || !u || !y) { set_error("NULL argument"); return IGA_EINVAL; }
+  Handle &h = const_cast<iga_handle *>(Hc)->h;
+  if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
+  iga_status st = check_material(h, young, nu);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h.d_part) {   // partial slots: allocated on first use (assemble-only users never pay it)
+    const size_t bytes = std::max<size_t>(8, sizeof(double) * (size_t)h.n_tiles * h.P * h.d);
+    if (cudaMalloc((void **)&h.d_part, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("cudaMalloc of %zu bytes of apply partials failed", bytes);
+      return IGA_ENOMEM;
+    }
+  }
+  Stager sg(h, s);
+  Prof pf(h, s);
+  int idst = pf.begin(6);
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  const double *dctrl, *dyoung, *du;
+  double *dy;
+  if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles_glob : 1, &dyoung) || !sg.in(u, (size_t)h.n_dof, &du) ||
+      !sg.out(y, (size_t)(h.n_nodes * h.d), &dy)) {
+    set_error("staging failed");
+    return IGA_ENOMEM;
+  }
+  pf.end(idst);
+  int id = pf.begin(0);
+  CU(launch_interpolate(h, dctrl, dyoung, young_per_tile, nu, h.d_coef, true, s));
+  pf.end(id);
+  id = pf.begin(9);
+  CU(launch_apply(h, du, dy, s));
+  pf.end(id);
+  idst = pf.begin(6);
+  if (!sg.flush()) { set_error("D2H copy failed"); return IGA_ECUDA; }
   pf.end(idst);
   st = check_flag(h, s);
   pf.collect();

@@ -97,6 +97,14 @@ struct Handle {
   std::vector<int32_t> k5_pair;      // [Kp] patch-local (A | B << 16), -1 = padding
   std::vector<int32_t> k5_col;       // [M] padded column of each table row
   std::vector<uint8_t> tperm;        // [Mpad] K3 transposed-pass row order within each 128-row block
+  // matrix-free apply (NEXT N1, Eq. 74): per 128-row block, runs of rows with equal A (row
+  // order) and equal B (tperm order) are summed into one partial slot each (tile-independent)
+  int64_t P = 0;                     // partial slots per tile
+  std::vector<uint16_t> g1len, g2len;   // [Mpad] run length at a run's first position, else 0
+  std::vector<int32_t> g1slot, g2slot;  // [Mpad] slot of that run
+  std::vector<int32_t> sA_ptr, sA_slot; // [nl+1], [P]: slots whose key is local control point A
+  std::vector<int64_t> inv_ptr;      // [n_nodes+1] owned node -> its (tile, A) occurrences
+  std::vector<int32_t> inv_ent;      // lt*nl + A, sorted
   bool on_device = false;
   // interpolation operator
   double interp_x[IGA_MAXQ + 1];
@@ -125,6 +133,10 @@ struct Handle {
   int32_t *d_k5_pair = nullptr;
   int32_t *d_k5_col = nullptr;   // [M]
   uint8_t *d_tperm = nullptr;    // [Mpad]
+  uint16_t *d_g1len = nullptr, *d_g2len = nullptr;
+  int32_t *d_g1slot = nullptr, *d_g2slot = nullptr, *d_sA_ptr = nullptr, *d_sA_slot = nullptr, *d_inv_ent = nullptr;
+  int64_t *d_inv_ptr = nullptr;
+  double *d_part = nullptr;      // [n_tiles][P][d] apply partials (allocated by the first iga_apply)
   int32_t *d_patch_info = nullptr; // [n_patches][3]: first K5a chunk, ctrl_off, n_ctrl (+ sentinel chunk)
   double *d_mknots = nullptr;    // macro knots, 3 directions concatenated
   int32_t *d_mspan = nullptr;    // element -> knot span, 3 directions concatenated
@@ -161,6 +173,7 @@ cudaError_t launch_pack_tables(const Handle &h, cudaStream_t s);
 // K3: vals != nullptr -> fused CSR epilogue (+ side slots); local != nullptr -> local[M][N] output
 cudaError_t launch_contraction(const Handle &h, double *vals, double *local, cudaStream_t s);
 cudaError_t launch_scatter_multi(const Handle &h, double *vals, cudaStream_t s);
+cudaError_t launch_apply(const Handle &h, const double *u, double *y, cudaStream_t s);   // K3 apply + gather
 cudaError_t launch_expand_pattern(const Handle &h, cudaStream_t s);
 cudaError_t launch_sens_X(const Handle &h, const double *u, const double *v, cudaStream_t s);
 cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s);

@@ -105,18 +105,28 @@ constexpr int K3_CROW = BN + 1;                                        // epilog
 constexpr int K3_THREADS = 32 * N_MMA_WARPS;
 constexpr size_t K3_OFF_BAR = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
 constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int));
-static_assert(sizeof(double) * BM * K3_CROW <= K3_OFF_BAR, "epilogue staging must fit in the stages");
+static_assert(sizeof(double) * BM * (K3_CROW + 4 * 3) <= K3_OFF_BAR, "epilogue staging must fit in the stages");
 static_assert(BM == IGA_K3_BM, "K3 CTA rows");
 
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
-// EPI = 0: local[M][N] (nzdata, Eq. 58) ; EPI = 1: fused CSR scatter (+ side slots)
+// matrix-free apply (EPI = 2, NEXT N1): u, the partial buffer and the run maps
+struct ApplyArgs {
+  const double *u;
+  double *part;
+  int64_t P;
+  const uint16_t *g1len, *g2len;
+  const int32_t *g1slot, *g2slot, *node_map;
+};
+
+// EPI = 0: local[M][N] (nzdata, Eq. 58) ; EPI = 1: fused CSR scatter (+ side slots);
+// EPI = 2: matrix-free apply y = K^π u (Eq. 74): block products summed into partial slots
 template <int D, int EPI>
 __global__ void __launch_bounds__(K3_THREADS, 2)
 k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int64_t M,
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
-            int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm) {
+            int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm, const ApplyArgs ap) {
   constexpr int DD = D * D, TPC = BN / DD, TPT = TPC / 2;   // tiles per CTA, per epilogue thread
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K3_STAGES * K3_A_CHUNK;
@@ -200,6 +210,78 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     }
     return;
   }
+  if (EPI == 2) {
+    // thread e: c1 = L u_J (diagonal: L_sym u_I) of row e into s1, and c2 = Lᵀ u_I of row
+    // tperm[e] into s2 (position e of the (B, A) order); the first thread of each run of
+    // equal A (s1) / equal B (s2) sums its run in order into the run's partial slot.
+    double *s1 = sC + BM * K3_CROW, *s2 = s1 + 2 * BM * D;
+    const int half = tid >> 7;
+    const int et = tperm[m0 + er];
+    const int64_t rt = m0 + et;
+    const bool live = r < M, live_t = rt < M;
+    const int A = live ? pairA[r] : 0, B = live ? pairB[r] : 0;
+    const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
+    const int len1 = ap.g1len[m0 + er], len2 = ap.g2len[m0 + er];
+    const int64_t sl1 = ap.g1slot[m0 + er], sl2 = ap.g2slot[m0 + er];
+    double *my1 = s1 + (half * BM + er) * D, *my2 = s2 + (half * BM + er) * D;
+    for (int k = 0; k < TPT; ++k) {
+      const int tl = et0 + k;
+      const int64_t t = t0 + tl;
+      const bool tv = t < n_tiles;
+      double c1[D], c2[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) c1[a] = c2[a] = 0.0;
+      if (tv && live) {
+        const double *L = sC + er * K3_CROW + tl * DD;
+        const int64_t I = ap.node_map[t * nl + A], J = ap.node_map[t * nl + B];
+        double uv[D];
+#pragma unroll
+        for (int b = 0; b < D; ++b) uv[b] = ap.u[(A == B ? I : J) * D + b];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) c1[a] += (A == B && a > b ? L[b * D + a] : L[a * D + b]) * uv[b];
+      }
+      if (tv && live_t && At != Bt) {
+        const double *L = sC + et * K3_CROW + tl * DD;
+        const int64_t I = ap.node_map[t * nl + At];
+        double uv[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) uv[a] = ap.u[I * D + a];
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+#pragma unroll
+          for (int a = 0; a < D; ++a) c2[b] += L[a * D + b] * uv[a];
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) { my1[a] = c1[a]; my2[a] = c2[a]; }
+      __syncthreads();
+      if (tv) {
+        if (len1) {
+          double acc[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) acc[a] = 0.0;
+          for (int j = 0; j < len1; ++j)
+#pragma unroll
+            for (int a = 0; a < D; ++a) acc[a] += my1[j * D + a];
+#pragma unroll
+          for (int a = 0; a < D; ++a) ap.part[(t * ap.P + sl1) * D + a] = acc[a];
+        }
+        if (len2) {
+          double acc[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) acc[a] = 0.0;
+          for (int j = 0; j < len2; ++j)
+#pragma unroll
+            for (int a = 0; a < D; ++a) acc[a] += my2[j * D + a];
+#pragma unroll
+          for (int a = 0; a < D; ++a) ap.part[(t * ap.P + sl2) * D + a] = acc[a];
+        }
+      }
+      __syncthreads();
+    }
+    return;
+  }
   // fused scatter (R9).  Pass 1: row er, blocks (I,J) (diagonal blocks mirrored from
   // their upper triangle); pass 2: row tperm[er] of the (B, A)-ordered block, blocks
   // (J,I) = Lᵀ.  Both orders put neighbouring blocks of one CSR row in neighbouring lanes;
@@ -264,14 +346,54 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
 }
 
 template <int D, int EPI>
-static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s) {
+static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, ApplyArgs ap = ApplyArgs{}) {
   cudaError_t e = cudaFuncSetAttribute(k3_contract<D, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM);
   if (e) return e;
   dim3 grid((unsigned)(h.Mpad / BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   k3_contract<D, EPI><<<grid, K3_THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.kstride / BK, (h.nk + 3) / 4, h.M,
                                                         h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,
-                                                        h.n_local_ctrl, h.d_side, h.d_tperm);
+                                                        h.n_local_ctrl, h.d_side, h.d_tperm, ap);
+  return cudaGetLastError();
+}
+
+// y[i] = Σ over the (tile, A) occurrences of owned node i (fixed order) of Σ over A's
+// partial slots (fixed order): deterministic, no atomics
+template <int D>
+__global__ void __launch_bounds__(256)
+k4_apply_gather(const double *__restrict__ part, int64_t P, const int32_t *__restrict__ sA_ptr,
+                const int32_t *__restrict__ sA_slot, const int64_t *__restrict__ inv_ptr,
+                const int32_t *__restrict__ inv_ent, int nl, int64_t n_nodes, double *__restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_nodes) return;
+  double acc[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) acc[a] = 0.0;
+  for (int64_t f = inv_ptr[i]; f < inv_ptr[i + 1]; ++f) {
+    const int32_t e = inv_ent[f];
+    const int64_t t = e / nl;
+    const int A = e % nl;
+    for (int q = sA_ptr[A]; q < sA_ptr[A + 1]; ++q) {
+      const double *src = part + (t * P + sA_slot[q]) * D;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc[a] += src[a];
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) y[i * D + a] = acc[a];
+}
+
+cudaError_t launch_apply(const Handle &h, const double *u, double *y, cudaStream_t s) {
+  ApplyArgs ap{u, h.d_part, h.P, h.d_g1len, h.d_g2len, h.d_g1slot, h.d_g2slot, h.d_node_map};
+  cudaError_t e = h.d == 2 ? launch_k3<2, 2>(h, nullptr, s, ap) : launch_k3<3, 2>(h, nullptr, s, ap);
+  if (e) return e;
+  const unsigned blocks = (unsigned)((h.n_nodes + 255) / 256);
+  if (h.d == 2)
+    k4_apply_gather<2><<<blocks, 256, 0, s>>>(h.d_part, h.P, h.d_sA_ptr, h.d_sA_slot, h.d_inv_ptr, h.d_inv_ent,
+                                              h.n_local_ctrl, h.n_nodes, y);
+  else
+    k4_apply_gather<3><<<blocks, 256, 0, s>>>(h.d_part, h.P, h.d_sA_ptr, h.d_sA_slot, h.d_inv_ptr, h.d_inv_ent,
+                                              h.n_local_ctrl, h.n_nodes, y);
   return cudaGetLastError();
 }
 

@@ -245,3 +245,40 @@ def test_fullsize_sensitivity(c):
     ref = S.sensitivity(prob, g["tabs"], _LibPattern(g), u, v, entries=ent)
     for k, a in ent:
         assert abs(got[k, a] - ref[k, a]) < TOL_SENS * scale * 10, (k, a, got[k, a], ref[k, a])
+
+
+@pytest.mark.parametrize("c", [4, 5])
+def test_fullsize_matrix_free_apply(c):
+    """iga_apply at full size equals the GPU CSR product (≤ 1e-12 rel.), and its
+    sampled entries equal the oracle's rows (from test_fullsize_csr_rows' assembly)
+    times u."""
+    from synth import draw_uv_seeded
+    g = case(c)
+    prob, A, s = g["prob"], g["A"], g["s"]
+    d = prob.d
+    u, _ = draw_uv_seeded(c, s.n_dof)
+    ut = torch.tensor(u, device="cuda")
+    y = torch.empty(s.n_dof, dtype=torch.float64, device="cuda")
+    A.apply(g["ctrl"], g["young"], prob.nu, ut, y)
+    yc = spmv(g, ut)
+    assert (torch.linalg.norm(y - yc) / torch.linalg.norm(yc)).item() < 1e-12
+    yh = y.cpu().numpy()
+    for I in sample_nodes(g, 6, 500 + c):
+        blocks = oracle_row_blocks(g, I)
+        ref = sum(blocks[J] @ u[J * d:(J + 1) * d] for J in blocks)
+        assert rel(yh[I * d:(I + 1) * d], ref) < 1e-11 * 10, I
+
+
+def spmv(g, v, max_nnz=1 << 30):
+    rp = g["rp_h"]
+    n = len(rp) - 1
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    r0 = 0
+    while r0 < n:
+        r1 = max(int(np.searchsorted(rp, rp[r0] + max_nnz, side="right")) - 1, r0 + 1)
+        a, b = int(rp[r0]), int(rp[r1])
+        sub = torch.sparse_csr_tensor(g["rp"][r0:r1 + 1] - a, g["ci"][a:b].to(torch.int64), g["vals"][a:b],
+                                      size=(r1 - r0, n))
+        out[r0:r1] = torch.mv(sub, v)
+        r0 = r1
+    return out
