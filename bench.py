@@ -244,11 +244,12 @@ def run_ours(args, rank, world):
     stream = torch.cuda.current_stream()
 
     def step():
-        A.assemble(ctrl, young, prob.nu, vals, stream=stream)
-        if sens:
-            A.sensitivity(ctrl, young, prob.nu, u, v, grad, stream=stream)
+        if sens:   # K and g in one call (iga_assemble_sensitivity)
+            A.assemble_sensitivity(ctrl, young, prob.nu, u, v, vals, grad, stream=stream)
             if shard:
                 allreduce_grad(grad, world)   # the sharded step's one collective (NCCL)
+        else:
+            A.assemble(ctrl, young, prob.nu, vals, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -285,10 +286,15 @@ def run_ours(args, rank, world):
         h_grad_np = h_grad.numpy()
 
         def step_e2e():
-            A.assemble(h_ctrl.numpy(), h_young.numpy(), prob.nu, vals, stream=stream)
             if sens:
-                A.sensitivity(h_ctrl.numpy(), h_young.numpy(), prob.nu, h_u.numpy(), h_v.numpy(), h_grad_np,
-                              stream=stream)
+                A.assemble_sensitivity(h_ctrl.numpy(), h_young.numpy(), prob.nu, h_u.numpy(), h_v.numpy(), vals,
+                                       h_grad_np, stream=stream)
+                if shard:
+                    gd = torch.from_numpy(h_grad_np).to(dev)
+                    allreduce_grad(gd, world)
+                    h_grad.copy_(gd)
+            else:
+                A.assemble(h_ctrl.numpy(), h_young.numpy(), prob.nu, vals, stream=stream)
         step_e2e()
         torch.cuda.synchronize()
         barrier(world)

@@ -174,6 +174,14 @@ iga_status iga_sensitivity(const iga_handle *h, const double *macro_ctrl, const 
                            int32_t young_per_tile, double nu, const double *u, const double *v,
                            double *grad, void *stream);
 
+/* iga_assemble_sensitivity — iga_assemble followed by iga_sensitivity in one call (the
+ * design-optimisation step: K and g together), one synchronisation at the end.  Host
+ * u, v are copied on an internal stream while K is formed.  Arguments as in the two calls
+ * (no local_values). */
+iga_status iga_assemble_sensitivity(const iga_handle *h, const double *macro_ctrl, const double *young,
+                                    int32_t young_per_tile, double nu, const double *u, const double *v,
+                                    double *csr_values, double *grad, void *stream);
+
 /* ---------------------------------------------------------------------------
  * iga_apply — matrix-free y = K^π u (Eq. 74: "the multiplication of a vector
  * with the system matrix with only the lookup table and the projection coefficients at

@@ -50,7 +50,8 @@ class iga_shard(C.Structure):
 
 
 N_PROF = 10   # IGA_N_PROF: 0 K2, 1 K3(+scatter), 2 K4, 3 K5a, 4 K5b, 5 K5c, 6 staging, 7 K5x, 8 K3 nzdata, 9 apply
-EXPORTS = ["iga_build_tables", "iga_build_topology", "iga_assemble", "iga_sensitivity", "iga_apply", "iga_interpolate",
+EXPORTS = ["iga_build_tables", "iga_build_topology", "iga_assemble", "iga_sensitivity", "iga_assemble_sensitivity",
+           "iga_apply", "iga_interpolate",
            "iga_get_sizes",
            "iga_get_pattern", "iga_get_block_map", "iga_get_node_map", "iga_get_tables", "iga_get_pairs",
            "iga_set_profiling", "iga_get_kernel_times", "iga_free", "iga_last_error", "iga_version"]
@@ -74,6 +75,7 @@ def load():
     lib.iga_sensitivity.argtypes = [vp, vp, vp, i32, d, vp, vp, vp, vp]
     lib.iga_interpolate.argtypes = [vp, vp, vp, i32, d, vp, vp]
     lib.iga_apply.argtypes = [vp, vp, vp, i32, d, vp, vp, vp]
+    lib.iga_assemble_sensitivity.argtypes = [vp, vp, vp, i32, d, vp, vp, vp, vp, vp]
     lib.iga_get_sizes.argtypes = [vp, C.POINTER(iga_sizes)]
     lib.iga_get_pattern.argtypes = [vp, vp, vp]
     lib.iga_get_block_map.argtypes = [vp, i64, i64, vp]
@@ -176,6 +178,11 @@ class Assembler:
     def sensitivity(self, ctrl, young, nu, u, v, grad, stream=None):
         _check(load().iga_sensitivity(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
                                       _ptr(u), _ptr(v), _ptr(grad), _stream_ptr(stream)))
+
+    def assemble_sensitivity(self, ctrl, young, nu, u, v, values, grad, stream=None):
+        """K (CSR values) and g = uᵀ(∂K/∂P)v in one call (iga_assemble_sensitivity)."""
+        _check(load().iga_assemble_sensitivity(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
+                                               _ptr(u), _ptr(v), _ptr(values), _ptr(grad), _stream_ptr(stream)))
 
     def apply(self, ctrl, young, nu, u, y, stream=None):
         """Matrix-free y = K^π u (iga_apply)."""

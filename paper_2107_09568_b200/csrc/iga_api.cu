@@ -18,6 +18,9 @@ Handle::~Handle() {
     if (b) cudaFree(b);
   for (int i = 0; i < N_STAGE; ++i)
     if (d_stage[i]) cudaFree(d_stage[i]);
+  if (aux_stream) cudaStreamDestroy(aux_stream);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   for (auto e : ev_pool) cudaEventDestroy(e);
 }
 
@@ -51,7 +54,7 @@ struct Stager {
   int slot = 0;
   std::vector<std::pair<double *, const double *>> pending_out;   // (device, host)
   std::vector<size_t> pending_bytes;
-  Stager(Handle &hh, cudaStream_t ss) : h(hh), s(ss) {}
+  Stager(Handle &hh, cudaStream_t ss, int first_slot = 0) : h(hh), s(ss), slot(first_slot) {}
   double *buffer(size_t n) {
     if (slot >= Handle::N_STAGE) return nullptr;
     const int i = slot++;
@@ -468,6 +471,68 @@ iga_status iga_sensitivity(const iga_handle *Hc, const double *macro_ctrl, const
   }
   pf.end(idst);
   int id = pf.begin(7);
+  CU(launch_sens_X(h, du, dv, s));
+  pf.end(id);
+  id = pf.begin(3);
+  CU(launch_sens_W(h, h.d_W, s));
+  pf.end(id);
+  id = pf.begin(4);
+  CU(launch_sens_reverse(h, dctrl, dyoung, young_per_tile, nu, h.d_W, h.d_gpart, s));
+  pf.end(id);
+  id = pf.begin(5);
+  CU(launch_sens_reduce(h, h.d_gpart, dgrad, s));
+  pf.end(id);
+  idst = pf.begin(6);
+  if (!sg.flush()) { set_error("D2H copy failed"); return IGA_ECUDA; }
+  pf.end(idst);
+  st = check_flag(h, s);
+  pf.collect();
+  return st;
+}
+
+iga_status iga_assemble_sensitivity(const iga_handle *Hc, const double *macro_ctrl, const double *young,
+                                    int32_t young_per_tile, double nu, const double *u, const double *v,
+                                    double *csr_values, double *grad, void *stream) {
+  if (!Hc || !macro_ctrl || !u || !v || !grad || !csr_values) { set_error("NULL argument"); return IGA_EINVAL; }
+  Handle &h = const_cast<iga_handle *>(Hc)->h;
+  if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
+  iga_status st = check_material(h, young, nu);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h.aux_stream) {
+    CU(cudaStreamCreateWithFlags(&h.aux_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+  }
+  // u, v travel on the auxiliary stream while K2 -> K3 -> K4 form K on the caller's stream
+  CU(cudaEventRecord(h.ev_fork, s));
+  CU(cudaStreamWaitEvent(h.aux_stream, h.ev_fork, 0));
+  Stager sg(h, s), sg2(h, h.aux_stream, 4);
+  Prof pf(h, s);
+  int idst = pf.begin(6);
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  const double *dctrl, *dyoung, *du, *dv;
+  double *dvals, *dgrad;
+  if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) ||
+      !sg.in(young, young_per_tile ? (size_t)h.n_tiles_glob : 1, &dyoung) ||
+      !sg.out(csr_values, (size_t)h.nnz, &dvals) || !sg.out(grad, (size_t)(h.n_cp * h.d), &dgrad) ||
+      !sg2.in(u, (size_t)h.n_dof, &du) || !sg2.in(v, (size_t)h.n_dof, &dv)) {
+    set_error("staging failed");
+    return IGA_ENOMEM;
+  }
+  CU(cudaEventRecord(h.ev_join, h.aux_stream));
+  pf.end(idst);
+  int id = pf.begin(0);
+  CU(launch_interpolate(h, dctrl, dyoung, young_per_tile, nu, h.d_coef, true, s));
+  pf.end(id);
+  id = pf.begin(1);
+  CU(launch_contraction(h, dvals, nullptr, s));
+  pf.end(id);
+  id = pf.begin(2);
+  CU(launch_scatter_multi(h, dvals, s));
+  pf.end(id);
+  CU(cudaStreamWaitEvent(s, h.ev_join, 0));
+  id = pf.begin(7);
   CU(launch_sens_X(h, du, dv, s));
   pf.end(id);
   id = pf.begin(3);

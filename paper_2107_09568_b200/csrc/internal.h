@@ -143,6 +143,8 @@ struct Handle {
   int *d_flag = nullptr;         // [0] error flag, [1] tile, [2] node
   // staging (host pointers in [any] arguments)
   static constexpr int N_STAGE = 6;
+  cudaStream_t aux_stream = nullptr;   // iga_assemble_sensitivity: u, v copies beside K formation
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double *d_stage[N_STAGE] = {nullptr};   // grow-only device copies of host [any] arguments
   size_t stage_cap[N_STAGE] = {0};
   // profiling

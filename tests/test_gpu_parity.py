@@ -352,3 +352,25 @@ def test_matrix_free_apply_sharded():
         yk = torch.empty(z.n_rows, dtype=torch.float64, device="cuda")
         B.apply(g["ctrl"], g["young"], prob.nu, ut, yk)
         assert torch.equal(yk, y[z.row_begin:z.row_begin + z.n_rows]), k
+
+
+def test_assemble_sensitivity_combined_call():
+    """iga_assemble_sensitivity gives the same bits as iga_assemble + iga_sensitivity, with
+    device and with (pinned) host u, v."""
+    from synth import draw_uv_seeded
+    g = gpu_case(2)
+    prob, A = g["prob"], g["A"]
+    s = A.sizes
+    u, v = draw_uv_seeded(2, s.n_dof)
+    ut, vt = torch.tensor(u, device="cuda"), torch.tensor(v, device="cuda")
+    g1 = torch.empty(s.n_macro_cp * prob.d, dtype=torch.float64, device="cuda")
+    A.sensitivity(g["ctrl"], g["young"], prob.nu, ut, vt, g1)
+    vals = torch.empty_like(g["vals"])
+    g2 = torch.empty_like(g1)
+    A.assemble_sensitivity(g["ctrl"], g["young"], prob.nu, ut, vt, vals, g2)
+    assert torch.equal(vals, g["vals"]) and torch.equal(g2, g1)
+    hu, hv = torch.tensor(u).pin_memory(), torch.tensor(v).pin_memory()
+    gh = np.empty(s.n_macro_cp * prob.d)
+    A.assemble_sensitivity(g["ctrl"], g["young"], prob.nu, hu.numpy(), hv.numpy(), vals, gh)
+    torch.cuda.synchronize()
+    assert np.array_equal(gh, g1.cpu().numpy()) and torch.equal(vals, g["vals"])
