@@ -201,6 +201,18 @@ iga_status iga_apply(const iga_handle *h, const double *macro_ctrl, const double
 iga_status iga_interpolate(const iga_handle *h, const double *macro_ctrl, const double *young,
                            int32_t young_per_tile, double nu, double *coef, void *stream);
 
+/* iga_set_projection — the projection Π^H of the macro field (Eq. 20) onto Q_q: the L2
+ * projection of Eqs. 23-24 (and 42) with its mass matrix and right-hand side integrated
+ * by an m-point Gauss rule per direction, m >= q+1.  m = q+1 (the
+ * default) is interpolation at the (q+1)^d Gauss nodes (reading R1, equal to that
+ * projection); larger m converge to the exact L2 projection (exact once 2m-1 >= q + the
+ * degree of Ā's polynomial part).  Applies to iga_assemble / iga_sensitivity /
+ * iga_interpolate / iga_apply; the tables do not depend on m.
+ * Errors: EINVAL (m < q+1 or m > 8), ELIMIT (per-tile staging exceeds shared memory,
+ * e.g. m > 5 in 3D). */
+iga_status iga_set_projection(iga_handle *h, int32_t m);
+iga_status iga_get_projection(const iga_handle *h, int32_t *m);
+
 /* Accessors.  iga_get_sizes: [host] out. */
 iga_status iga_get_sizes(const iga_handle *h, iga_sizes *out);
 

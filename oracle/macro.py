@@ -207,18 +207,47 @@ def interpolate(samples, q, d):
     return c.reshape(s.shape)
 
 
-def tile_coefficients(prob, ctrl, t, E=None, route=A_closed):
-    """⟨Ā_ij⟩_C for tile t (Eq. 42 in interpolation form): shape (n_pi, d, d, d, d)
-    indexed [C, i, j, a, b].  Raises if det J <= 0 at a node (reading R5)."""
+def projection_nodes(m, d):
+    """m^d tensor Gauss–Legendre nodes on [0,1]^d (direction-0 fastest) and weights."""
+    x, w1 = gauss_01(m)
+    pts = np.zeros((m ** d, d))
+    w = np.ones(m ** d)
+    for i in range(m ** d):
+        for k in range(d):
+            pts[i, k] = x[(i // m ** k) % m]
+            w[i] *= w1[(i // m ** k) % m]
+    return pts, w
+
+
+def project_l2(samples, q, d, m):
+    """L2 projection onto Q_q (Eqs. 23-24): M_π d = r_π with [M_π]_kl = ∫ N_k N_l and
+    (r_π)_k = ∫ N_k f, both integrated by the m-point Gauss rule per direction; samples
+    = f at projection_nodes(m, d).  Plain definition (full tensor mass matrix)."""
+    X, w = projection_nodes(m, d)
+    N = bernstein(q, X)                          # (C, m^d)
+    Mpi = (N * w) @ N.T
+    s = np.asarray(samples)
+    flat = s.reshape(s.shape[0], -1)
+    r = (N * w).astype(np.result_type(flat, np.float64)) @ flat
+    c = np.linalg.solve(Mpi.astype(r.dtype), r)
+    return c.reshape((N.shape[0],) + s.shape[1:])
+
+
+def tile_coefficients(prob, ctrl, t, E=None, route=A_closed, m=None):
+    """⟨Ā_ij⟩_C for tile t (Eq. 42): shape (n_pi, d, d, d, d) indexed [C, i, j, a, b].
+    m (default prob.n_proj, 0 -> q+1): Gauss points per direction of the projection; q+1
+    is interpolation at the Gauss nodes (reading R1), larger m the L2 projection of
+    Eqs. 23-24 with that rule (NEXT N2).  Raises if det J <= 0 at a node (reading R5)."""
     d, q = prob.d, prob.q
+    m = m or getattr(prob, "n_proj", 0) or q + 1
     E = prob.young[t] if E is None else E
     lam, mu = lame(E, prob.nu)
-    X = interp_nodes(q, d)
+    X = interp_nodes(q, d) if m == q + 1 else projection_nodes(m, d)[0]
     J = macro_jacobian(prob.macro, ctrl, t, X)
     if np.any(np.real(np.linalg.det(J)) <= 0):
         raise ValueError(f"degenerate macro element: tile {t}")
     A = route(J, lam, mu)                       # (m, i, j, a, b)
-    return interpolate(A, q, d)
+    return interpolate(A, q, d) if m == q + 1 else project_l2(A, q, d, m)
 
 
 def field_from_coefficients(coef, q, xi):

@@ -54,7 +54,8 @@ EXPORTS = ["iga_build_tables", "iga_build_topology", "iga_assemble", "iga_sensit
            "iga_apply", "iga_interpolate",
            "iga_get_sizes",
            "iga_get_pattern", "iga_get_block_map", "iga_get_node_map", "iga_get_tables", "iga_get_pairs",
-           "iga_set_profiling", "iga_get_kernel_times", "iga_free", "iga_last_error", "iga_version"]
+           "iga_set_projection", "iga_get_projection", "iga_set_profiling", "iga_get_kernel_times", "iga_free",
+           "iga_last_error", "iga_version"]
 
 _lib = None
 
@@ -83,6 +84,8 @@ def load():
     lib.iga_get_tables.argtypes = [vp, vp]
     lib.iga_get_pairs.argtypes = [vp, vp]
     lib.iga_set_profiling.argtypes = [vp, i32]
+    lib.iga_set_projection.argtypes = [vp, i32]
+    lib.iga_get_projection.argtypes = [vp, C.POINTER(i32)]
     lib.iga_get_kernel_times.argtypes = [vp, vp, vp]
     lib.iga_free.argtypes = [vp]
     lib.iga_free.restype = None
@@ -217,6 +220,15 @@ class Assembler:
         out = np.empty((self.sizes.n_local_rows, 2), dtype=np.int32)
         _check(load().iga_get_pairs(self._h, out.ctypes.data))
         return out
+
+    def set_projection(self, m):
+        """L2 projection with an m-point Gauss rule per direction (m = q+1: interpolation)."""
+        _check(load().iga_set_projection(self._h, int(m)))
+
+    def projection(self):
+        m = C.c_int32()
+        _check(load().iga_get_projection(self._h, C.byref(m)))
+        return m.value
 
     def set_profiling(self, enable=True):
         _check(load().iga_set_profiling(self._h, int(enable)))

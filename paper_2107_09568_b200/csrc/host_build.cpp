@@ -631,13 +631,51 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   h.k5_rows = (h.kstride + IGA_K3_BM - 1) / IGA_K3_BM * IGA_K3_BM;
   if (k5x_smem_bytes(d, h.max_patch_ctrl) > 227 * 1024) { set_error("tile patch too large for the K5 shared-memory staging (%d control points)", h.max_patch_ctrl); return IGA_ELIMIT; }
 
-  // ---- interpolation operator Π1 = V1^{-1} (R1) --------------------------------
-  double w[IGA_MAXQ + 1], V[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
-  gauss_legendre01(q + 1, h.interp_x, w);
-  for (int m = 0; m <= q; ++m)
-    for (int k = 0; k <= q; ++k)
-      V[m * (q + 1) + k] = binom(q, k) * std::pow(h.interp_x[m], k) * std::pow(1.0 - h.interp_x[m], q - k);
-  if (!invert(q + 1, V, h.Pi1)) { set_error("singular interpolation matrix"); return IGA_EINVAL; }
+  // ---- projection operator (R1: interpolation at the q+1 Gauss nodes) -------------
+  {
+    const iga_status st = set_projection(h, q + 1);
+    if (st != IGA_OK) return st;
+  }
+  return IGA_OK;
+}
+
+// Π1 for an m-point Gauss rule per direction (Eqs. 23-24: M_π d = r_π with
+// [M_π]_kl = Σ_i w_i N_k(x_i) N_l(x_i), (r_π)_k = Σ_i w_i N_k(x_i) f(x_i), tensorised):
+// Pi1 = (VᵀWV)⁻¹VᵀW, V[i][c] = B_c^q(x_i).  m = q+1 reduces to V⁻¹ (interpolation at the
+// Gauss nodes, reading R1), computed directly.
+iga_status set_projection(Handle &h, int m) {
+  const int q = h.q, q1 = q + 1;
+  if (m < q1 || m > IGA_MAXM) { set_error("projection points m=%d outside [q+1=%d, %d]", m, q1, IGA_MAXM); return IGA_EINVAL; }
+  if (macro_smem_bytes(h.d, q, m, true) > 227 * 1024 || macro_smem_bytes(h.d, q, m, false) > 227 * 1024) {
+    set_error("projection points m=%d: per-tile staging exceeds shared memory", m);
+    return IGA_ELIMIT;
+  }
+  double x[IGA_MAXM], w[IGA_MAXM], V[IGA_MAXM * (IGA_MAXQ + 1)];
+  gauss_legendre01(m, x, w);
+  for (int i = 0; i < m; ++i)
+    for (int c = 0; c <= q; ++c) V[i * q1 + c] = binom(q, c) * std::pow(x[i], c) * std::pow(1.0 - x[i], q - c);
+  double P[(IGA_MAXQ + 1) * IGA_MAXM];
+  if (m == q1) {
+    if (!invert(q1, V, P)) { set_error("singular interpolation matrix"); return IGA_EINVAL; }
+  } else {
+    double Mpi[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)], Minv[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
+    for (int k = 0; k < q1; ++k)
+      for (int l = 0; l < q1; ++l) {
+        double v = 0.0;
+        for (int i = 0; i < m; ++i) v += w[i] * V[i * q1 + k] * V[i * q1 + l];
+        Mpi[k * q1 + l] = v;
+      }
+    if (!invert(q1, Mpi, Minv)) { set_error("singular projection mass matrix"); return IGA_EINVAL; }
+    for (int c = 0; c < q1; ++c)
+      for (int i = 0; i < m; ++i) {
+        double v = 0.0;
+        for (int k = 0; k < q1; ++k) v += Minv[c * q1 + k] * V[i * q1 + k];
+        P[c * m + i] = v * w[i];
+      }
+  }
+  h.m_proj = m;
+  for (int i = 0; i < m; ++i) h.interp_x[i] = x[i];
+  for (int i = 0; i < q1 * m; ++i) h.Pi1[i] = P[i];
   return IGA_OK;
 }
 

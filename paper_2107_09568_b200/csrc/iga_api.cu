@@ -628,6 +628,17 @@ iga_status iga_get_pairs(const iga_handle *Hc, int32_t *out) {
   return IGA_OK;
 }
 
+iga_status iga_set_projection(iga_handle *H, int32_t m) {
+  if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
+  return set_projection(H->h, m);
+}
+
+iga_status iga_get_projection(const iga_handle *H, int32_t *m) {
+  if (!H || !m) { set_error("NULL argument"); return IGA_EINVAL; }
+  *m = H->h.m_proj;
+  return IGA_OK;
+}
+
 iga_status iga_set_profiling(iga_handle *H, int32_t enable) {
   if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
   H->h.profiling = enable != 0;

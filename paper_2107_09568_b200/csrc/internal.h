@@ -10,6 +10,7 @@
 #define IGA_MAXD 3
 #define IGA_MAXP 4          // max spline degree (tile and macro)
 #define IGA_MAXQ 4          // max interpolation degree
+#define IGA_MAXM 8          // max L2-projection points per direction (NEXT N2)
 #define IGA_KCHUNK 16       // GEMM k-chunk; k_stride is a multiple of it
 #define IGA_K3_BM 128       // K3 CTA rows (table rows)
 #define IGA_GEMM_BN 72      // K3/K5a CTA columns (tiles × d²): 8 tiles in 3D, 18 in 2D
@@ -106,9 +107,11 @@ struct Handle {
   std::vector<int64_t> inv_ptr;      // [n_nodes+1] owned node -> its (tile, A) occurrences
   std::vector<int32_t> inv_ent;      // lt*nl + A, sorted
   bool on_device = false;
-  // interpolation operator
-  double interp_x[IGA_MAXQ + 1];
-  double Pi1[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];   // V1^{-1}
+  // projection operator (Eqs. 23-24 with an m-point Gauss rule per direction; m = q+1:
+  // interpolation at the Gauss nodes, reading R1): coef_c = Σ_i Pi1[c*m + i] f(x_i)
+  int m_proj = 0;
+  double interp_x[IGA_MAXM];
+  double Pi1[(IGA_MAXQ + 1) * IGA_MAXM];
   // device buffers
   double *d_table = nullptr;     // [M][kstride] row-major (K1 output, accessor)
   double *d_tabA = nullptr;      // FM [Mpad][kstride], BR = IGA_K3_BM (K3 A operand)
@@ -160,8 +163,9 @@ struct InterpConst {
   int d, q, pm[3], mn[3], mel[3], moff[3], soff[3];   // offsets of direction k in d_mknots / d_mspan
   int64_t t_base;        // global id of local tile 0
   int64_t n_own;         // owned local tiles (sensitivity reduction)
-  double Pi1[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
-  double x[IGA_MAXQ + 1];
+  int m;                 // projection points per direction (q+1: interpolation)
+  double Pi1[(IGA_MAXQ + 1) * IGA_MAXM];   // [(q+1) x m]
+  double x[IGA_MAXM];
 };
 
 // --- kernel launchers (kernels_*.cu) ---
@@ -189,6 +193,8 @@ InterpConst make_interp_const(const Handle &h);
 iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const iga_interface *ifc,
                       int n_ifc, const iga_spline *macro, int q, int n_gauss, const iga_shard *shard);
 void gauss_legendre01(int n, double *x, double *w);
+iga_status set_projection(Handle &h, int m);   // host: Pi1, x for m points per direction
+size_t macro_smem_bytes(int d, int q, int m, bool reverse);
 iga_status upload_topology(Handle &h);
 
 }  // namespace iga

@@ -423,7 +423,7 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
         int nl, const double *__restrict__ u, const double *__restrict__ v, int64_t n_tiles, int nkc,
         double *__restrict__ X) {
   constexpr int DD = D * D, TPC = BN / DD;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const int64_t nb = blockIdx.y, t0 = nb * TPC;
   const int kc0 = pinfo[3 * p], kc1 = pinfo[3 * (p + 1)], off = pinfo[3 * p + 1], nc = pinfo[3 * p + 2];

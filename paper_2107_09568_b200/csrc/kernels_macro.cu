@@ -32,16 +32,17 @@ InterpConst make_interp_const(const Handle &h) {
   }
   ic.t_base = h.t_base;
   ic.n_own = h.n_tiles_own;
-  for (int i = 0; i < (IGA_MAXQ + 1) * (IGA_MAXQ + 1); ++i) ic.Pi1[i] = h.Pi1[i];
-  for (int i = 0; i <= IGA_MAXQ; ++i) ic.x[i] = h.interp_x[i];
+  ic.m = h.m_proj;
+  for (int i = 0; i < (IGA_MAXQ + 1) * IGA_MAXM; ++i) ic.Pi1[i] = h.Pi1[i];
+  for (int i = 0; i < IGA_MAXM; ++i) ic.x[i] = h.interp_x[i];
   return ic;
 }
 
 // Shared per-tile macro data: 1D basis at the nodes and the active control points.
 template <int D>
 struct MacroTile {
-  double B1[D][IGA_MAXQ + 1][IGA_MAXP + 1];
-  double D1[D][IGA_MAXQ + 1][IGA_MAXP + 1];   // derivative w.r.t. ξ_k (includes span length)
+  double B1[D][IGA_MAXM][IGA_MAXP + 1];
+  double D1[D][IGA_MAXM][IGA_MAXP + 1];   // derivative w.r.t. ξ_k (includes span length)
   double P[(D == 2 ? (IGA_MAXP + 1) * (IGA_MAXP + 1) : (IGA_MAXP + 1) * (IGA_MAXP + 1) * (IGA_MAXP + 1)) * D];
   int nact;
 };
@@ -50,12 +51,12 @@ template <int D>
 __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64_t t, const double *__restrict__ ctrl,
                                 const double *__restrict__ mknots, const int *__restrict__ mspan,
                                 int tid = threadIdx.x, int nthr = blockDim.x) {
-  const int q = c_ip.q;
+  const int m1 = c_ip.m;   // sample points per direction
   int e[3] = {0, 0, 0};
   int64_t tmp = t;
   for (int k = 0; k < D; ++k) { e[k] = (int)(tmp % c_ip.mel[k]); tmp /= c_ip.mel[k]; }
-  if (tid < D * (q + 1)) {
-    int k = tid / (q + 1), m = tid % (q + 1);
+  if (tid < D * m1) {
+    int k = tid / m1, m = tid % m1;
     const double *U = mknots + c_ip.moff[k];
     int s = mspan[c_ip.soff[k] + e[k]];
     double h = U[s + 1] - U[s];
@@ -81,10 +82,10 @@ __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64
   }
 }
 
-// J[a][β] = ∂F_a/∂ξ_β at tensor node m (direction-0-fastest node index)
+// J[a][β] = ∂F_a/∂ξ_β at tensor sample node m (m^d nodes, direction-0 fastest)
 template <int D>
 __device__ void macro_J(const InterpConst &c_ip, const MacroTile<D> &mt, int m, double J[D][D]) {
-  const int q1 = c_ip.q + 1;
+  const int q1 = c_ip.m;
   int mm[3] = {m % q1, (m / q1) % q1, m / (q1 * q1)};
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   for (int a = 0; a < D; ++a)
@@ -109,8 +110,34 @@ __device__ __forceinline__ void lame(double E, double nu, double &lam, double &m
   mu = E / (2.0 * (1.0 + nu));
 }
 
-// apply the 1D operator Π1 = V1⁻¹ (or its transpose) along direction DIR of an
-// (Q+1)^D × NCOMP array in shared memory; every index is a compile-time constant.
+// one 1D pass of the projection along direction `dir` of an n[0]×n[1]×n[2] array of
+// NCOMP-vectors in shared memory: forward (samples -> coefficients) out[..c..] =
+// Σ_i Π1[c][i] in[..i..] (n[dir]: m -> q+1); transposed out[..i..] = Σ_c Π1[c][i] in[..c..]
+// (n[dir]: q+1 -> m).  Updates n[] to the output shape.
+template <int NCOMP>
+__device__ void proj_pass(const InterpConst &c_ip, const double *in, double *out, int n[3], int dir, bool transpose) {
+  const int q1 = c_ip.q + 1, m1 = c_ip.m;
+  const int nin = n[dir], nout = transpose ? m1 : q1;
+  int o[3] = {n[0], n[1], n[2]};
+  o[dir] = nout;
+  const int stride_in = dir == 0 ? 1 : (dir == 1 ? n[0] : n[0] * n[1]);
+  const int stride_out = dir == 0 ? 1 : (dir == 1 ? o[0] : o[0] * o[1]);
+  const int total = o[0] * o[1] * o[2];
+  for (int idx = threadIdx.x; idx < total * NCOMP; idx += blockDim.x) {
+    const int C = idx / NCOMP, comp = idx - C * NCOMP;
+    const int c = (C / stride_out) % nout;
+    const int rest = C - c * stride_out;                         // other indices, output strides
+    const int hi = rest / (stride_out * nout), lo = rest % stride_out;
+    const double *src = in + ((hi * nin) * stride_in + lo) * NCOMP + comp;
+    double acc = 0.0;
+    for (int k = 0; k < nin; ++k)
+      acc = fma(transpose ? c_ip.Pi1[k * m1 + c] : c_ip.Pi1[c * m1 + k], src[k * stride_in * NCOMP], acc);
+    out[idx] = acc;
+  }
+  n[dir] = nout;
+}
+
+// the m = q+1 case with every index a compile-time constant
 template <int D, int Q, int DIR, bool TRANSPOSE, int NCOMP>
 __device__ __forceinline__ void tensor_pass(const InterpConst &c_ip, const double *in, double *out) {
   constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
@@ -121,14 +148,14 @@ __device__ __forceinline__ void tensor_pass(const InterpConst &c_ip, const doubl
     const double *src = in + (C - c * STRIDE) * NCOMP + comp;
     double acc = 0.0;
 #pragma unroll
-    for (int m = 0; m < Q1; ++m)
-      acc = fma(TRANSPOSE ? c_ip.Pi1[m * Q1 + c] : c_ip.Pi1[c * Q1 + m], src[m * STRIDE * NCOMP], acc);
+    for (int k = 0; k < Q1; ++k)
+      acc = fma(TRANSPOSE ? c_ip.Pi1[k * Q1 + c] : c_ip.Pi1[c * Q1 + k], src[k * STRIDE * NCOMP], acc);
     out[idx] = acc;
   }
 }
 
 template <int D, int Q, bool TRANSPOSE, int NCOMP>
-__device__ __forceinline__ const double *tensor_apply(const InterpConst &c_ip, double *a, double *b) {
+__device__ const double *tensor_apply(const InterpConst &c_ip, double *a, double *b) {
   tensor_pass<D, Q, 0, TRANSPOSE, NCOMP>(c_ip, a, b);
   __syncthreads();
   tensor_pass<D, Q, 1, TRANSPOSE, NCOMP>(c_ip, b, a);
@@ -139,17 +166,31 @@ __device__ __forceinline__ const double *tensor_apply(const InterpConst &c_ip, d
   return b;
 }
 
+// all d passes; a, b: the two buffers; returns the one holding the result
+template <int D, int NCOMP>
+__device__ const double *proj_apply(const InterpConst &c_ip, double *a, double *b, bool transpose) {
+  const int n0 = transpose ? c_ip.q + 1 : c_ip.m;
+  int n[3] = {n0, n0, D == 3 ? n0 : 1};
+  double *in = a, *out = b;
+  for (int dir = 0; dir < D; ++dir) {
+    proj_pass<NCOMP>(c_ip, in, out, n, dir, transpose);
+    __syncthreads();
+    double *t = in; in = out; out = t;
+  }
+  return in;
+}
+
 // per-node geometry: G = J⁻¹ (rows ǧ_i), det J, gg = G Gᵀ
 template <int D>
 struct NodeGeo {
   double G[D][D], gg[D][D], det;
 };
 
-template <int D, int Q>
+template <int D>
 __device__ __forceinline__ void node_geometry(const InterpConst &c_ip, const MacroTile<D> &mt, NodeGeo<D> *geo,
                                               int64_t t, int *flag) {
-  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
-  for (int m = threadIdx.x; m < NPI; m += blockDim.x) {
+  const int ns = D == 2 ? c_ip.m * c_ip.m : c_ip.m * c_ip.m * c_ip.m;
+  for (int m = threadIdx.x; m < ns; m += blockDim.x) {
     double J[D][D], G[D][D];
     macro_J<D>(c_ip, mt, m, J);
     const double det = det_inv<D>(J, G);
@@ -174,7 +215,7 @@ __device__ __forceinline__ void node_geometry(const InterpConst &c_ip, const Mac
 template <int D, int Q>
 struct K2Shape {
   static constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, DD = D * D, NC = DD * DD;
-  static constexpr int TPB = D == 2 ? 16 : 4;   // tiles per CTA: 256 / 324 threads
+  static constexpr int TPB = D == 2 ? (Q <= 2 ? 16 : 8) : 4;   // tiles per CTA: 256 (128) / 324 threads
   static constexpr int THREADS = TPB * NC;
   static constexpr bool REG = NPI <= 27;        // register path; larger q: shared-memory passes
 };
@@ -260,7 +301,17 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   }
 }
 
-// K2 for (q+1)^d > 27 (3D, q >= 3): one CTA per tile, component arrays in shared memory.
+// shared memory of the one-CTA-per-tile macro kernels (K2 projection path, K5b):
+// two ns×d⁴ buffers (+ ∂S/∂J ns×d² for K5b) and the ns node geometries, ns = m^d
+size_t macro_smem_bytes(int d, int q, int m, bool reverse) {
+  (void)q;
+  const size_t ns = d == 2 ? (size_t)m * m : (size_t)m * m * m, nc = (size_t)d * d * d * d;
+  const size_t geo = d == 2 ? sizeof(NodeGeo<2>) : sizeof(NodeGeo<3>);
+  return sizeof(double) * (2 * ns * nc + (reverse ? ns * d * d : 0)) + ns * geo;
+}
+
+// K2 for (q+1)^d > 27 or an L2 projection with m > q+1 points (NEXT N2): one CTA per tile,
+// Ā sampled at the m^d Gauss nodes into shared memory, d projection passes.
 template <int D, int Q>
 __global__ void __launch_bounds__(256)
 k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl,
@@ -268,18 +319,19 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
                     int ypt, double nu, double *__restrict__ coef, int kstride, int fm, int64_t n_tiles, int *flag) {
   constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
   constexpr int DD = D * D, NC = DD * DD, NK = DD * NPI;
+  const int ns = D == 2 ? c_ip.m * c_ip.m : c_ip.m * c_ip.m * c_ip.m;
   extern __shared__ double dyn[];
-  double *S0 = dyn, *S1 = dyn + NPI * NC;
+  double *S0 = dyn, *S1 = dyn + (size_t)ns * NC;
+  NodeGeo<D> *geo = reinterpret_cast<NodeGeo<D> *>(dyn + 2 * (size_t)ns * NC);
   __shared__ MacroTile<D> mt;
-  __shared__ NodeGeo<D> geo[NPI];
   const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
   load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
   __syncthreads();
-  node_geometry<D, Q>(c_ip, mt, geo, tg, flag);
+  node_geometry<D>(c_ip, mt, geo, tg, flag);
   double lam, mu;
   lame(young[ypt ? tg : 0], nu, lam, mu);
   __syncthreads();
-  for (int it = threadIdx.x; it < NPI * DD; it += blockDim.x) {   // Ā (Eq. 37, closed form)
+  for (int it = threadIdx.x; it < ns * DD; it += blockDim.x) {   // Ā (Eq. 37, closed form)
     const int m = it / DD, ij = it % DD, i = ij / D, j = ij % D;
     const NodeGeo<D> &g = geo[m];
     double *o = S0 + m * NC + ij * DD;
@@ -290,7 +342,7 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
         o[a * D + b] = g.det * (lam * g.G[i][a] * g.G[j][b] + mu * g.G[j][a] * g.G[i][b] + (a == b ? mu * g.gg[i][j] : 0.0));
   }
   __syncthreads();
-  const double *res = tensor_apply<D, Q, false, NC>(c_ip, S0, S1);
+  const double *res = c_ip.m == Q + 1 ? tensor_apply<D, Q, false, NC>(c_ip, S0, S1) : proj_apply<D, NC>(c_ip, S0, S1, false);
   for (int idx = threadIdx.x; idx < DD * NK; idx += blockDim.x) {
     const int ab = idx / NK, kap = idx % NK, ij = kap / NPI, C = kap % NPI;
     const int64_t n = t * DD + ab;
@@ -299,8 +351,8 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
   }
 }
 
-// K5b: one CTA per tile: Ŵ = Πᵀ W, reverse mode of S = ⟨Ŵ, Ā(J)⟩ per node, chain to the
-// active macro control points.
+// K5b: one CTA per tile: Ŵ = Πᵀ W at the m^d sample nodes, reverse mode of
+// S = ⟨Ŵ, Ā(J)⟩ per node, chain to the active macro control points.
 template <int D, int Q>
 __global__ void __launch_bounds__(256)
 k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
@@ -308,10 +360,11 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
             const double *__restrict__ W, int kstride, double *__restrict__ gpart, int *flag) {
   constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
   constexpr int DD = D * D, NC = DD * DD, NK = DD * NPI;
+  const int m1 = c_ip.m, ns = D == 2 ? m1 * m1 : m1 * m1 * m1;
   extern __shared__ double dyn[];
-  double *S0 = dyn, *S1 = dyn + NPI * NC, *dSdJ = dyn + 2 * NPI * NC;
+  double *S0 = dyn, *S1 = dyn + (size_t)ns * NC, *dSdJ = dyn + 2 * (size_t)ns * NC;
+  NodeGeo<D> *geo = reinterpret_cast<NodeGeo<D> *>(dSdJ + (size_t)ns * DD);
   __shared__ MacroTile<D> mt;
-  __shared__ NodeGeo<D> geo[NPI];
   const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
   load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
   const double *src = W + (size_t)t * DD * kstride;
@@ -320,11 +373,12 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
     S0[C * NC + ij * DD + ab] = src[(size_t)ab * kstride + kap];
   }
   __syncthreads();
-  node_geometry<D, Q>(c_ip, mt, geo, tg, flag);
-  const double *Wh_all = tensor_apply<D, Q, true, NC>(c_ip, S0, S1);   // Ŵ = Πᵀ W (also syncs geo)
+  node_geometry<D>(c_ip, mt, geo, tg, flag);
+  // Ŵ = Πᵀ W (also syncs geo)
+  const double *Wh_all = m1 == Q + 1 ? tensor_apply<D, Q, true, NC>(c_ip, S0, S1) : proj_apply<D, NC>(c_ip, S0, S1, true);
   double lam, mu;
   lame(young[ypt ? tg : 0], nu, lam, mu);
-  for (int m = threadIdx.x; m < NPI; m += blockDim.x) {
+  for (int m = threadIdx.x; m < ns; m += blockDim.x) {
     const double *Wh = Wh_all + m * NC;   // Ŵ[ij*DD + ab]
     const NodeGeo<D> &g = geo[m];
     const double det = g.det;
@@ -374,8 +428,8 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
     const int ra = idx / D, a = idx % D;
     const int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
     double acc = 0.0;
-    for (int m = 0; m < NPI; ++m) {
-      const int mm[3] = {m % Q1, (m / Q1) % Q1, m / (Q1 * Q1)};
+    for (int m = 0; m < ns; ++m) {
+      const int mm[3] = {m % m1, (m / m1) % m1, m / (m1 * m1)};
       for (int be = 0; be < D; ++be) {
         double v = 1.0;
         for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
@@ -429,11 +483,15 @@ static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *
                              double *coef, bool fm, cudaStream_t s) {
   using S = K2Shape<D, Q>;
   if constexpr (S::REG) {
-    const unsigned grid = (unsigned)((h.n_tiles + S::TPB - 1) / S::TPB);
-    k2_interpolate<D, Q><<<grid, S::THREADS, 0, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt,
-                                                     nu, coef, h.kstride, (int)fm, h.n_tiles, h.d_flag);
-  } else {
-    const size_t sm = sizeof(double) * 2 * S::NPI * S::NC;
+    if (h.m_proj == Q + 1) {   // interpolation: register path (else L2 projection, m > q+1)
+      const unsigned grid = (unsigned)((h.n_tiles + S::TPB - 1) / S::TPB);
+      k2_interpolate<D, Q><<<grid, S::THREADS, 0, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt,
+                                                       nu, coef, h.kstride, (int)fm, h.n_tiles, h.d_flag);
+      return cudaGetLastError();
+    }
+  }
+  {
+    const size_t sm = macro_smem_bytes(D, Q, h.m_proj, false);
     cudaError_t e = cudaFuncSetAttribute(k2_interpolate_smem<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     k2_interpolate_smem<D, Q><<<(unsigned)h.n_tiles, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan,
@@ -446,8 +504,7 @@ static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *
 template <int D, int Q>
 static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
                               const double *W, double *gpart, cudaStream_t s) {
-  constexpr int NPI = D == 2 ? (Q + 1) * (Q + 1) : (Q + 1) * (Q + 1) * (Q + 1);
-  const size_t sm = sizeof(double) * (2 * NPI * D * D * D * D + NPI * D * D);
+  const size_t sm = macro_smem_bytes(D, Q, h.m_proj, true);
   cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,

@@ -73,6 +73,7 @@ class Problem:
     young: Optional[np.ndarray] = None   # per-tile E (len n_tiles)
     n_el: Tuple[int, ...] = ()
     config_index: int = 0
+    n_proj: int = 0             # L2-projection Gauss points per direction (0: q+1 = interpolation)
 
     @property
     def n_tiles(self) -> int:

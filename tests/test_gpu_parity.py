@@ -374,3 +374,77 @@ def test_assemble_sensitivity_combined_call():
     A.assemble_sensitivity(g["ctrl"], g["young"], prob.nu, hu.numpy(), hv.numpy(), vals, gh)
     torch.cuda.synchronize()
     assert np.array_equal(gh, g1.cpu().numpy()) and torch.equal(vals, g["vals"])
+
+
+# ---------------------------------------------------------------------------
+# L2 projection with an m-point Gauss rule (iga_set_projection; Eqs. 23-24; NEXT N2)
+
+@pytest.mark.parametrize("c,m,kw", [(1, 4, {}), (1, 6, {}), (2, 4, {}), (2, 5, dict(n_el=(2, 2, 1))),
+                                    (4, 5, dict(n_el=(2, 2, 2)))])
+def test_l2_projection_parity(c, m, kw):
+    """Coefficients, element matrices, K and the sensitivity with the L2 projection of
+    m points per direction against the oracle's plain Eqs. 23-24 solve."""
+    import dataclasses
+    from paper_2107_09568_b200 import Assembler
+    from oracle import assemble as As, macro as M, sensitivity as S
+    from oracle.dofmap import DofMap, Pattern
+    from synth import make_config, draw_uv_seeded
+    prob = dataclasses.replace(make_config(c, **kw), n_proj=m)
+    # both sides solve the projection (GPU: explicit 1D operator (VᵀWV)⁻¹VᵀW per
+    # direction; oracle: the full tensor M_π system): rounding is bounded by
+    # κ(M_π)^d·ε, κ(M_π,1D) = 10 at q=2, 35 at q=3 (9.5e-12 in 3D at q=3)
+    X1, w1 = M.projection_nodes(m, 1)
+    from oracle.bspline import bernstein
+    N1 = bernstein(prob.q, X1)
+    kappa = np.linalg.cond((N1 * w1) @ N1.T) ** prob.d * 2.0 ** -52
+    tol_c, tol_e, tol_k, tol_s = (max(t, 2 * kappa) for t in (TOL_COEF, TOL_ELEM, TOL_K, TOL_SENS))
+    A = Assembler(prob)
+    A.set_projection(m)
+    assert A.projection() == m
+    s = A.sizes
+    d = prob.d
+    dev = torch.device("cuda")
+    ctrl = torch.tensor(prob.macro.ctrl, device=dev)
+    young = torch.tensor(prob.young, device=dev)
+    coef = torch.zeros(s.n_tiles * d * d * s.k_stride, dtype=torch.float64, device=dev)
+    A.interpolate(ctrl, young, prob.nu, coef)
+    cg = coef.view(s.n_tiles, d * d, s.k_stride)[:, :, :s.n_k].cpu().numpy()
+    for t in range(min(prob.n_tiles, 8)):
+        ref = M.tile_coefficients(prob, prob.macro.ctrl, t)
+        refm = np.transpose(ref, (3, 4, 1, 2, 0)).reshape(d * d, -1)
+        assert rel(cg[t], refm) < tol_c, t
+    dm = DofMap(prob)
+    tabs = As.Tables(prob)
+    pt = Pattern(prob, dm, tabs.pairs)
+    vals = torch.empty(s.nnz, dtype=torch.float64, device=dev)
+    local = torch.empty(s.n_local_rows * s.n_tiles * d * d, dtype=torch.float64, device=dev)
+    A.assemble(ctrl, young, prob.nu, vals, local)
+    ref_vals, ref_local = As.assemble_lookup(prob, tabs, pt)
+    L = local.view(s.n_local_rows, s.n_tiles, d, d).permute(1, 0, 2, 3).cpu().numpy()
+    for t in range(prob.n_tiles):
+        assert rel(L[t], ref_local[t]) < tol_e, t
+    assert rel(vals.cpu().numpy(), ref_vals) < tol_k
+    u, v = draw_uv_seeded(c, s.n_dof)
+    grad = torch.empty(s.n_macro_cp * d, dtype=torch.float64, device=dev)
+    A.sensitivity(ctrl, young, prob.nu, torch.tensor(u, device=dev), torch.tensor(v, device=dev), grad)
+    got = grad.cpu().numpy().reshape(-1, d)
+    if prob.n_tiles <= 16:
+        ref = S.sensitivity(prob, tabs, pt, u, v)
+        assert rel(got, ref) < tol_s
+    else:
+        ent = [(int(k), int(a)) for k, a in zip(np.random.default_rng(m).integers(0, len(got), 4),
+                                                np.random.default_rng(m + 1).integers(0, d, 4))]
+        ref = S.sensitivity(prob, tabs, pt, u, v, entries=ent)
+        for k, a in ent:
+            assert abs(got[k, a] - ref[k, a]) < tol_s * np.abs(got).max() * 10
+
+
+def test_projection_errors():
+    from paper_2107_09568_b200 import IgaError
+    g = gpu_case(2)
+    A = g["A"]
+    with pytest.raises(IgaError, match="EINVAL"):
+        A.set_projection(2)            # m < q+1
+    with pytest.raises(IgaError, match="ELIMIT|EINVAL"):
+        A.set_projection(7)            # 3D staging exceeds shared memory
+    assert A.projection() == 3

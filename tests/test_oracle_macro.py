@@ -118,3 +118,83 @@ def test_affine_macro_field_is_constant():
     # box [0,4]x[0,1]^2 with 4x4x4 elements: J = diag(1, .25, .25)
     A = M.A_closed(np.diag([1.0, 0.25, 0.25])[None], *M.lame(1.0, 0.3))[0]
     assert np.allclose(coef[0], A, atol=1e-14)
+
+
+# ---------------------------------------------------------------------------
+# L2 projection with an m-point Gauss rule (Eqs. 23-24; NEXT N2)
+
+def _exact_l2_1d(q, k):
+    """Exact L2 projection of x^k onto the degree-q Bernstein basis on [0,1], in rational
+    arithmetic: M_ij = C(q,i)C(q,j) B(i+j+1, 2q-i-j+1), r_i = C(q,i) B(i+k+1, q-i+1)."""
+    from fractions import Fraction
+    from math import comb, factorial
+
+    def beta(a, b):                     # B(a, b) = (a-1)!(b-1)!/(a+b-1)! for integers
+        return Fraction(factorial(a - 1) * factorial(b - 1), factorial(a + b - 1))
+    n = q + 1
+    Mx = [[comb(q, i) * comb(q, j) * beta(i + j + 1, 2 * q - i - j + 1) for j in range(n)] for i in range(n)]
+    r = [comb(q, i) * beta(i + k + 1, q - i + 1) for i in range(n)]
+    for c in range(n):                  # Gauss-Jordan in fractions
+        piv = next(i for i in range(c, n) if Mx[i][c] != 0)
+        Mx[c], Mx[piv] = Mx[piv], Mx[c]
+        r[c], r[piv] = r[piv], r[c]
+        f = Mx[c][c]
+        Mx[c] = [v / f for v in Mx[c]]
+        r[c] /= f
+        for i in range(n):
+            if i != c and Mx[i][c] != 0:
+                g = Mx[i][c]
+                Mx[i] = [a - g * b for a, b in zip(Mx[i], Mx[c])]
+                r[i] -= g * r[c]
+    return np.array([float(v) for v in r])
+
+
+@pytest.mark.parametrize("q,k,m", [(2, 4, 4), (2, 5, 4), (3, 6, 5), (1, 3, 3)])
+def test_l2_projection_matches_exact_rational_projection(q, k, m):
+    """For f = x^k the m-point rule integrates N_i f exactly when 2m-1 >= q+k, so the
+    projection equals the exact L2 projection computed in rational arithmetic."""
+    X, _ = M.projection_nodes(m, 1)
+    c = M.project_l2(X[:, 0] ** k, q, 1, m)
+    assert np.allclose(c, _exact_l2_1d(q, k), rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_l2_projection_tensor_product_of_1d(d):
+    """A separable f = x^4 y^3 (z^2) projects to the tensor product of the 1D exact
+    projections (Bernstein C direction-0 fastest)."""
+    q, m = 2, 4
+    ks = [4, 3, 2][:d]
+    X, _ = M.projection_nodes(m, d)
+    f = np.prod([X[:, k] ** ks[k] for k in range(d)], axis=0)
+    c = M.project_l2(f, q, d, m)
+    ref = _exact_l2_1d(q, ks[0])
+    for k in range(1, d):
+        ref = np.kron(_exact_l2_1d(q, ks[k]), ref)      # direction k slower
+    assert np.allclose(c, ref, rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("m", [3, 4, 6])
+def test_l2_projection_properties(m):
+    """Exact on Q_q, idempotent, residual orthogonal to Q_q in the m-point inner product,
+    and m = q+1 equals interpolation at the Gauss nodes (reading R1)."""
+    q, d = 2, 2
+    X, w = M.projection_nodes(m, d)
+    N = bernstein(q, X)
+    c0 = np.random.default_rng(m).standard_normal(N.shape[0])
+    assert np.allclose(M.project_l2(N.T @ c0, q, d, m), c0, atol=1e-13)          # exact on Q_q
+    f = np.exp(X[:, 0]) * np.sin(3 * X[:, 1])
+    c = M.project_l2(f, q, d, m)
+    assert np.allclose(M.project_l2(N.T @ c, q, d, m), c, atol=1e-13)           # idempotent
+    assert np.abs((N * w) @ (f - N.T @ c)).max() < 1e-14                          # orthogonality
+    if m == q + 1:
+        assert np.allclose(c, M.interpolate(f, q, d), atol=1e-13)
+
+
+def test_tile_coefficients_projection_converges():
+    """Curved macro map: the m-point projections converge (m -> large) to the L2
+    projection; m = q+1 and m = q+2 differ (the field is not in Q_q)."""
+    from synth import make_config
+    p = make_config(2)
+    cs = {m: M.tile_coefficients(p, p.macro.ctrl, 5, m=m) for m in (3, 4, 6, 8, 10)}
+    assert np.abs(cs[3] - cs[4]).max() > 1e-10
+    assert np.abs(cs[8] - cs[10]).max() < 1e-12 * np.abs(cs[10]).max() < np.abs(cs[4] - cs[10]).max()
