@@ -174,6 +174,26 @@ iga_status iga_sensitivity(const iga_handle *h, const double *macro_ctrl, const 
                            int32_t young_per_tile, double nu, const double *u, const double *v,
                            double *grad, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * iga_volume — V^π = Σ_t t^h · d^(t) (§3.1, Eqs. 14-19): t^h the volume lookup
+ * table (Eq. 18, built offline with the tables), d^(t) the projection coefficients of
+ * det J_ℳ(t) (Eq. 15, with the projection of iga_set_projection).  Exact when det J_ℳ ∈ Q_q
+ * (q >= d·p_M - 1, Eq. 22).  SURVEY §8(f) N3.
+ *  volume [host] 1 double: the sum over this handle's (owned) tiles.
+ *  grad   [any] optional n_macro_cp*d doubles: dV^π/dP (Eqs. 66-67: the adjoint field
+ *         Πᵀ t^h at the projection samples times ∂det J_ℳ/∂P), owned tiles only.
+ * Errors: EINVAL, EDEGENERATE, ECUDA.
+ * ------------------------------------------------------------------------- */
+iga_status iga_volume(const iga_handle *h, const double *macro_ctrl, double *volume, double *grad, void *stream);
+
+/* iga_load_vector — body-force load vector for a constant body force b (Eq. 53,
+ * body part): f_{node(t,A)} += b Σ_C 𝔉[A][C] d^(t)_C with the load lookup table
+ * 𝔉[A][C] = ∫ R_A |det J_T| N_C∘𝒯 dθ (built offline), gathered per node in a fixed order.
+ *  body_force [host] d doubles.   f [any] n_rows doubles (this handle's rows), overwritten.
+ * Σ_I f_I = b·V^π.  Errors: EINVAL, EDEGENERATE, ECUDA. */
+iga_status iga_load_vector(const iga_handle *h, const double *macro_ctrl, const double *body_force, double *f,
+                           void *stream);
+
 /* iga_assemble_sensitivity — iga_assemble followed by iga_sensitivity in one call (the
  * design-optimisation step: K and g together), one synchronisation at the end.  Host
  * u, v are copied on an internal stream while K is formed.  Arguments as in the two calls

@@ -51,7 +51,7 @@ class iga_shard(C.Structure):
 
 N_PROF = 10   # IGA_N_PROF: 0 K2, 1 K3(+scatter), 2 K4, 3 K5a, 4 K5b, 5 K5c, 6 staging, 7 K5x, 8 K3 nzdata, 9 apply
 EXPORTS = ["iga_build_tables", "iga_build_topology", "iga_assemble", "iga_sensitivity", "iga_assemble_sensitivity",
-           "iga_apply", "iga_interpolate",
+           "iga_apply", "iga_volume", "iga_load_vector", "iga_interpolate",
            "iga_get_sizes",
            "iga_get_pattern", "iga_get_block_map", "iga_get_node_map", "iga_get_tables", "iga_get_pairs",
            "iga_set_projection", "iga_get_projection", "iga_set_profiling", "iga_get_kernel_times", "iga_free",
@@ -77,6 +77,8 @@ def load():
     lib.iga_interpolate.argtypes = [vp, vp, vp, i32, d, vp, vp]
     lib.iga_apply.argtypes = [vp, vp, vp, i32, d, vp, vp, vp]
     lib.iga_assemble_sensitivity.argtypes = [vp, vp, vp, i32, d, vp, vp, vp, vp, vp]
+    lib.iga_volume.argtypes = [vp, vp, vp, vp, vp]
+    lib.iga_load_vector.argtypes = [vp, vp, vp, vp, vp]
     lib.iga_get_sizes.argtypes = [vp, C.POINTER(iga_sizes)]
     lib.iga_get_pattern.argtypes = [vp, vp, vp]
     lib.iga_get_block_map.argtypes = [vp, i64, i64, vp]
@@ -186,6 +188,17 @@ class Assembler:
         """K (CSR values) and g = uᵀ(∂K/∂P)v in one call (iga_assemble_sensitivity)."""
         _check(load().iga_assemble_sensitivity(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
                                                _ptr(u), _ptr(v), _ptr(values), _ptr(grad), _stream_ptr(stream)))
+
+    def volume(self, ctrl, grad=None, stream=None):
+        """V^π (float) and optionally dV^π/dP into grad (iga_volume)."""
+        out = np.zeros(1)
+        _check(load().iga_volume(self._h, _ptr(ctrl), out.ctypes.data, _ptr(grad), _stream_ptr(stream)))
+        return float(out[0])
+
+    def load_vector(self, ctrl, body_force, f, stream=None):
+        """Body-force load vector for a constant b (iga_load_vector)."""
+        b = np.ascontiguousarray(body_force, dtype=np.float64)
+        _check(load().iga_load_vector(self._h, _ptr(ctrl), b.ctypes.data, _ptr(f), _stream_ptr(stream)))
 
     def apply(self, ctrl, young, nu, u, y, stream=None):
         """Matrix-free y = K^π u (iga_apply)."""

@@ -13,7 +13,7 @@ Handle::~Handle() {
   void *bufs[] = {d_table, d_tabA, d_tabAT, d_coef, d_side, d_W, d_X, d_gpart, d_node_map, d_pairA, d_pairB,
                   d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_mperm, d_slot_tr,
                   d_k5_pair, d_k5_col, d_tperm, d_g1len, d_g2len, d_g1slot, d_g2slot, d_sA_ptr, d_sA_slot,
-                  d_inv_ptr, d_inv_ent, d_part, d_patch_info, d_mknots, d_mspan, d_flag};
+                  d_inv_ptr, d_inv_ent, d_part, d_F, d_th, d_det, d_Vt, d_patch_info, d_mknots, d_mspan, d_flag};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (int i = 0; i < N_STAGE; ++i)
@@ -210,6 +210,10 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, c
   CUB(cudaMalloc((void **)&h.d_coef, sizeof(double) * h.Npad * h.kstride));
   CUB(cudaMemsetAsync(h.d_coef, 0, sizeof(double) * h.Npad * h.kstride, s));
   CUB(cudaMalloc((void **)&h.d_W, sizeof(double) * N * h.kstride));
+  CUB(cudaMalloc((void **)&h.d_F, sizeof(double) * h.n_local_ctrl * h.npi));
+  CUB(cudaMalloc((void **)&h.d_th, sizeof(double) * h.npi));
+  CUB(cudaMalloc((void **)&h.d_det, sizeof(double) * h.n_tiles * h.npi));
+  CUB(cudaMalloc((void **)&h.d_Vt, sizeof(double) * (h.n_tiles + 1)));
   CUB(cudaMalloc((void **)&h.d_X, sizeof(double) * h.Npad * h.Kp));
   int nact_m = 1;
   for (int k = 0; k < d; ++k) nact_m *= h.pm[k] + 1;
@@ -415,6 +419,54 @@ iga_status iga_apply(const iga_handle *Hc, const double *macro_ctrl, const doubl
   if (!sg.flush()) { set_error("D2H copy failed"); return IGA_ECUDA; }
   pf.end(idst);
   st = check_flag(h, s);
+  pf.collect();
+  return st;
+}
+
+iga_status iga_volume(const iga_handle *Hc, const double *macro_ctrl, double *volume, double *grad, void *stream) {
+  if (!Hc || !macro_ctrl || !volume) { set_error("NULL argument"); return IGA_EINVAL; }
+  Handle &h = const_cast<iga_handle *>(Hc)->h;
+  if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Stager sg(h, s);
+  Prof pf(h, s);
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  const double *dctrl;
+  double *dgrad = nullptr;
+  if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) || (grad && !sg.out(grad, (size_t)(h.n_cp * h.d), &dgrad))) {
+    set_error("staging failed");
+    return IGA_ENOMEM;
+  }
+  CU(launch_volume(h, dctrl, h.d_Vt + h.n_tiles, dgrad ? h.d_gpart : nullptr, s));
+  if (dgrad) {
+    CU(launch_sens_reduce(h, h.d_gpart, dgrad, s));   // same per-tile partial layout as K5b
+  }
+  CU(cudaMemcpyAsync(volume, h.d_Vt + h.n_tiles, sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (!sg.flush()) { set_error("D2H copy failed"); return IGA_ECUDA; }
+  iga_status st = check_flag(h, s);
+  pf.collect();
+  return st;
+}
+
+iga_status iga_load_vector(const iga_handle *Hc, const double *macro_ctrl, const double *body_force, double *f,
+                           void *stream) {
+  if (!Hc || !macro_ctrl || !body_force || !f) { set_error("NULL argument"); return IGA_EINVAL; }
+  Handle &h = const_cast<iga_handle *>(Hc)->h;
+  if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Stager sg(h, s);
+  Prof pf(h, s);
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  const double *dctrl;
+  double *df;
+  if (!sg.in(macro_ctrl, (size_t)h.n_cp * h.d, &dctrl) || !sg.out(f, (size_t)(h.n_nodes * h.d), &df)) {
+    set_error("staging failed");
+    return IGA_ENOMEM;
+  }
+  CU(launch_volume(h, dctrl, nullptr, nullptr, s));   // d^(t) of every local tile
+  CU(launch_load(h, body_force, df, s));
+  if (!sg.flush()) { set_error("D2H copy failed"); return IGA_ECUDA; }
+  iga_status st = check_flag(h, s);
   pf.collect();
   return st;
 }

@@ -140,6 +140,11 @@ struct Handle {
   int32_t *d_g1slot = nullptr, *d_g2slot = nullptr, *d_sA_ptr = nullptr, *d_sA_slot = nullptr, *d_inv_ent = nullptr;
   int64_t *d_inv_ptr = nullptr;
   double *d_part = nullptr;      // [n_tiles][P][d] apply partials (allocated by the first iga_apply)
+  // volume / load (NEXT N3)
+  double *d_F = nullptr;         // [n_local_ctrl][npi] load table 𝔉 (Eq. 53)
+  double *d_th = nullptr;        // [npi] volume table t^h (Eq. 18)
+  double *d_det = nullptr;       // [n_tiles][npi] projection coefficients of det J_ℳ (Eq. 15)
+  double *d_Vt = nullptr;        // [n_tiles] tile volumes, [n_tiles] + 1: the total
   int32_t *d_patch_info = nullptr; // [n_patches][3]: first K5a chunk, ctrl_off, n_ctrl (+ sentinel chunk)
   double *d_mknots = nullptr;    // macro knots, 3 directions concatenated
   int32_t *d_mspan = nullptr;    // element -> knot span, 3 directions concatenated
@@ -187,6 +192,8 @@ size_t k5x_smem_bytes(int d, int max_patch_ctrl);
 cudaError_t launch_sens_reverse(const Handle &h, const double *ctrl, const double *young, int young_per_tile,
                                 double nu, const double *W, double *gpart, cudaStream_t s);
 cudaError_t launch_sens_reduce(const Handle &h, const double *gpart, double *grad, cudaStream_t s);
+cudaError_t launch_volume(const Handle &h, const double *ctrl, double *d_volume, double *gpart, cudaStream_t s);
+cudaError_t launch_load(const Handle &h, const double *b, double *f, cudaStream_t s);
 InterpConst make_interp_const(const Handle &h);
 
 // host build steps (host_build.cpp)

@@ -440,6 +440,145 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Volume, volume gradient, body-force load vector (§3.1 Eqs. 14-19, Eq. 53,
+// Eqs. 66-67).  Per tile: det J_ℳ at the m^d sample nodes, its
+// projection coefficients d^(t) = Π·det (Eq. 15), V_t = t^h · d^(t) (Eq. 19); for the
+// gradient the adjoint weights ŵ_m = (Πᵀ t^h)_m (the adjoint field of Eq. 67 at the
+// samples) give ∂V_t/∂J_m = ŵ_m det J_m J_m⁻ᵀ, chained to the control points.
+template <int D>
+__global__ void __launch_bounds__(128)
+kv_tile(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
+        const int *__restrict__ mspan, const double *__restrict__ th, int npi, double *__restrict__ dcoef,
+        double *__restrict__ Vt, double *__restrict__ gpart, int *flag) {
+  // 3D: m <= 6 (set_projection bounds the staging of K2/K5b to m <= 5)
+  constexpr int MAXNS = D == 2 ? IGA_MAXM * IGA_MAXM : 216;
+  __shared__ MacroTile<D> mt;
+  __shared__ double sdet[MAXNS], swh[MAXNS];
+  __shared__ double sG[MAXNS][D][D];
+  __shared__ double sd[(IGA_MAXQ + 1) * (IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
+  const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
+  const int q1 = c_ip.q + 1, m1 = c_ip.m, ns = D == 2 ? m1 * m1 : m1 * m1 * m1;
+  load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
+  __syncthreads();
+  for (int m = threadIdx.x; m < ns; m += blockDim.x) {
+    double J[D][D], G[D][D];
+    macro_J<D>(c_ip, mt, m, J);
+    const double det = det_inv<D>(J, G);
+    if (!(det > 0.0)) raise_flag(flag, 2, (int)tg, m);
+    sdet[m] = det;
+    for (int i = 0; i < D; ++i)
+      for (int j = 0; j < D; ++j) sG[m][i][j] = G[i][j];
+  }
+  __syncthreads();
+  // Π[C][m] = Π_k Pi1[c_k][m_k]
+  auto Pi = [&](int C, int m) {
+    double v = 1.0;
+    for (int k = 0; k < D; ++k) {
+      const int c = (C / (k == 0 ? 1 : (k == 1 ? q1 : q1 * q1))) % q1;
+      const int mk = (m / (k == 0 ? 1 : (k == 1 ? m1 : m1 * m1))) % m1;
+      v *= c_ip.Pi1[c * m1 + mk];
+    }
+    return v;
+  };
+  for (int C = threadIdx.x; C < npi; C += blockDim.x) {
+    double acc = 0.0;
+    for (int m = 0; m < ns; ++m) acc = fma(Pi(C, m), sdet[m], acc);
+    sd[C] = acc;
+    dcoef[t * npi + C] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int C = 0; C < npi; ++C) v = fma(th[C], sd[C], v);
+    Vt[t] = v;
+  }
+  if (!gpart || t >= c_ip.n_own) return;
+  for (int m = threadIdx.x; m < ns; m += blockDim.x) {
+    double acc = 0.0;
+    for (int C = 0; C < npi; ++C) acc = fma(Pi(C, m), th[C], acc);
+    swh[m] = acc * sdet[m];   // ŵ_m det_m: ∂V/∂J_m[a][β] = swh_m G_m[β][a]
+  }
+  __syncthreads();
+  int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
+  for (int idx = threadIdx.x; idx < mt.nact * D; idx += blockDim.x) {
+    const int ra = idx / D, a = idx % D;
+    const int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
+    double acc = 0.0;
+    for (int m = 0; m < ns; ++m) {
+      const int mm[3] = {m % m1, (m / m1) % m1, m / (m1 * m1)};
+      for (int be = 0; be < D; ++be) {
+        double v = 1.0;
+        for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
+        acc += swh[m] * sG[m][be][a] * v;
+      }
+    }
+    gpart[((size_t)t * mt.nact + ra) * D + a] = acc;
+  }
+}
+
+// V = Σ_{owned t} V_t, fixed order (one block: strided partial sums, then a fixed tree)
+__global__ void kv_sum(const double *__restrict__ Vt, int64_t n, double *__restrict__ out) {
+  __shared__ double part[256];
+  double acc = 0.0;
+  for (int64_t t = threadIdx.x; t < n; t += 256) acc += Vt[t];
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = part[0];
+}
+
+// f[i] = b Σ_{(t,A) occurrences of owned node i, fixed order} Σ_C 𝔉[A][C] d^(t)_C   (Eq. 53)
+template <int D>
+__global__ void __launch_bounds__(256)
+kf_gather(const double *__restrict__ F, const double *__restrict__ dcoef, int npi, const int64_t *__restrict__ inv_ptr,
+          const int32_t *__restrict__ inv_ent, int nl, int64_t n_nodes, double b0, double b1, double b2,
+          double *__restrict__ f) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_nodes) return;
+  double s = 0.0;
+  for (int64_t k = inv_ptr[i]; k < inv_ptr[i + 1]; ++k) {
+    const int32_t e = inv_ent[k];
+    const int64_t t = e / nl;
+    const int A = e % nl;
+    double v = 0.0;
+    for (int C = 0; C < npi; ++C) v = fma(F[(size_t)A * npi + C], dcoef[t * npi + C], v);
+    s += v;
+  }
+  const double b[3] = {b0, b1, b2};
+#pragma unroll
+  for (int a = 0; a < D; ++a) f[i * D + a] = b[a] * s;
+}
+
+cudaError_t launch_volume(const Handle &h, const double *ctrl, double *d_volume, double *gpart, cudaStream_t s) {
+  const InterpConst ic = make_interp_const(h);
+  if (h.d == 2)
+    kv_tile<2><<<(unsigned)h.n_tiles, 128, 0, s>>>(ic, ctrl, h.d_mknots, h.d_mspan, h.d_th, h.npi, h.d_det, h.d_Vt,
+                                                   gpart, h.d_flag);
+  else
+    kv_tile<3><<<(unsigned)h.n_tiles, 128, 0, s>>>(ic, ctrl, h.d_mknots, h.d_mspan, h.d_th, h.npi, h.d_det, h.d_Vt,
+                                                   gpart, h.d_flag);
+  cudaError_t e = cudaGetLastError();
+  if (e || !d_volume) return e;
+  kv_sum<<<1, 256, 0, s>>>(h.d_Vt, h.n_tiles_own, d_volume);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_load(const Handle &h, const double *b, double *f, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((h.n_nodes + 255) / 256);
+  const double b2 = h.d == 3 ? b[2] : 0.0;
+  if (h.d == 2)
+    kf_gather<2><<<blocks, 256, 0, s>>>(h.d_F, h.d_det, h.npi, h.d_inv_ptr, h.d_inv_ent, h.n_local_ctrl, h.n_nodes,
+                                        b[0], b[1], b2, f);
+  else
+    kf_gather<3><<<blocks, 256, 0, s>>>(h.d_F, h.d_det, h.npi, h.d_inv_ptr, h.d_inv_ent, h.n_local_ctrl, h.n_nodes,
+                                        b[0], b[1], b2, f);
+  return cudaGetLastError();
+}
+
 template <int D>
 __global__ void k5c_reduce(const __grid_constant__ InterpConst c_ip, const int *__restrict__ mspan, const double *__restrict__ gpart, int nact,
                            int64_t n_cp, double *__restrict__ grad) {

@@ -20,7 +20,7 @@ template <int D>
 __global__ void k1_point_data(int n_patches, int n_g, int p, int q, const double *__restrict__ tile_ctrl,
                               const double *__restrict__ knots, const int *__restrict__ elspan, int total_pts,
                               double *__restrict__ wD, double *__restrict__ G, double *__restrict__ Nc,
-                              int *flag) {
+                              double *__restrict__ Rv, int *flag) {
   int gp = blockIdx.x * blockDim.x + threadIdx.x;
   if (gp >= total_pts) return;
   int pi = 0;
@@ -80,6 +80,9 @@ __global__ void k1_point_data(int n_patches, int n_g, int p, int q, const double
   double *Gp = G + (size_t)gp * nact * D;
   for (int la = 0; la < nact; ++la) {
     int r[3] = {la % n1, (la / n1) % n1, la / (n1 * n1)};
+    double R = 1.0;
+    for (int k = 0; k < D; ++k) R *= N1[k][r[k]];
+    Rv[(size_t)gp * nact + la] = R;
     double dR[D];
     for (int m = 0; m < D; ++m) {
       double v = 1.0;
@@ -159,6 +162,58 @@ __global__ void k1_table_rows(int n_patches, int n_g, int p, int q, int nk, int 
   }
 }
 
+// Load / volume tables (Eq. 53 body part, Eq. 18), offline:
+//   𝔉[A][C] = Σ_spans(A) Σ_g w_g |span| det J_T R_A N_C(𝒯(θ_g))   one CTA per control point
+//   t^h[C]  = Σ_patches Σ_spans Σ_g w_g |span| det J_T N_C(𝒯(θ_g))  one thread per C
+template <int D>
+__global__ void k1_load_rows(int n_patches, int n_g, int p, int npi, const int *__restrict__ elspan,
+                             const double *__restrict__ wD, const double *__restrict__ Nc,
+                             const double *__restrict__ Rv, double *__restrict__ F) {
+  const int Aglob = blockIdx.x;
+  int pi = 0;
+  while (pi + 1 < n_patches && Aglob >= c_patches[pi + 1].ctrl_off) ++pi;
+  const DevPatch &P = c_patches[pi];
+  const int A = Aglob - P.ctrl_off;
+  const int a[3] = {A % P.n[0], (A / P.n[0]) % P.n[1], A / (P.n[0] * P.n[1])};
+  const int n1 = p + 1;
+  int nact = 1, ng_d = 1;
+  for (int k = 0; k < D; ++k) { nact *= n1; ng_d *= n_g; }
+  int elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
+  for (int k = 0; k < D; ++k) {   // elements whose span s satisfies a_k <= s <= a_k + p
+    const int *es = elspan + P.elspan_off[k];
+    elo[k] = P.n_span[k];
+    ehi[k] = -1;
+    for (int e = 0; e < P.n_span[k]; ++e)
+      if (es[e] >= a[k] && es[e] <= a[k] + p) { elo[k] = min(elo[k], e); ehi[k] = max(ehi[k], e); }
+  }
+  for (int C = threadIdx.x; C < npi; C += blockDim.x) {
+    double acc = 0.0;
+    for (int e2 = (D == 3 ? elo[2] : 0); e2 <= (D == 3 ? ehi[2] : 0); ++e2)
+      for (int e1 = elo[1]; e1 <= ehi[1]; ++e1)
+        for (int e0 = elo[0]; e0 <= ehi[0]; ++e0) {
+          const int e[3] = {e0, e1, e2};
+          const int span_lin = e0 + P.n_span[0] * (e1 + P.n_span[1] * e2);
+          int la = 0;
+          for (int k = D - 1; k >= 0; --k) la = la * n1 + (a[k] - (elspan[P.elspan_off[k] + e[k]] - p));
+          const int64_t base = P.pt_off + (int64_t)span_lin * ng_d;
+          for (int g = 0; g < ng_d; ++g) {
+            const int64_t pt = base + g;
+            acc += wD[pt] * Rv[(size_t)pt * nact + la] * Nc[(size_t)pt * npi + C];
+          }
+        }
+    F[(size_t)Aglob * npi + C] = acc;
+  }
+}
+
+__global__ void k1_volume_table(int total_pts, int npi, const double *__restrict__ wD, const double *__restrict__ Nc,
+                                double *__restrict__ th) {
+  const int C = blockIdx.x * blockDim.x + threadIdx.x;
+  if (C >= npi) return;
+  double acc = 0.0;
+  for (int pt = 0; pt < total_pts; ++pt) acc += wD[pt] * Nc[(size_t)pt * npi + C];
+  th[C] = acc;
+}
+
 // Offline re-layout of the row-major table into the two fragment-major GEMM operands
 // (device_common.cuh fm_index): K3's A (rows = table rows, BR = IGA_K3_BM) and K5a's A
 // (rows = κ, reduction columns = table rows with each patch padded to 16, BR = 32W).
@@ -191,8 +246,9 @@ cudaError_t launch_tables(const Handle &h, const DevPatch *dpatches, int n_patch
   if ((e = cudaMemcpyToSymbolAsync(c_gw, gw, sizeof(double) * h.n_g, 0, cudaMemcpyHostToDevice, s))) return e;
   int nact = 1;
   for (int k = 0; k < h.d; ++k) nact *= (h.p + 1);
-  double *wD, *G, *Nc;
+  double *wD, *G, *Nc, *Rv;
   int *row_patch;
+  if ((e = cudaMallocAsync((void **)&Rv, sizeof(double) * (size_t)total_pts * nact, s))) return e;
   if ((e = cudaMallocAsync((void **)&wD, sizeof(double) * total_pts, s))) return e;
   if ((e = cudaMallocAsync((void **)&G, sizeof(double) * (size_t)total_pts * nact * h.d, s))) return e;
   if ((e = cudaMallocAsync((void **)&Nc, sizeof(double) * (size_t)total_pts * h.npi, s))) return e;
@@ -204,10 +260,10 @@ cudaError_t launch_tables(const Handle &h, const DevPatch *dpatches, int n_patch
   int threads = 128, blocks = (total_pts + threads - 1) / threads;
   if (h.d == 2)
     k1_point_data<2><<<blocks, threads, 0, s>>>(n_patches, h.n_g, h.p, h.q, d_tile_ctrl, d_tile_knots, d_tile_elspan,
-                                                total_pts, wD, G, Nc, h.d_flag);
+                                                total_pts, wD, G, Nc, Rv, h.d_flag);
   else
     k1_point_data<3><<<blocks, threads, 0, s>>>(n_patches, h.n_g, h.p, h.q, d_tile_ctrl, d_tile_knots, d_tile_elspan,
-                                                total_pts, wD, G, Nc, h.d_flag);
+                                                total_pts, wD, G, Nc, Rv, h.d_flag);
   if ((e = cudaGetLastError())) return e;
   int tpb = h.nk >= 256 ? 256 : 128;
   if (h.d == 2)
@@ -217,6 +273,13 @@ cudaError_t launch_tables(const Handle &h, const DevPatch *dpatches, int n_patch
     k1_table_rows<3><<<(unsigned)h.M, tpb, 0, s>>>(n_patches, h.n_g, h.p, h.q, h.nk, h.kstride, h.M, (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK, row_patch,
                                                    h.d_pairA, h.d_pairB, d_tile_elspan, wD, G, Nc, h.d_table);
   if ((e = cudaGetLastError())) return e;
+  if (h.d == 2)
+    k1_load_rows<2><<<(unsigned)h.n_local_ctrl, 64, 0, s>>>(n_patches, h.n_g, h.p, h.npi, d_tile_elspan, wD, Nc, Rv, h.d_F);
+  else
+    k1_load_rows<3><<<(unsigned)h.n_local_ctrl, 64, 0, s>>>(n_patches, h.n_g, h.p, h.npi, d_tile_elspan, wD, Nc, Rv, h.d_F);
+  k1_volume_table<<<(h.npi + 63) / 64, 64, 0, s>>>(total_pts, h.npi, wD, Nc, h.d_th);
+  if ((e = cudaGetLastError())) return e;
+  cudaFreeAsync(Rv, s);
   cudaFreeAsync(wD, s);
   cudaFreeAsync(G, s);
   cudaFreeAsync(Nc, s);

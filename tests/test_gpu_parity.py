@@ -448,3 +448,53 @@ def test_projection_errors():
     with pytest.raises(IgaError, match="ELIMIT|EINVAL"):
         A.set_projection(7)            # 3D staging exceeds shared memory
     assert A.projection() == 3
+
+
+# ---------------------------------------------------------------------------
+# volume, volume gradient, load vector (NEXT N3; Eqs. 14-19, 53, 66-67)
+
+@pytest.mark.parametrize("c,kw", [(1, {}), (2, {}), (3, dict(n_el=(2, 2, 2))), (4, dict(n_el=(2, 2, 2))),
+                                  (2, dict(n_proj=5))])
+def test_volume_load_parity(c, kw):
+    """V^π, dV^π/dP and the body-force load vector against the oracle."""
+    import dataclasses
+    from paper_2107_09568_b200 import Assembler
+    from oracle import volume as V
+    from oracle.dofmap import DofMap
+    from synth import make_config
+    m = kw.pop("n_proj", 0)
+    prob = make_config(c, **kw)
+    if m:
+        prob = dataclasses.replace(prob, n_proj=m)
+    A = Assembler(prob)
+    if m:
+        A.set_projection(m)
+    s = A.sizes
+    d = prob.d
+    ctrl = torch.tensor(prob.macro.ctrl, device="cuda")
+    grad = torch.empty(s.n_macro_cp * d, dtype=torch.float64, device="cuda")
+    vol = A.volume(ctrl, grad)
+    vref = V.volume_lookup(prob)
+    assert abs(vol - vref) < 1e-13 * abs(vref)
+    gref = V.volume_gradient(prob)
+    assert rel(grad.cpu().numpy().reshape(-1, d), gref) < 1e-12
+    dm = DofMap(prob)
+    b = np.array([0.5, -1.0, 2.0][:d])
+    f = torch.empty(s.n_dof, dtype=torch.float64, device="cuda")
+    A.load_vector(ctrl, b, f)
+    fref = V.load_vector(prob, dm.node, dm.n_nodes, b)
+    assert rel(f.cpu().numpy().reshape(-1, d), fref) < 1e-12
+    # shards: volumes and gradients add up, load rows are the whole problem's rows
+    if c == 3:
+        vs, gs = 0.0, torch.zeros_like(grad)
+        for k in range(2):
+            B = Assembler(prob, shard=(2, k))
+            z = B.sizes
+            gk = torch.empty_like(grad)
+            vs += B.volume(ctrl, gk)
+            gs += gk
+            fk = torch.empty(z.n_rows, dtype=torch.float64, device="cuda")
+            B.load_vector(ctrl, b, fk)
+            assert torch.equal(fk, f[z.row_begin:z.row_begin + z.n_rows])
+        assert abs(vs - vol) < 1e-13 * abs(vol)
+        assert (torch.linalg.norm(gs - grad) / torch.linalg.norm(grad)).item() < 1e-13
