@@ -47,7 +47,9 @@ typedef enum {
   IGA_ELIMIT = 6           /* problem exceeds an index-width limit of this build */
 } iga_status;
 
-/* A tensor-product B-spline patch (Eq. 2).  [host]
+/* A tensor-product B-spline patch (Eq. 2), or a NURBS patch when weights is
+ * not NULL (macro map only: the rational F of the paper's torus and
+ * twist, §3.3.4; tile patches must be B-splines).  [host]
  * dim: parametric = physical dimension d (2 or 3).
  * degree[k] >= 1, knots[k] (n_knots[k] values): open, non-decreasing, first = 0,
  * last = 1, interior multiplicity <= degree[k].  n_ctrl = Π_k (n_knots[k]-degree[k]-1).
@@ -59,6 +61,7 @@ typedef struct {
   int32_t n_knots[3];
   const double *knots[3];
   const double *ctrl;
+  const double *weights;   /* n_ctrl positive weights (NURBS) or NULL (B-spline) */
 } iga_spline;
 
 /* Declared intra-tile interface (R10): face (dir_a, side_a) of patch_a is glued to

@@ -68,6 +68,8 @@ def macro_jacobian(macro, ctrl, t, xi):
     """J[a, k] = ∂F_a/∂ξ_k at element-local points xi (n_pts, d) of tile t.
 
     F(u) = Σ_i R_i^H(u) m_i (Eq. 4); u_k = U_k[s_k] + h_k ξ_k; ∂/∂ξ_k = h_k ∂/∂u_k.
+    NURBS (macro.weights, NEXT N4): R_i = w_i N_i / W with W = Σ_j w_j N_j, so
+    ∂_k R_i = w_i (∂_k N_i W - N_i ∂_k W) / W².
     `ctrl` may be complex (complex-step sensitivity).  Returns (n_pts, d, d)."""
     d = macro.dim
     spans = tile_element(macro, t)
@@ -81,13 +83,21 @@ def macro_jacobian(macro, ctrl, t, xi):
         vals.append(N)
         ders.append(dN * h)
     n = macro.n_per_dir
-    J = np.zeros((xi.shape[0], d, d), dtype=np.result_type(ctrl, np.float64))
-    for A in _active(macro, spans):           # basis functions nonzero on the element
+    act = _active(macro, spans)               # basis functions nonzero on the element
+    Nt, dNt = {}, {}
+    for A in act:                             # tensor-product N_A and ∂_k N_A
         ii = multi_index(n, A)
+        Nt[A] = np.prod([vals[m][ii[m]] for m in range(d)], axis=0)
+        dNt[A] = [np.prod([ders[m][ii[m]] if m == k else vals[m][ii[m]] for m in range(d)], axis=0)
+                  for k in range(d)]
+    w = getattr(macro, "weights", None)
+    if w is not None:
+        W = sum(w[A] * Nt[A] for A in act)
+        dW = [sum(w[A] * dNt[A][k] for A in act) for k in range(d)]
+    J = np.zeros((xi.shape[0], d, d), dtype=np.result_type(ctrl, np.float64))
+    for A in act:
         for k in range(d):
-            g = np.ones(xi.shape[0])
-            for m in range(d):
-                g = g * (ders[m][ii[m]] if m == k else vals[m][ii[m]])
+            g = dNt[A][k] if w is None else w[A] * (dNt[A][k] * W - Nt[A] * dW[k]) / W ** 2
             J[:, :, k] += g[:, None] * ctrl[A][None, :]
     return J
 
@@ -104,9 +114,15 @@ def macro_position(macro, ctrl, t, xi):
         vals.append(basis_1d(U, macro.degree[k], s, u)[0])
     n = macro.n_per_dir
     X = np.zeros((xi.shape[0], d))
+    w = getattr(macro, "weights", None)
+    W = 0.0
+    if w is not None:
+        for A in _active(macro, spans):
+            ii = multi_index(n, A)
+            W = W + w[A] * np.prod([vals[m][ii[m]] for m in range(d)], axis=0)
     for A in _active(macro, spans):
         ii = multi_index(n, A)
-        g = np.ones(xi.shape[0])
+        g = np.ones(xi.shape[0]) if w is None else w[A] / W
         for m in range(d):
             g = g * vals[m][ii[m]]
         X += g[:, None] * ctrl[A][None, :]

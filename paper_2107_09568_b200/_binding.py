@@ -27,7 +27,8 @@ class IgaError(RuntimeError):
 
 class iga_spline(C.Structure):
     _fields_ = [("dim", C.c_int32), ("degree", C.c_int32 * 3), ("n_knots", C.c_int32 * 3),
-                ("knots", C.POINTER(C.c_double) * 3), ("ctrl", C.POINTER(C.c_double))]
+                ("knots", C.POINTER(C.c_double) * 3), ("ctrl", C.POINTER(C.c_double)),
+                ("weights", C.POINTER(C.c_double))]
 
 
 class iga_interface(C.Structure):
@@ -142,6 +143,10 @@ def _spline(s, keep):
         P = np.ascontiguousarray(s.ctrl, dtype=np.float64)
         keep.append(P)
         sp.ctrl = P.ctypes.data_as(C.POINTER(C.c_double))
+    if getattr(s, "weights", None) is not None:
+        w = np.ascontiguousarray(s.weights, dtype=np.float64)
+        keep.append(w)
+        sp.weights = w.ctypes.data_as(C.POINTER(C.c_double))
     return sp
 
 

@@ -202,6 +202,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       P.n_spans *= P.n_span[k];
     }
     if (!s.ctrl) { set_error("tile patch %d: no control points", pi); return IGA_EINVAL; }
+    if (s.weights) { set_error("tile patch %d: rational (NURBS) tile patches are not supported", pi); return IGA_EINVAL; }
     P.ctrl.assign(s.ctrl, s.ctrl + (size_t)P.n_ctrl * d);
     for (double c : P.ctrl)
       if (!(c >= -1e-12 && c <= 1.0 + 1e-12)) { set_error("tile patch %d: control point outside [0,1]^d (Eq. 10 condition)", pi); return IGA_EINVAL; }
@@ -218,6 +219,12 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     h.mel[k] = (int)h.mel_span[k].size();
     h.n_cp *= h.mn[k];
     h.n_tiles *= h.mel[k];
+  }
+  h.mweights.clear();
+  if (macro->weights) {   // NURBS macro map (NEXT N4)
+    h.mweights.assign(macro->weights, macro->weights + h.n_cp);
+    for (double w : h.mweights)
+      if (!(w > 0.0)) { set_error("macro weights must be positive"); return IGA_EINVAL; }
   }
   h.n_g = n_gauss > 0 ? n_gauss : h.p + (q + 2) / 2;
   if (h.n_g > 12) { set_error("n_gauss=%d > 12", h.n_g); return IGA_EINVAL; }

@@ -67,6 +67,7 @@ struct Handle {
   int mn[3] = {1, 1, 1};         // macro control points per dir
   int mel[3] = {1, 1, 1};        // macro elements per dir
   std::vector<double> mknots[3];
+  std::vector<double> mweights;  // NURBS macro weights (empty: B-spline)
   std::vector<int> mel_span[3];
   int64_t n_cp = 0;
   // tiles: global count; this handle's local tiles [t_base, t_base + n_tiles) of which the
@@ -147,6 +148,7 @@ struct Handle {
   double *d_Vt = nullptr;        // [n_tiles] tile volumes, [n_tiles] + 1: the total
   int32_t *d_patch_info = nullptr; // [n_patches][3]: first K5a chunk, ctrl_off, n_ctrl (+ sentinel chunk)
   double *d_mknots = nullptr;    // macro knots, 3 directions concatenated
+  double *d_mweights = nullptr;  // [n_cp] NURBS macro weights (nullptr: B-spline)
   int32_t *d_mspan = nullptr;    // element -> knot span, 3 directions concatenated
   int *d_flag = nullptr;         // [0] error flag, [1] tile, [2] node
   // staging (host pointers in [any] arguments)
@@ -167,6 +169,7 @@ struct Handle {
 struct InterpConst {
   int d, q, pm[3], mn[3], mel[3], moff[3], soff[3];   // offsets of direction k in d_mknots / d_mspan
   int64_t t_base;        // global id of local tile 0
+  const double *mweights;   // NURBS macro weights (nullptr: B-spline)
   int64_t n_own;         // owned local tiles (sensitivity reduction)
   int m;                 // projection points per direction (q+1: interpolation)
   double Pi1[(IGA_MAXQ + 1) * IGA_MAXM];   // [(q+1) x m]

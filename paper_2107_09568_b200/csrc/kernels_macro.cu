@@ -31,6 +31,7 @@ InterpConst make_interp_const(const Handle &h) {
     soff += (k < h.d) ? (int)h.mel_span[k].size() : 0;
   }
   ic.t_base = h.t_base;
+  ic.mweights = h.d_mweights;
   ic.n_own = h.n_tiles_own;
   ic.m = h.m_proj;
   for (int i = 0; i < (IGA_MAXQ + 1) * IGA_MAXM; ++i) ic.Pi1[i] = h.Pi1[i];
@@ -44,7 +45,9 @@ struct MacroTile {
   double B1[D][IGA_MAXM][IGA_MAXP + 1];
   double D1[D][IGA_MAXM][IGA_MAXP + 1];   // derivative w.r.t. ξ_k (includes span length)
   double P[(D == 2 ? (IGA_MAXP + 1) * (IGA_MAXP + 1) : (IGA_MAXP + 1) * (IGA_MAXP + 1) * (IGA_MAXP + 1)) * D];
+  double Wt[D == 2 ? (IGA_MAXP + 1) * (IGA_MAXP + 1) : (IGA_MAXP + 1) * (IGA_MAXP + 1) * (IGA_MAXP + 1)];   // NURBS weights
   int nact;
+  int rational;
 };
 
 template <int D>
@@ -69,7 +72,10 @@ __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64
   }
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   int nact = n1[0] * n1[1] * n1[2];
-  if (tid == 0) mt.nact = nact;
+  if (tid == 0) {
+    mt.nact = nact;
+    mt.rational = c_ip.mweights != nullptr;
+  }
   for (int idx = tid; idx < nact * D; idx += nthr) {
     int ra = idx / D, a = idx % D;
     int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
@@ -79,6 +85,47 @@ __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64
       cp = cp * c_ip.mn[k] + (s - c_ip.pm[k] + r[k]);
     }
     mt.P[idx] = ctrl[cp * D + a];
+    if (a == 0) mt.Wt[ra] = c_ip.mweights ? c_ip.mweights[cp] : 1.0;
+  }
+}
+
+// NURBS (NEXT N4): W = Σ_r w_r N_r and ∂_β W at sample node m (B-spline: 1, 0)
+template <int D>
+__device__ void macro_W(const InterpConst &c_ip, const MacroTile<D> &mt, int m, double &W, double dW[D]) {
+  W = 1.0;
+  for (int be = 0; be < D; ++be) dW[be] = 0.0;
+  if (!mt.rational) return;
+  const int q1 = c_ip.m;
+  int mm[3] = {m % q1, (m / q1) % q1, m / (q1 * q1)};
+  int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
+  W = 0.0;
+  for (int ra = 0; ra < mt.nact; ++ra) {
+    int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
+    double N = 1.0;
+    for (int k = 0; k < D; ++k) N *= mt.B1[k][mm[k]][r[k]];
+    W += mt.Wt[ra] * N;
+    for (int be = 0; be < D; ++be) {
+      double v = 1.0;
+      for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
+      dW[be] += mt.Wt[ra] * v;
+    }
+  }
+}
+
+// ∂R_r/∂ξ_β at sample node m (rational: w_r (∂_β N_r W - N_r ∂_β W) / W²)
+template <int D>
+__device__ __forceinline__ void basis_grad(const InterpConst &c_ip, const MacroTile<D> &mt, int m, int ra, double W,
+                                           const double *dW, double g[D]) {
+  const int q1 = c_ip.m;
+  int mm[3] = {m % q1, (m / q1) % q1, m / (q1 * q1)};
+  int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
+  int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
+  double N = 1.0;
+  for (int k = 0; k < D; ++k) N *= mt.B1[k][mm[k]][r[k]];
+  for (int be = 0; be < D; ++be) {
+    double v = 1.0;
+    for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
+    g[be] = mt.rational ? mt.Wt[ra] * (v * W - N * dW[be]) / (W * W) : v;
   }
 }
 
@@ -90,13 +137,19 @@ __device__ void macro_J(const InterpConst &c_ip, const MacroTile<D> &mt, int m, 
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   for (int a = 0; a < D; ++a)
     for (int b = 0; b < D; ++b) J[a][b] = 0.0;
+  double W = 1.0, dW[D];
+  if (mt.rational) macro_W<D>(c_ip, mt, m, W, dW);
   for (int ra = 0; ra < mt.nact; ++ra) {
     int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
     double g[D];
-    for (int be = 0; be < D; ++be) {
-      double v = 1.0;
-      for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
-      g[be] = v;
+    if (mt.rational) {
+      basis_grad<D>(c_ip, mt, m, ra, W, dW, g);
+    } else {
+      for (int be = 0; be < D; ++be) {
+        double v = 1.0;
+        for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
+        g[be] = v;
+      }
     }
     for (int a = 0; a < D; ++a) {
       double x = mt.P[ra * D + a];
@@ -184,6 +237,7 @@ __device__ const double *proj_apply(const InterpConst &c_ip, double *a, double *
 template <int D>
 struct NodeGeo {
   double G[D][D], gg[D][D], det;
+  double W, dW[D];   // NURBS denominator and its gradient at the node (B-spline: 1, 0)
 };
 
 template <int D>
@@ -204,6 +258,7 @@ __device__ __forceinline__ void node_geometry(const InterpConst &c_ip, const Mac
         o.gg[i][j] = v;
       }
     o.det = det;
+    macro_W<D>(c_ip, mt, m, o.W, o.dW);
   }
 }
 
@@ -422,19 +477,14 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
       }
   }
   __syncthreads();
-  // chain to the active control points: g[r][a] = Σ_m Σ_β ∂S/∂J[a][β] ∂_β N_r(ξ_m)
-  int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
+  // chain to the active control points: g[r][a] = Σ_m Σ_β ∂S/∂J[a][β] ∂_β R_r(ξ_m)
   for (int idx = threadIdx.x; idx < mt.nact * D; idx += blockDim.x) {
     const int ra = idx / D, a = idx % D;
-    const int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
     double acc = 0.0;
     for (int m = 0; m < ns; ++m) {
-      const int mm[3] = {m % m1, (m / m1) % m1, m / (m1 * m1)};
-      for (int be = 0; be < D; ++be) {
-        double v = 1.0;
-        for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
-        acc += dSdJ[m * DD + a * D + be] * v;
-      }
+      double g[D];
+      basis_grad<D>(c_ip, mt, m, ra, geo[m].W, geo[m].dW, g);
+      for (int be = 0; be < D; ++be) acc += dSdJ[m * DD + a * D + be] * g[be];
     }
     gpart[((size_t)t * mt.nact + ra) * D + a] = acc;
   }
@@ -456,6 +506,7 @@ kv_tile(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctr
   __shared__ MacroTile<D> mt;
   __shared__ double sdet[MAXNS], swh[MAXNS];
   __shared__ double sG[MAXNS][D][D];
+  __shared__ double sW[MAXNS], sdW[MAXNS][D];
   __shared__ double sd[(IGA_MAXQ + 1) * (IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
   const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
   const int q1 = c_ip.q + 1, m1 = c_ip.m, ns = D == 2 ? m1 * m1 : m1 * m1 * m1;
@@ -469,6 +520,7 @@ kv_tile(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctr
     sdet[m] = det;
     for (int i = 0; i < D; ++i)
       for (int j = 0; j < D; ++j) sG[m][i][j] = G[i][j];
+    macro_W<D>(c_ip, mt, m, sW[m], sdW[m]);
   }
   __syncthreads();
   // Π[C][m] = Π_k Pi1[c_k][m_k]
@@ -500,18 +552,13 @@ kv_tile(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctr
     swh[m] = acc * sdet[m];   // ŵ_m det_m: ∂V/∂J_m[a][β] = swh_m G_m[β][a]
   }
   __syncthreads();
-  int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   for (int idx = threadIdx.x; idx < mt.nact * D; idx += blockDim.x) {
     const int ra = idx / D, a = idx % D;
-    const int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
     double acc = 0.0;
     for (int m = 0; m < ns; ++m) {
-      const int mm[3] = {m % m1, (m / m1) % m1, m / (m1 * m1)};
-      for (int be = 0; be < D; ++be) {
-        double v = 1.0;
-        for (int k = 0; k < D; ++k) v *= (k == be) ? mt.D1[k][mm[k]][r[k]] : mt.B1[k][mm[k]][r[k]];
-        acc += swh[m] * sG[m][be][a] * v;
-      }
+      double g[D];
+      basis_grad<D>(c_ip, mt, m, ra, sW[m], sdW[m], g);
+      for (int be = 0; be < D; ++be) acc += swh[m] * sG[m][be][a] * g[be];
     }
     gpart[((size_t)t * mt.nact + ra) * D + a] = acc;
   }

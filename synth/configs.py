@@ -34,6 +34,7 @@ class Spline:
     degree: List[int]
     knots: List[np.ndarray]
     ctrl: np.ndarray
+    weights: Optional[np.ndarray] = None   # NURBS weights (n_ctrl,); None = B-spline
 
     @property
     def dim(self) -> int:
@@ -163,6 +164,48 @@ def macro_annulus(p, n_el, Ri=1.0, Ro=2.0, H=1.0):
     return Spline([p] * 3, U, ctrl)
 
 
+def _insert_knots_1d(U, p, Pw, new):
+    """Boehm knot insertion of the knots `new` into a 1D curve with homogeneous control
+    points Pw (n, dim+1): geometry is unchanged (placement only)."""
+    U = list(U)
+    Pw = [np.asarray(x, dtype=float) for x in Pw]
+    for u in new:
+        k = max(i for i in range(len(U) - 1) if U[i] <= u < U[i + 1])
+        Q = []
+        for i in range(len(Pw) + 1):
+            if i <= k - p:
+                Q.append(Pw[i])
+            elif i > k:
+                Q.append(Pw[i - 1])
+            else:
+                a = (u - U[i]) / (U[i + p] - U[i])
+                Q.append(a * Pw[i] + (1.0 - a) * Pw[i - 1])
+        Pw = Q
+        U.insert(k + 1, u)
+    return np.array(U), np.array(Pw)
+
+
+def macro_annulus_nurbs(n_el, Ri=1.0, Ro=2.0, H=1.0):
+    """EXACT quarter annulus swept along z as a NURBS (NEXT N4; the paper's torus of
+    §3.3.4 in miniature): angular direction = the rational quadratic 90° arc (weights
+    1, √2/2, 1) refined by knot insertion to n_el[0] elements; radial and z directions
+    polynomial (linear functions placed at the Greville abscissae, exact).  Same
+    orientation as macro_annulus (ξ0 along the arc from angle π/2 to 0)."""
+    p = 2
+    w = math.sqrt(0.5)
+    arc = np.array([[0.0, 1.0, 1.0], [w, w, w], [1.0, 0.0, 1.0]])   # homogeneous (w x, w y, w)
+    U0, arcw = _insert_knots_1d([0, 0, 0, 1, 1, 1], p, arc, [i / n_el[0] for i in range(1, n_el[0])])
+    U1 = open_uniform_knots(p, n_el[1])
+    U2 = open_uniform_knots(p, n_el[2])
+    r = Ri + (Ro - Ri) * greville(U1, p)
+    z = H * greville(U2, p)
+    idx = _index_grid([len(arcw), len(r), len(z)])
+    wts = arcw[idx[:, 0], 2]
+    xy = arcw[idx[:, 0], :2] / wts[:, None]
+    ctrl = np.stack([r[idx[:, 1]] * xy[:, 0], r[idx[:, 1]] * xy[:, 1], z[idx[:, 2]]], axis=1)
+    return Spline([p] * 3, [np.asarray(U0, float), U1, U2], ctrl, weights=wts)
+
+
 def macro_twist(p, n_el, length=4.0, twist=0.5 * math.pi):
     """Square 1x1 section extruded along x over `length`, rotated by twist*xi0
     (SURVEY.md §8(d), cfg4), control points = F(Greville)."""
@@ -236,7 +279,8 @@ def make_config(c: int, *, macro_amp: Optional[float] = None, macro_kind: Option
 
     Optional overrides build the exact-regime variants and small cases used by
     tests: macro_amp=0 (affine elements for box macros), macro_kind='shear',
-    a smaller n_el, or another q."""
+    macro_kind='nurbs' (cfg3/5: the exact rational quarter annulus), a smaller n_el,
+    or another q."""
     rng = np.random.default_rng([SEED_BASE, c])
     nu = 0.3
     if c == 1:
@@ -260,6 +304,8 @@ def make_config(c: int, *, macro_amp: Optional[float] = None, macro_kind: Option
         if macro_kind == "box":
             amp = 0.0 if macro_amp is None else macro_amp
             macro = macro_box(2, n_el, (4.0, 1.0, 1.0), rng, amp)
+        elif macro_kind == "nurbs":   # exact rational quarter annulus (NEXT N4)
+            macro = macro_annulus_nurbs(n_el)
         else:
             macro = macro_annulus(2, n_el)
         tile, ifaces = tile_lattice(2, 6)

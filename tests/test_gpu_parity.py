@@ -498,3 +498,44 @@ def test_volume_load_parity(c, kw):
             assert torch.equal(fk, f[z.row_begin:z.row_begin + z.n_rows])
         assert abs(vs - vol) < 1e-13 * abs(vol)
         assert (torch.linalg.norm(gs - grad) / torch.linalg.norm(grad)).item() < 1e-13
+
+
+# ---------------------------------------------------------------------------
+# NURBS macro map (NEXT N4): the exact rational quarter annulus
+
+@pytest.mark.parametrize("n_el", [(2, 2, 2), (3, 2, 1)])
+def test_nurbs_macro_parity(n_el):
+    """K, element matrices, the sensitivity and the volume (+ gradient) with a rational
+    macro map against the oracle (rational basis, quotient rule, complex step)."""
+    from paper_2107_09568_b200 import Assembler
+    from oracle import assemble as As, sensitivity as S, volume as V
+    from oracle.dofmap import DofMap, Pattern
+    from synth import make_config, draw_uv_seeded
+    prob = make_config(3, macro_kind="nurbs", n_el=n_el)
+    assert prob.macro.weights is not None
+    A = Assembler(prob)
+    s = A.sizes
+    d = 3
+    dev = torch.device("cuda")
+    ctrl = torch.tensor(prob.macro.ctrl, device=dev)
+    young = torch.tensor(prob.young, device=dev)
+    vals = torch.empty(s.nnz, dtype=torch.float64, device=dev)
+    local = torch.empty(s.n_local_rows * s.n_tiles * d * d, dtype=torch.float64, device=dev)
+    A.assemble(ctrl, young, prob.nu, vals, local)
+    dm = DofMap(prob)
+    tabs = As.Tables(prob)
+    pt = Pattern(prob, dm, tabs.pairs)
+    ref_vals, ref_local = As.assemble_lookup(prob, tabs, pt)
+    L = local.view(s.n_local_rows, s.n_tiles, d, d).permute(1, 0, 2, 3).cpu().numpy()
+    for t in range(prob.n_tiles):
+        assert rel(L[t], ref_local[t]) < TOL_ELEM, t
+    assert rel(vals.cpu().numpy(), ref_vals) < TOL_K
+    u, v = draw_uv_seeded(3, s.n_dof)
+    grad = torch.empty(s.n_macro_cp * d, dtype=torch.float64, device=dev)
+    A.sensitivity(ctrl, young, prob.nu, torch.tensor(u, device=dev), torch.tensor(v, device=dev), grad)
+    ref = S.sensitivity(prob, tabs, pt, u, v)
+    assert rel(grad.cpu().numpy().reshape(-1, d), ref) < TOL_SENS
+    gv = torch.empty_like(grad)
+    vol = A.volume(ctrl, gv)
+    assert abs(vol - V.volume_lookup(prob)) < 1e-13 * vol
+    assert rel(gv.cpu().numpy().reshape(-1, d), V.volume_gradient(prob)) < 1e-12
