@@ -539,3 +539,66 @@ def test_nurbs_macro_parity(n_el):
     vol = A.volume(ctrl, gv)
     assert abs(vol - V.volume_lookup(prob)) < 1e-13 * vol
     assert rel(gv.cpu().numpy().reshape(-1, d), V.volume_gradient(prob)) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# edge cases: one tile, lowest / highest degrees, ragged tile counts, degree-1 maps
+
+def _custom_problem(d, p, q, n_el, tile_el, pm=2, amp=0.05, tile_amp=0.08, seed=7):
+    from synth.configs import Problem, macro_box, tile_single
+    rng = np.random.default_rng(seed)
+    lengths = (2.0, 1.0, 1.0)[:d]
+    macro = macro_box(pm, n_el, lengths, rng, amp)
+    tile = tile_single(p, tile_el, rng, tile_amp)
+    prob = Problem(f"edge{d}{p}{q}", d, p, q, 0.3, macro, tile, [], None, tuple(n_el), 0)
+    prob.young = rng.uniform(0.5, 2.0, size=int(np.prod(n_el)))
+    return prob
+
+
+@pytest.mark.parametrize("d,p,q,n_el,tile_el,pm", [
+    (2, 2, 2, (1, 1), (3, 3), 2),          # a single tile
+    (3, 2, 2, (1, 1, 1), (2, 2, 2), 2),    # a single 3D tile
+    (2, 2, 0, (3, 2), (3, 3), 2),          # q = 0: n_k = d² (one K3 chunk, tail only)
+    (3, 2, 1, (3, 1, 2), (2, 2, 2), 2),    # q = 1
+    (2, 3, 4, (2, 2), (2, 3), 3),          # q = 4 (max), p = 3, (q+1)^d = 25
+    (3, 1, 2, (5, 3, 1), (3, 2, 2), 1),    # p = 1 tiles and a degree-1 macro map; 15 tiles (ragged N-block)
+    (2, 4, 3, (9, 2), (2, 2), 2),          # p = 4 (max), 18 tiles = one full 2D N-block
+])
+def test_edge_case_parity(d, p, q, n_el, tile_el, pm):
+    """K, element matrices and the sensitivity against the oracle on edge configurations."""
+    from paper_2107_09568_b200 import Assembler
+    from oracle import assemble as As, sensitivity as S
+    from oracle.dofmap import DofMap, Pattern
+    from synth import draw_uv_seeded
+    prob = _custom_problem(d, p, q, n_el, tile_el, pm)
+    A = Assembler(prob)
+    s = A.sizes
+    dev = torch.device("cuda")
+    ctrl = torch.tensor(prob.macro.ctrl, device=dev)
+    young = torch.tensor(prob.young, device=dev)
+    vals = torch.empty(s.nnz, dtype=torch.float64, device=dev)
+    local = torch.empty(s.n_local_rows * s.n_tiles * d * d, dtype=torch.float64, device=dev)
+    A.assemble(ctrl, young, prob.nu, vals, local)
+    dm = DofMap(prob)
+    tabs = As.Tables(prob)
+    pt = Pattern(prob, dm, tabs.pairs)
+    rp = torch.empty(s.n_dof + 1, dtype=torch.int64, device=dev)
+    ci = torch.empty(s.nnz, dtype=torch.int32, device=dev)
+    A.pattern(rp, ci)
+    assert np.array_equal(rp.cpu().numpy(), pt.row_ptr) and np.array_equal(ci.cpu().numpy(), pt.col_idx())
+    ref_vals, ref_local = As.assemble_lookup(prob, tabs, pt)
+    L = local.view(s.n_local_rows, s.n_tiles, d, d).permute(1, 0, 2, 3).cpu().numpy()
+    kappa = 35.0 ** d * 2.0 ** -52 * 4 if q >= 3 else 0.0   # κ(V1)^d rounding of the interpolation inverse
+    for t in range(prob.n_tiles):
+        assert rel(L[t], ref_local[t]) < max(TOL_ELEM, kappa), t
+    assert rel(vals.cpu().numpy(), ref_vals) < max(TOL_K, kappa)
+    u, v = draw_uv_seeded(11, s.n_dof)
+    grad = torch.empty(s.n_macro_cp * d, dtype=torch.float64, device=dev)
+    A.sensitivity(ctrl, young, prob.nu, torch.tensor(u, device=dev), torch.tensor(v, device=dev), grad)
+    ref = S.sensitivity(prob, tabs, pt, u, v)
+    assert rel(grad.cpu().numpy().reshape(-1, d), ref) < max(TOL_SENS, kappa)
+    y = torch.empty(s.n_dof, dtype=torch.float64, device=dev)
+    A.apply(ctrl, young, prob.nu, torch.tensor(u, device=dev), y)
+    import scipy.sparse as sp
+    Kref = sp.csr_matrix((ref_vals, pt.col_idx(), pt.row_ptr), shape=(s.n_dof, s.n_dof))
+    assert rel(y.cpu().numpy(), Kref @ u) < max(TOL_K, kappa)
