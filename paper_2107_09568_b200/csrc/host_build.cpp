@@ -635,7 +635,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     }
   }
   // K5a CTA height IGA_K3_BM κ rows
-  h.k5_rows = (h.kstride + IGA_K3_BM - 1) / IGA_K3_BM * IGA_K3_BM;
+  h.k5_rows = (h.kstride + IGA_K5_BM - 1) / IGA_K5_BM * IGA_K5_BM;
   if (k5x_smem_bytes(d, h.max_patch_ctrl) > 227 * 1024) { set_error("tile patch too large for the K5 shared-memory staging (%d control points)", h.max_patch_ctrl); return IGA_ELIMIT; }
 
   // ---- projection operator (R1: interpolation at the q+1 Gauss nodes) -------------

@@ -12,7 +12,8 @@
 #define IGA_MAXQ 4          // max interpolation degree
 #define IGA_MAXM 8          // max L2-projection points per direction (NEXT N2)
 #define IGA_KCHUNK 16       // GEMM k-chunk; k_stride is a multiple of it
-#define IGA_K3_BM 128       // K3 CTA rows (table rows)
+#define IGA_K3_BM 96        // K3 CTA rows (table rows): 6 MMA warps, 3 CTAs per SM
+#define IGA_K5_BM 128       // K5a CTA rows (κ)
 #define IGA_GEMM_BN 72      // K3/K5a CTA columns (tiles × d²): 8 tiles in 3D, 18 in 2D
 
 namespace iga {
@@ -92,7 +93,7 @@ struct Handle {
   // operand layouts (fragment-major, device_common.cuh fm_index)
   int64_t Mpad = 0;                  // rows of d_tabA (multiple of IGA_K3_BM)
   int64_t Npad = 0;                  // rows of d_coef (multiple of IGA_GEMM_BN)
-  int64_t k5_rows = 0;               // κ rows of d_tabAT (multiple of IGA_K3_BM)
+  int64_t k5_rows = 0;               // κ rows of d_tabAT (multiple of IGA_K5_BM)
   int64_t Kp = 0;                    // K5a reduction length: table rows, each patch padded to 16
   int max_patch_ctrl = 0;
   std::vector<int32_t> pcol;         // [n_patches+1] first padded column of each patch
@@ -116,7 +117,7 @@ struct Handle {
   // device buffers
   double *d_table = nullptr;     // [M][kstride] row-major (K1 output, accessor)
   double *d_tabA = nullptr;      // FM [Mpad][kstride], BR = IGA_K3_BM (K3 A operand)
-  double *d_tabAT = nullptr;     // FM [k5_rows][Kp], BR = IGA_K3_BM (K5a A operand)
+  double *d_tabAT = nullptr;     // FM [k5_rows][Kp], BR = IGA_K5_BM (K5a A operand)
   double *d_coef = nullptr;      // FM [Npad][kstride], BR = IGA_GEMM_BN (K3 B operand)
   double *d_side = nullptr;      // [n_slots][d*d] multi-contribution blocks (K3 -> K4)
   double *d_W = nullptr;         // [N][kstride]

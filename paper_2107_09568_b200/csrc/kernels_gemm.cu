@@ -36,8 +36,10 @@ constexpr int BK = IGA_KCHUNK;     // 16
 constexpr int BN = IGA_GEMM_BN;    // 72
 constexpr int NI = BN / 8;         // 9 DMMA column tiles per warp
 constexpr int MI = 2;              // 2 DMMA row tiles per warp (16 rows)
-constexpr int N_MMA_WARPS = 8;
-constexpr int BM = 16 * N_MMA_WARPS;                                        // 128
+constexpr int N_MMA_WARPS = 8;                                              // K5a
+constexpr int BM = 16 * N_MMA_WARPS;                                        // 128 (K5a κ rows)
+constexpr int K3_BM = IGA_K3_BM, K3_WARPS = K3_BM / 16;                     // K3: 96 rows, 6 MMA warps
+static_assert(BM == IGA_K5_BM, "K5a CTA rows");
 constexpr int K5_X_CHUNK_ = BN * BK;                                        // doubles per X chunk
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
@@ -99,14 +101,15 @@ __device__ __forceinline__ void store_row(double *p, double x0, double x1, doubl
 // refilled by the last warp to release a stage, 2 CTAs per SM (16 MMA warps: the DMMA
 // pipe stays fed while the co-resident CTA runs its epilogue).  After the main loop
 // the same warps stage the tile in shared memory and scatter it.
-constexpr int K3_STAGES = 4;
-constexpr int K3_A_CHUNK = BM * BK, K3_B_CHUNK = BN * BK;             // doubles
+constexpr int K3_STAGES = 3;
+constexpr int K3_A_CHUNK = K3_BM * BK, K3_B_CHUNK = BN * BK;          // doubles
 constexpr int K3_CROW = BN + 1;                                        // epilogue pitch (odd)
-constexpr int K3_THREADS = 32 * N_MMA_WARPS;
-constexpr size_t K3_OFF_BAR = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
+constexpr int K3_THREADS = 32 * K3_WARPS;
+constexpr size_t K3_STAGE_BYTES = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
+constexpr size_t K3_EPI_BYTES = sizeof(double) * (size_t)K3_BM * (K3_CROW + 4 * 3);   // staging + apply runs
+constexpr size_t K3_OFF_BAR = K3_STAGE_BYTES > K3_EPI_BYTES ? K3_STAGE_BYTES : K3_EPI_BYTES;
 constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int));
-static_assert(sizeof(double) * BM * (K3_CROW + 4 * 3) <= K3_OFF_BAR, "epilogue staging must fit in the stages");
-static_assert(BM == IGA_K3_BM, "K3 CTA rows");
+static_assert(K3_THREADS == 2 * K3_BM, "epilogue: two threads (tile halves) per row");
 
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
@@ -122,7 +125,7 @@ struct ApplyArgs {
 // EPI = 0: local[M][N] (nzdata, Eq. 58) ; EPI = 1: fused CSR scatter (+ side slots);
 // EPI = 2: matrix-free apply y = K^π u (Eq. 74): block products summed into partial slots
 template <int D, int EPI>
-__global__ void __launch_bounds__(K3_THREADS, 2)
+__global__ void __launch_bounds__(K3_THREADS, 3)
 k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int64_t M,
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
@@ -133,10 +136,10 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K3_OFF_BAR);
   int *released = reinterpret_cast<int *>(full + K3_STAGES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t mb = blockIdx.x, nb = blockIdx.y, m0 = mb * BM, t0 = nb * TPC;
+  const int64_t mb = blockIdx.x, nb = blockIdx.y, m0 = mb * K3_BM, t0 = nb * TPC;
   const double *gA = tabA + mb * nkc * K3_A_CHUNK, *gB = coef + nb * nkc * K3_B_CHUNK;
   // epilogue ownership: row er of the tile, tiles [et0, et0 + TPT) of the CTA
-  const int er = tid & (BM - 1), et0 = (tid >> 7) * TPT;
+  const int er = tid % K3_BM, et0 = (tid / K3_BM) * TPT;
   const int64_t r = m0 + er;
   if (tid == 0) {
     for (int s = 0; s < K3_STAGES; ++s) {
@@ -171,7 +174,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     __syncwarp();
     if (lane == 0) {   // the last warp to release a stage refills it
       __threadfence_block();
-      if (atomicAdd(&released[st], 1) == N_MMA_WARPS - 1) {
+      if (atomicAdd(&released[st], 1) == K3_WARPS - 1) {
         released[st] = 0;
         __threadfence_block();
         if (kc + K3_STAGES < nkc) produce(kc + K3_STAGES);
@@ -195,7 +198,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) {
-        const int rr = warp * 16 + mi * 8 + fr, c = ni * 8 + 2 * fc;
+        const int rr = warp * 16 + mi * 8 + fr, c = ni * 8 + 2 * fc;   // K3_WARPS × 16 rows
         sC[rr * K3_CROW + c] = acc[mi][ni][0];
         sC[rr * K3_CROW + c + 1] = acc[mi][ni][1];
       }
@@ -203,7 +206,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   __syncthreads();
   if (EPI == 0) {
     const int64_t N = n_tiles * DD, n0 = nb * BN;
-    for (int i = tid; i < BM * BN; i += K3_THREADS) {
+    for (int i = tid; i < K3_BM * BN; i += K3_THREADS) {
       const int rr = i / BN, c = i % BN;
       const int64_t gr = m0 + rr, gc = n0 + c;
       if (gr < M && gc < N) out[gr * N + gc] = sC[rr * K3_CROW + c];
@@ -214,8 +217,8 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     // thread e: c1 = L u_J (diagonal: L_sym u_I) of row e into s1, and c2 = Lᵀ u_I of row
     // tperm[e] into s2 (position e of the (B, A) order); the first thread of each run of
     // equal A (s1) / equal B (s2) sums its run in order into the run's partial slot.
-    double *s1 = sC + BM * K3_CROW, *s2 = s1 + 2 * BM * D;
-    const int half = tid >> 7;
+    double *s1 = sC + K3_BM * K3_CROW, *s2 = s1 + 2 * K3_BM * D;
+    const int half = tid / K3_BM;
     const int et = tperm[m0 + er];
     const int64_t rt = m0 + et;
     const bool live = r < M, live_t = rt < M;
@@ -223,7 +226,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
     const int len1 = ap.g1len[m0 + er], len2 = ap.g2len[m0 + er];
     const int64_t sl1 = ap.g1slot[m0 + er], sl2 = ap.g2slot[m0 + er];
-    double *my1 = s1 + (half * BM + er) * D, *my2 = s2 + (half * BM + er) * D;
+    double *my1 = s1 + (half * K3_BM + er) * D, *my2 = s2 + (half * K3_BM + er) * D;
     for (int k = 0; k < TPT; ++k) {
       const int tl = et0 + k;
       const int64_t t = t0 + tl;
@@ -349,7 +352,7 @@ template <int D, int EPI>
 static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, ApplyArgs ap = ApplyArgs{}) {
   cudaError_t e = cudaFuncSetAttribute(k3_contract<D, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM);
   if (e) return e;
-  dim3 grid((unsigned)(h.Mpad / BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
+  dim3 grid((unsigned)(h.Mpad / K3_BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   k3_contract<D, EPI><<<grid, K3_THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.kstride / BK, (h.nk + 3) / 4, h.M,
                                                         h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,

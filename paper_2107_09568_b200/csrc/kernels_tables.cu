@@ -232,7 +232,7 @@ __global__ void k1_pack(const double *__restrict__ table, int64_t M, int nk, int
 cudaError_t launch_pack_tables(const Handle &h, cudaStream_t s) {
   const int64_t n = h.M * h.nk;
   k1_pack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.d_table, h.M, h.nk, h.kstride, h.d_k5_col, h.d_tabA,
-                                                      h.kstride / IGA_KCHUNK, h.d_tabAT, IGA_K3_BM,
+                                                      h.kstride / IGA_KCHUNK, h.d_tabAT, IGA_K5_BM,
                                                       (int)(h.Kp / IGA_KCHUNK));
   return cudaGetLastError();
 }
