@@ -38,7 +38,7 @@ constexpr int NI = BN / 8;         // 9 DMMA column tiles per warp
 constexpr int MI = 2;              // 2 DMMA row tiles per warp (16 rows)
 constexpr int N_MMA_WARPS = 8;                                              // K5a
 constexpr int BM = 16 * N_MMA_WARPS;                                        // 128 (K5a κ rows)
-constexpr int K3_BM = IGA_K3_BM, K3_WARPS = K3_BM / 16;                     // K3: 96 rows, 6 MMA warps
+constexpr int K3_BM = IGA_K3_BM, K3_WARPS = K3_BM / 16;                     // K3: 64 rows, 4 MMA warps
 static_assert(BM == IGA_K5_BM, "K5a CTA rows");
 constexpr int K5_X_CHUNK_ = BN * BK;                                        // doubles per X chunk
 
@@ -97,10 +97,11 @@ __device__ __forceinline__ void store_row(double *p, double x0, double x1, doubl
 }
 
 // ---------------------------------------------------------------------------------
-// K3: one CTA per 128×72 output tile, 8 MMA warps of 16×72, 4-stage bulk-copy ring
-// refilled by the last warp to release a stage, 2 CTAs per SM (16 MMA warps: the DMMA
-// pipe stays fed while the co-resident CTA runs its epilogue).  After the main loop
-// the same warps stage the tile in shared memory and scatter it.
+// K3: one CTA per 64×72 output tile, 4 MMA warps of 16×72, 3-stage bulk-copy ring
+// refilled by the last warp to release a stage, 4 CTAs per SM (16 MMA warps: the DMMA
+// pipe stays fed while co-resident CTAs run their epilogues; measured 128-row/2-CTA
+// 22.1 ms, 96-row/3-CTA 21.8 ms, 64-row/4-CTA 21.3 ms at cfg5).  After the main loop the
+// same warps stage the tile in shared memory and scatter it.
 constexpr int K3_STAGES = 3;
 constexpr int K3_A_CHUNK = K3_BM * BK, K3_B_CHUNK = BN * BK;          // doubles
 constexpr int K3_CROW = BN + 1;                                        // epilogue pitch (odd)
@@ -125,7 +126,7 @@ struct ApplyArgs {
 // EPI = 0: local[M][N] (nzdata, Eq. 58) ; EPI = 1: fused CSR scatter (+ side slots);
 // EPI = 2: matrix-free apply y = K^π u (Eq. 74): block products summed into partial slots
 template <int D, int EPI>
-__global__ void __launch_bounds__(K3_THREADS, 3)
+__global__ void __launch_bounds__(K3_THREADS, 4)
 k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int64_t M,
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
