@@ -69,16 +69,37 @@ def bernstein_1d(q: int, x):
     return np.stack([comb(q, k) * x ** k * (1 - x) ** (q - k) for k in range(q + 1)])
 
 
-def bernstein(q: int, xi):
-    """Multivariate Bernstein N_C(ξ) = Π_k B_{c_k}^q(ξ_k), C = c0 + (q+1)(c1 + (q+1)c2)
-    (direction-0 fastest).  xi: (n_pts, d) -> (n_pi, n_pts)."""
+def qvec(q, d):
+    """Per-direction degrees (q_0, …, q_{d-1}) of the projection space: an int is the
+    isotropic Q_q, a sequence the anisotropic space of the twist example, p_π = 3, 3, 4
+    (§3.3.4)."""
+    if np.ndim(q) == 0:
+        return (int(q),) * d
+    q = tuple(int(x) for x in q)
+    if len(q) != d:
+        raise ValueError(f"q has {len(q)} entries for d = {d}")
+    return q
+
+
+def n_pi(q, d):
+    """Number of Bernstein functions Π_k (q_k + 1) (Eq. 21)."""
+    return int(np.prod([x + 1 for x in qvec(q, d)]))
+
+
+def bernstein(q, xi):
+    """Multivariate Bernstein N_C(ξ) = Π_k B_{c_k}^{q_k}(ξ_k) (Eq. 21), C = c0 +
+    (q0+1)(c1 + (q1+1)c2) (direction-0 fastest); q an int or per-direction degrees.
+    xi: (n_pts, d) -> (n_pi, n_pts)."""
     xi = np.asarray(xi)
     d = xi.shape[1]
-    B = [bernstein_1d(q, xi[:, k]) for k in range(d)]
-    n1 = q + 1
+    qv = qvec(q, d)
+    B = [bernstein_1d(qv[k], xi[:, k]) for k in range(d)]
     out = []
-    for C in range(n1 ** d):
-        c = [(C // n1 ** k) % n1 for k in range(d)]
+    for C in range(n_pi(qv, d)):
+        c, r = [], C
+        for k in range(d):
+            c.append(r % (qv[k] + 1))
+            r //= qv[k] + 1
         v = np.ones(xi.shape[0], dtype=xi.dtype)
         for k in range(d):
             v = v * B[k][c[k]]

@@ -23,7 +23,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .bspline import basis_1d, bernstein, elements_of, gauss_01, multi_index
+from .bspline import basis_1d, bernstein, elements_of, gauss_01, multi_index, qvec
 
 
 def lame(E, nu):
@@ -202,14 +202,9 @@ def A_tensor(J, lam, mu):
 # interpolation onto Q_q (reading R1)
 # --------------------------------------------------------------------------
 def interp_nodes(q, d):
-    """(q+1)^d tensor Gauss–Legendre nodes on [0,1]^d, direction-0 fastest, ascending."""
-    x, _ = gauss_01(q + 1)
-    n1 = q + 1
-    pts = np.zeros((n1 ** d, d))
-    for m in range(n1 ** d):
-        for k in range(d):
-            pts[m, k] = x[(m // n1 ** k) % n1]
-    return pts
+    """Π_k (q_k+1) tensor Gauss–Legendre nodes on [0,1]^d (q_k+1 per direction k),
+    direction-0 fastest, ascending; q an int or per-direction degrees."""
+    return projection_nodes(tuple(x + 1 for x in qvec(q, d)), d)[0]
 
 
 def interpolate(samples, q, d):
@@ -224,21 +219,27 @@ def interpolate(samples, q, d):
 
 
 def projection_nodes(m, d):
-    """m^d tensor Gauss–Legendre nodes on [0,1]^d (direction-0 fastest) and weights."""
-    x, w1 = gauss_01(m)
-    pts = np.zeros((m ** d, d))
-    w = np.ones(m ** d)
-    for i in range(m ** d):
+    """Tensor Gauss–Legendre nodes on [0,1]^d with m_k points in direction k (m an int or
+    per-direction counts; direction-0 fastest) and their weights."""
+    mv = qvec(m, d)
+    rules = [gauss_01(mk) for mk in mv]
+    n = int(np.prod(mv))
+    pts = np.zeros((n, d))
+    w = np.ones(n)
+    for i in range(n):
+        r = i
         for k in range(d):
-            pts[i, k] = x[(i // m ** k) % m]
-            w[i] *= w1[(i // m ** k) % m]
+            pts[i, k] = rules[k][0][r % mv[k]]
+            w[i] *= rules[k][1][r % mv[k]]
+            r //= mv[k]
     return pts, w
 
 
 def project_l2(samples, q, d, m):
     """L2 projection onto Q_q (Eqs. 23-24): M_π d = r_π with [M_π]_kl = ∫ N_k N_l and
-    (r_π)_k = ∫ N_k f, both integrated by the m-point Gauss rule per direction; samples
-    = f at projection_nodes(m, d).  Plain definition (full tensor mass matrix)."""
+    (r_π)_k = ∫ N_k f, both integrated by the m-point Gauss rule per direction (q, m ints
+    or per-direction); samples = f at projection_nodes(m, d).  Plain definition (full
+    tensor mass matrix)."""
     X, w = projection_nodes(m, d)
     N = bernstein(q, X)                          # (C, m^d)
     Mpi = (N * w) @ N.T
@@ -254,16 +255,35 @@ def tile_coefficients(prob, ctrl, t, E=None, route=A_closed, m=None):
     m (default prob.n_proj, 0 -> q+1): Gauss points per direction of the projection; q+1
     is interpolation at the Gauss nodes (reading R1), larger m the L2 projection of
     Eqs. 23-24 with that rule (NEXT N2).  Raises if det J <= 0 at a node (reading R5)."""
-    d, q = prob.d, prob.q
-    m = m or getattr(prob, "n_proj", 0) or q + 1
+    d = prob.d
     E = prob.young[t] if E is None else E
     lam, mu = lame(E, prob.nu)
-    X = interp_nodes(q, d) if m == q + 1 else projection_nodes(m, d)[0]
-    J = macro_jacobian(prob.macro, ctrl, t, X)
-    if np.any(np.real(np.linalg.det(J)) <= 0):
-        raise ValueError(f"degenerate macro element: tile {t}")
-    A = route(J, lam, mu)                       # (m, i, j, a, b)
-    return interpolate(A, q, d) if m == q + 1 else project_l2(A, q, d, m)
+    return project_field(lambda X: route(macro_jacobian(prob.macro, ctrl, t, X), lam, mu), prob.q, d,
+                         m or getattr(prob, "n_proj", 0), check_tile=t, ctrl=ctrl, macro=prob.macro)
+
+
+def projection_points(q, d, m=0):
+    """m per direction: 0 -> q_k+1 (interpolation, R1); else m (>= q_k+1) points per
+    direction for every k.  Returns (per-direction counts, interpolation?)."""
+    qv = qvec(q, d)
+    mv = tuple(x + 1 for x in qv) if not m else qvec(m, d)
+    if any(mk < qk + 1 for mk, qk in zip(mv, qv)):
+        raise ValueError(f"projection points {mv} < q+1 = {tuple(x + 1 for x in qv)}")
+    return mv, all(mk == qk + 1 for mk, qk in zip(mv, qv))
+
+
+def project_field(f, q, d, m=0, check_tile=None, ctrl=None, macro=None):
+    """Π^H f (Eq. 20) for f evaluated at sample points X (n, d) -> (n, ...): interpolation
+    at the Gauss nodes when every m_k = q_k+1 (R1), else the Gauss-discretised L2
+    projection of Eqs. 23-24.  Raises on det J <= 0 at a node of tile check_tile (R5)."""
+    mv, interp = projection_points(q, d, m)
+    X = projection_nodes(mv, d)[0]
+    if check_tile is not None:
+        J = macro_jacobian(macro, ctrl, check_tile, X)
+        if np.any(np.real(np.linalg.det(J)) <= 0):
+            raise ValueError(f"degenerate macro element: tile {check_tile}")
+    A = f(X)
+    return interpolate(A, q, d) if interp else project_l2(A, q, d, mv)
 
 
 def field_from_coefficients(coef, q, xi):

@@ -17,7 +17,7 @@ import itertools
 
 import numpy as np
 
-from .bspline import bernstein, elements_of, gauss_01, tensor_basis
+from .bspline import bernstein, elements_of, gauss_01, n_pi, tensor_basis
 
 
 def patch_spans(spline):
@@ -89,11 +89,12 @@ def tile_point_data(spline, spans, n_g):
 
 
 def lookup_table(spline, q, n_g):
-    """mat𝔎 (n_nz × n_π d²) for one tile patch (Eqs. 52, 57)."""
+    """mat𝔎 (n_nz × n_π d²) for one tile patch (Eqs. 52, 57); q an int or per-direction
+    degrees of the projection space (n_π = Π_k (q_k+1))."""
     d = spline.dim
     pairs = icoo(spline)
     row_of = {(int(a), int(b)): r for r, (a, b) in enumerate(pairs)}
-    npi = (q + 1) ** d
+    npi = n_pi(q, d)
     T = np.zeros((len(pairs), d, d, npi))
     for s in patch_spans(spline):
         act = active_functions(spline, s)

@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import macro as M
-from .bspline import bernstein, tensor_basis
+from .bspline import bernstein, n_pi, tensor_basis
 from .tables import gauss_points_span, patch_spans
 
 H = 1e-30
@@ -48,7 +48,7 @@ def load_tables(prob):
     in the tile-local control-point order."""
     out = []
     for sp in prob.tile:
-        F = np.zeros((sp.ctrl.shape[0], (prob.q + 1) ** prob.d))
+        F = np.zeros((sp.ctrl.shape[0], n_pi(prob.q, prob.d)))
         for s in patch_spans(sp):
             R, xi, DT, w = _span_data(sp, s, prob.n_gauss)
             F += (R * (w * DT)) @ bernstein(prob.q, xi).T
@@ -59,13 +59,8 @@ def load_tables(prob):
 def det_coefficients(prob, ctrl, t, m=None):
     """d^(t): projection coefficients of |det J_ℳ(t)| (Eq. 15; interpolation at the
     q+1 Gauss nodes, reading R1, or the m-point L2 projection of Eqs. 23-24)."""
-    d, q = prob.d, prob.q
-    m = m or getattr(prob, "n_proj", 0) or q + 1
-    X = M.interp_nodes(q, d) if m == q + 1 else M.projection_nodes(m, d)[0]
-    det = np.linalg.det(M.macro_jacobian(prob.macro, ctrl, t, X))
-    if np.any(np.real(det) <= 0):
-        raise ValueError(f"degenerate macro element: tile {t}")
-    return M.interpolate(det, q, d) if m == q + 1 else M.project_l2(det, q, d, m)
+    return M.project_field(lambda X: np.linalg.det(M.macro_jacobian(prob.macro, ctrl, t, X)), prob.q, prob.d,
+                           m or getattr(prob, "n_proj", 0), check_tile=t, ctrl=ctrl, macro=prob.macro)
 
 
 def volume_lookup(prob, ctrl=None, tiles=None, th=None):

@@ -66,7 +66,7 @@ class Problem:
     name: str
     d: int
     p: int                      # analysis (tile) degree
-    q: int                      # interpolation degree p_pi
+    q: "int | Tuple[int, ...]"  # projection degree p_pi: isotropic, or per direction
     nu: float
     macro: Spline               # macro map F (Eq. 4)
     tile: List[Spline]          # reference tile patches (Eq. 3)
@@ -82,8 +82,10 @@ class Problem:
 
     @property
     def n_gauss(self) -> int:
-        """DESIGN.md reading R3: n_g = p + ceil((q+1)/2) per direction per span."""
-        return self.p + (self.q + 2) // 2
+        """DESIGN.md reading R3: n_g = p + ceil((q+1)/2) per direction per span (q = the
+        largest per-direction degree when anisotropic)."""
+        q = self.q if np.ndim(self.q) == 0 else max(self.q)
+        return self.p + (q + 2) // 2
 
 
 # --------------------------------------------------------------------------
@@ -274,13 +276,13 @@ def tile_lattice(p, n_len, radius=0.15, n_sec=2):
 # configs
 # --------------------------------------------------------------------------
 def make_config(c: int, *, macro_amp: Optional[float] = None, macro_kind: Optional[str] = None,
-                n_el: Optional[Tuple[int, ...]] = None, q: Optional[int] = None) -> Problem:
+                n_el: Optional[Tuple[int, ...]] = None, q=None) -> Problem:
     """Config c in 1..5 (1-based, BASELINE.json configs[c-1]).
 
     Optional overrides build the exact-regime variants and small cases used by
     tests: macro_amp=0 (affine elements for box macros), macro_kind='shear',
     macro_kind='nurbs' (cfg3/5: the exact rational quarter annulus), a smaller n_el,
-    or another q."""
+    or another q (an int, or per-direction degrees as in the twist's p_pi = 3, 3, 4)."""
     rng = np.random.default_rng([SEED_BASE, c])
     nu = 0.3
     if c == 1:

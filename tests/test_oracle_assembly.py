@@ -48,10 +48,27 @@ def test_shear_macro_exact_at_q2_not_q1(c, kw, oracle_problem):
     assert rel(local1, std1) > 1e-8
 
 
-@pytest.mark.parametrize("c,t", [(1, 5), (3, 0)])
-def test_lookup_equals_quadrature_with_interpolated_field(c, t, oracle_problem):
-    """For ANY F, K^π equals the tile quadrature of Eq. 49 with Π_qĀ in place of Ā."""
-    kw = dict(n_el=(2, 1, 1)) if c == 3 else {}
+@pytest.mark.parametrize("c,kw", [(1, dict(macro_kind="shear", q=(0, 2))),
+                                  (2, dict(macro_kind="shear", n_el=(2, 2, 1), q=(0, 2, 0)))])
+def test_shear_macro_exact_at_anisotropic_q(c, kw, oracle_problem):
+    """The shear Ā depends on ξ1 only, quadratically: exact in the anisotropic space
+    Q_{0,2(,0)} (n_π = 3) and not in Q_{2,1(,2)}."""
+    ob = oracle_problem(c, **kw)
+    _, local = As.assemble_lookup(ob["prob"], ob["tabs"], ob["pattern"])
+    assert rel(local, standard_all(ob)) < 1e-13
+    q_bad = (2, 1) if c == 1 else (2, 1, 2)
+    ob1 = oracle_problem(c, **dict(kw, q=q_bad))
+    _, local1 = As.assemble_lookup(ob1["prob"], ob1["tabs"], ob1["pattern"])
+    assert rel(local1, standard_all(ob1)) > 1e-8
+
+
+@pytest.mark.parametrize("c,t,q", [(1, 5, None), (3, 0, None), (1, 6, (3, 1)), (2, 3, (1, 2, 3))])
+def test_lookup_equals_quadrature_with_interpolated_field(c, t, q, oracle_problem):
+    """For ANY F, K^π equals the tile quadrature of Eq. 49 with Π_qĀ in place of Ā
+    (also for anisotropic projection spaces)."""
+    kw = dict(n_el=(2, 1, 1)) if c == 3 else (dict(n_el=(2, 2, 1)) if c == 2 else {})
+    if q is not None:
+        kw["q"] = q
     ob = oracle_problem(c, **kw)
     prob, tabs = ob["prob"], ob["tabs"]
     local = As.local_lookup(prob, tabs, prob.macro.ctrl, [t])[0]

@@ -44,8 +44,9 @@ def exact_affine_table(p, q, o, s):
     """𝔎 for the single-element degree-p tile 𝒯(θ) = o + s⊙θ, exactly (Eq. 52 by
     change of variables: ∂_ξk = (1/s_k) ∂_θk, dξ = Π s_k dθ)."""
     d = len(o)
-    n1, q1 = p + 1, q + 1
-    nT, npi = n1 ** d, q1 ** d
+    qv = (q,) * d if np.ndim(q) == 0 else tuple(q)   # per-direction degrees (P:524)
+    n1 = p + 1
+    nT, npi = n1 ** d, int(np.prod([x + 1 for x in qv]))
     pairs = [(A, B) for A in range(nT) for B in range(A, nT)]
     T = np.zeros((len(pairs), d, d, npi))
     for r, (A, B) in enumerate(pairs):
@@ -54,7 +55,10 @@ def exact_affine_table(p, q, o, s):
         for i in range(d):
             for j in range(d):
                 for C in range(npi):
-                    c = [(C // q1 ** k) % q1 for k in range(d)]
+                    c, rem = [], C
+                    for k in range(d):
+                        c.append(rem % (qv[k] + 1))
+                        rem //= qv[k] + 1
                     val = Fr(1)
                     for k in range(d):
                         fa = bern(p, a[k])
@@ -63,7 +67,7 @@ def exact_affine_table(p, q, o, s):
                             fa = [x / s[k] for x in pder(fa)]
                         if k == j:
                             fb = [x / s[k] for x in pder(fb)]
-                        val *= s[k] * pint01(pmul(pmul(fa, fb), bern(q, c[k], o[k], s[k])))
+                        val *= s[k] * pint01(pmul(pmul(fa, fb), bern(qv[k], c[k], o[k], s[k])))
                     T[r, i, j, C] = float(val)
     return T.reshape(len(pairs), -1)
 
@@ -72,6 +76,9 @@ def exact_affine_table(p, q, o, s):
     (2, 2, (Fr(1, 4), Fr(1, 10)), (Fr(1, 2), Fr(3, 5))),
     (2, 1, (Fr(0), Fr(1, 5)), (Fr(1), Fr(2, 5))),
     (1, 1, (Fr(1, 8), Fr(0), Fr(1, 4)), (Fr(3, 4), Fr(1), Fr(1, 2))),
+    # anisotropic projection spaces (the twist's p_π = 3, 3, 4)
+    (2, (1, 3), (Fr(1, 4), Fr(1, 10)), (Fr(1, 2), Fr(3, 5))),
+    (1, (0, 2, 1), (Fr(1, 8), Fr(0), Fr(1, 4)), (Fr(3, 4), Fr(1), Fr(1, 2))),
 ])
 def test_table_exact_rational_affine_tile(p, q, o, s):
     d = len(o)
@@ -80,7 +87,7 @@ def test_table_exact_rational_affine_tile(p, q, o, s):
     mesh = np.meshgrid(*g, indexing="ij")
     ctrl = np.stack([m.transpose(*reversed(range(d))).reshape(-1) for m in mesh], axis=1)
     spline = Spline([p] * d, [U] * d, ctrl)
-    n_g = p + (q + 2) // 2
+    n_g = p + (max(np.atleast_1d(q)) + 2) // 2
     T, pairs = lookup_table(spline, q, n_g)
     ref = exact_affine_table(p, q, o, s)
     assert np.allclose(T, ref, rtol=0, atol=2e-15 * np.abs(ref).max())
@@ -93,8 +100,8 @@ def perturbed_tile(d, p, n_el, amp, seed):
 
 
 def _check_row_sums_and_symmetry(spline, q, d):
-    T, pairs = lookup_table(spline, q, spline.degree[0] + (q + 2) // 2)
-    npi = (q + 1) ** d
+    T, pairs = lookup_table(spline, q, spline.degree[0] + (max(np.atleast_1d(q)) + 2) // 2)
+    npi = int(np.prod([x + 1 for x in ((q,) * d if np.ndim(q) == 0 else q)]))
     T4 = T.reshape(len(pairs), d, d, npi)
     scale = np.abs(T).max()
     nT = spline.n_ctrl
@@ -114,6 +121,7 @@ def _check_row_sums_and_symmetry(spline, q, d):
 def test_row_sums_and_symmetry_perturbed_tiles():
     _check_row_sums_and_symmetry(perturbed_tile(2, 2, (4, 4), 0.10, 3), 2, 2)
     _check_row_sums_and_symmetry(perturbed_tile(3, 2, (2, 2, 2), 0.08, 4), 2, 3)
+    _check_row_sums_and_symmetry(perturbed_tile(3, 2, (2, 2, 2), 0.08, 4), (1, 3, 2), 3)
 
 
 def test_row_sums_lattice_patch():
@@ -131,6 +139,8 @@ def test_sum_over_C_equals_q0_table():
     assert np.array_equal(pairs, pairs0)
     Tq4 = Tq.reshape(len(pairs), 4, 9)
     assert np.allclose(Tq4.sum(-1), T0, rtol=0, atol=1e-14 * np.abs(T0).max())
+    Ta, _ = lookup_table(tile, (3, 1), n_g)            # anisotropic Q_{3,1}: still Σ_C N_C ≡ 1
+    assert np.allclose(Ta.reshape(len(pairs), 4, 8).sum(-1), T0, rtol=0, atol=1e-14 * np.abs(T0).max())
 
 
 @pytest.mark.parametrize("n,p,expect", [(6, 2, 15), (4, 2, 9), (7, 3, 22)])
