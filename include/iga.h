@@ -112,6 +112,8 @@ typedef struct {
   int64_t n_tiles_owned;  /* tiles of the slab (the sensitivity's partial sum) */
   int64_t row_begin;      /* first CSR row (global scalar row = node*d + a) of this handle */
   int64_t n_rows;         /* CSR rows of this handle: row_ptr has n_rows + 1 entries */
+  int32_t q_dir[3];       /* projection degree per direction (q above = the largest; unused dirs 0) */
+  int32_t m_dir[3];       /* projection sample points per direction (q_dir+1: interpolation) */
 } iga_sizes;
 
 /* ---------------------------------------------------------------------------
@@ -136,6 +138,16 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches,
                             const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
                             const iga_shard *shard, void *stream, iga_handle **out);
 
+/* iga_build_tables_q — iga_build_tables with one projection degree per direction, q[k]
+ * for k < d (the anisotropic spaces of §3.3.4, e.g. the twist's p_π = 3, 3, 4, P:524;
+ * SURVEY §8(f) N2): n_π = Π_k (q_k+1) Bernstein functions N_C(ξ) = Π_k B_{c_k}^{q_k}(ξ_k),
+ * C = c0 + (q0+1)(c1 + (q1+1)c2).  n_gauss = 0 takes R3 with the largest q_k.  Otherwise
+ * identical (iga_build_tables(…, q, …) == iga_build_tables_q(…, {q, q, q}, …)). */
+iga_status iga_build_tables_q(const iga_spline *tile_patches, int32_t n_patches,
+                              const iga_interface *interfaces, int32_t n_interfaces,
+                              const iga_spline *macro_topology, const int32_t *q, int32_t n_gauss,
+                              const iga_shard *shard, void *stream, iga_handle **out);
+
 /* iga_build_topology — host-only variant of iga_build_tables: validation, I_coo,
  * DofMap and the CSR pattern, no device work and no tables.  The handle answers
  * iga_get_sizes / iga_get_pattern (host pointers) / iga_get_block_map /
@@ -145,6 +157,10 @@ iga_status iga_build_topology(const iga_spline *tile_patches, int32_t n_patches,
                               const iga_interface *interfaces, int32_t n_interfaces,
                               const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
                               const iga_shard *shard, iga_handle **out);
+iga_status iga_build_topology_q(const iga_spline *tile_patches, int32_t n_patches,
+                                const iga_interface *interfaces, int32_t n_interfaces,
+                                const iga_spline *macro_topology, const int32_t *q, int32_t n_gauss,
+                                const iga_shard *shard, iga_handle **out);
 
 /* ---------------------------------------------------------------------------
  * iga_assemble — form K^π (Eq. 50) into CSR values: the hot path (§3.2.4 steps 1-4).
@@ -226,15 +242,46 @@ iga_status iga_interpolate(const iga_handle *h, const double *macro_ctrl, const 
 
 /* iga_set_projection — the projection Π^H of the macro field (Eq. 20) onto Q_q: the L2
  * projection of Eqs. 23-24 (and 42) with its mass matrix and right-hand side integrated
- * by an m-point Gauss rule per direction, m >= q+1.  m = q+1 (the
- * default) is interpolation at the (q+1)^d Gauss nodes (reading R1, equal to that
- * projection); larger m converge to the exact L2 projection (exact once 2m-1 >= q + the
- * degree of Ā's polynomial part).  Applies to iga_assemble / iga_sensitivity /
- * iga_interpolate / iga_apply; the tables do not depend on m.
- * Errors: EINVAL (m < q+1 or m > 8), ELIMIT (per-tile staging exceeds shared memory,
- * e.g. m > 5 in 3D). */
+ * by an m-point Gauss rule per direction, m >= q_k+1 for every k.
+ * m = 0 (or m = q+1 for isotropic q, the default) is interpolation at the q_k+1 Gauss
+ * nodes of each direction (reading R1, equal to that projection); larger m converge to the
+ * exact L2 projection (exact once 2m-1 >= q + the degree of Ā's polynomial part).  Applies
+ * to iga_assemble / iga_sensitivity / iga_interpolate / iga_apply / iga_volume /
+ * iga_load_vector; the tables do not depend on m.  iga_get_projection returns m as set
+ * (q+1 for isotropic interpolation, 0 for anisotropic interpolation).
+ * Errors: EINVAL (0 < m < q_k+1 or m > 8), ELIMIT (per-tile staging exceeds shared
+ * memory, e.g. m > 5 in 3D). */
 iga_status iga_set_projection(iga_handle *h, int32_t m);
 iga_status iga_get_projection(const iga_handle *h, int32_t *m);
+
+/* ---------------------------------------------------------------------------
+ * iga_projection_error — the a-priori projection error of Eq. 59, evaluated "by a
+ * simple sampling-based approach ... a priori to the assembly":
+ *   e_t = max_{ξ ∈ S} ‖Ā^(t)(ξ) − Π^H Ā^(t)(ξ)‖_F / ‖Ā^(t)(ξ)‖_F,   E_proj = max_t e_t,
+ * ‖·‖_F over all d⁴ components, S = n_samples equispaced points per direction of the
+ * element-local cube, endpoints included (reading R18); Ā ∝ E, so E does not enter.
+ * No tables are needed: this is the a-priori step of the degree selection.
+ *  macro      the macro map F with control points (and weights for NURBS) [host].
+ *  q          d projection degrees (0..4).   m_extra >= 0: q_k+1+m_extra Gauss points per
+ *             direction (0 = interpolation, R1; else the L2 projection of Eqs. 23-24).
+ *  nu         Poisson ratio.   n_samples in [2, 8] (0 = 8).
+ *  e_max      [host] E_proj.   e_tile [any] optional n_tiles doubles: e_t per tile.
+ * Device work: one CTA per tile (K2's passes, then evaluation passes at S); fixed order,
+ * exact max.  Errors: EINVAL, EDEGENERATE (det ∇F <= 0 at a node or sample), ELIMIT
+ * (staging exceeds shared memory), ENOMEM, ECUDA. */
+iga_status iga_projection_error(const iga_spline *macro, const int32_t *q, int32_t m_extra, double nu,
+                                int32_t n_samples, double *e_max, double *e_tile, void *stream);
+
+/* iga_select_degree — Eq. 65: find p_π with E_proj(p_π) <= tol, starting from
+ * the macro map's degrees and enriching or coarsening the space.  Reading
+ * R19: uniformly, q(s) = (max(p_M,k + s, 0))_k; returns the smallest such q(s) (for the
+ * twist's macro degrees 1, 1, 2 this gives 3, 3, 4 at s = 2).
+ *  tol > 0;  m_extra, n_samples as in iga_projection_error;  q_max: largest admissible
+ *  degree (<= 0: 4).   q_out [host] d degrees;  e_out [host, optional] E_proj(q_out).
+ * Errors: ELIMIT if no q(s) with max_k q_k <= q_max meets tol (q_out, e_out then hold the
+ * largest one tried); otherwise as iga_projection_error. */
+iga_status iga_select_degree(const iga_spline *macro, double nu, double tol, int32_t m_extra, int32_t n_samples,
+                             int32_t q_max, int32_t *q_out, double *e_out, void *stream);
 
 /* Accessors.  iga_get_sizes: [host] out. */
 iga_status iga_get_sizes(const iga_handle *h, iga_sizes *out);

@@ -5,4 +5,4 @@ isogeometric stiffness matrix K of microstructured geometries F∘M
 The product is libiga.so (C ABI, include/iga.h): hand-written CUDA for sm_100a.
 This package holds only the thin ctypes binding (`Assembler`) and the build script.
 """
-from ._binding import Assembler, IgaError, load  # noqa: F401
+from ._binding import Assembler, IgaError, load, projection_error, select_degree  # noqa: F401

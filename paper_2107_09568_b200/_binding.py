@@ -43,7 +43,7 @@ class iga_sizes(C.Structure):
                 ("n_nodes", C.c_int64), ("n_dof", C.c_int64), ("nnz", C.c_int64), ("n_blocks", C.c_int64),
                 ("n_contrib", C.c_int64), ("n_multi_blocks", C.c_int64), ("n_side_slots", C.c_int64),
                 ("tile_begin", C.c_int64), ("n_tiles_local", C.c_int64), ("n_tiles_owned", C.c_int64),
-                ("row_begin", C.c_int64), ("n_rows", C.c_int64)]
+                ("row_begin", C.c_int64), ("n_rows", C.c_int64), ("q_dir", C.c_int32 * 3), ("m_dir", C.c_int32 * 3)]
 
 
 class iga_shard(C.Structure):
@@ -51,7 +51,8 @@ class iga_shard(C.Structure):
 
 
 N_PROF = 10   # IGA_N_PROF: 0 K2, 1 K3(+scatter), 2 K4, 3 K5a, 4 K5b, 5 K5c, 6 staging, 7 K5x, 8 K3 nzdata, 9 apply
-EXPORTS = ["iga_build_tables", "iga_build_topology", "iga_assemble", "iga_sensitivity", "iga_assemble_sensitivity",
+EXPORTS = ["iga_build_tables", "iga_build_tables_q", "iga_build_topology", "iga_build_topology_q",
+           "iga_projection_error", "iga_select_degree", "iga_assemble", "iga_sensitivity", "iga_assemble_sensitivity",
            "iga_apply", "iga_volume", "iga_load_vector", "iga_interpolate",
            "iga_get_sizes",
            "iga_get_pattern", "iga_get_block_map", "iga_get_node_map", "iga_get_tables", "iga_get_pairs",
@@ -73,6 +74,14 @@ def load():
                                      C.POINTER(iga_spline), i32, i32, C.POINTER(iga_shard), vp, C.POINTER(vp)]
     lib.iga_build_topology.argtypes = [C.POINTER(iga_spline), i32, C.POINTER(iga_interface), i32,
                                        C.POINTER(iga_spline), i32, i32, C.POINTER(iga_shard), C.POINTER(vp)]
+    lib.iga_build_tables_q.argtypes = [C.POINTER(iga_spline), i32, C.POINTER(iga_interface), i32,
+                                       C.POINTER(iga_spline), C.POINTER(i32), i32, C.POINTER(iga_shard), vp,
+                                       C.POINTER(vp)]
+    lib.iga_build_topology_q.argtypes = [C.POINTER(iga_spline), i32, C.POINTER(iga_interface), i32,
+                                         C.POINTER(iga_spline), C.POINTER(i32), i32, C.POINTER(iga_shard),
+                                         C.POINTER(vp)]
+    lib.iga_projection_error.argtypes = [C.POINTER(iga_spline), C.POINTER(i32), i32, d, i32, C.POINTER(d), vp, vp]
+    lib.iga_select_degree.argtypes = [C.POINTER(iga_spline), d, d, i32, i32, i32, C.POINTER(i32), C.POINTER(d), vp]
     lib.iga_assemble.argtypes = [vp, vp, vp, i32, d, vp, vp, vp]
     lib.iga_sensitivity.argtypes = [vp, vp, vp, i32, d, vp, vp, vp, vp]
     lib.iga_interpolate.argtypes = [vp, vp, vp, i32, d, vp, vp]
@@ -150,6 +159,35 @@ def _spline(s, keep):
     return sp
 
 
+def _qvec(q, d):
+    qs = [int(q)] * d if np.ndim(q) == 0 else [int(x) for x in q]
+    if len(qs) != d:
+        raise ValueError(f"q has {len(qs)} entries for d = {d}")
+    return (C.c_int32 * 3)(*(qs + [0] * (3 - d)))
+
+
+def projection_error(macro, q, nu, n_samples=8, m_extra=0, e_tile=None, stream=None):
+    """iga_projection_error: E_proj (Eq. 59) of the macro spline for degree(s) q; e_tile
+    (optional, n_tiles doubles, host or device) receives the per-tile maxima."""
+    keep = []
+    mac = _spline(macro, keep)
+    e = C.c_double()
+    _check(load().iga_projection_error(C.byref(mac), _qvec(q, macro.dim), int(m_extra), float(nu), int(n_samples),
+                                       C.byref(e), _ptr(e_tile), _stream_ptr(stream)))
+    return e.value
+
+
+def select_degree(macro, nu, tol, n_samples=8, m_extra=0, q_max=0, stream=None):
+    """iga_select_degree (Eq. 65, reading R19): (q per direction, E_proj(q))."""
+    keep = []
+    mac = _spline(macro, keep)
+    q = (C.c_int32 * 3)()
+    e = C.c_double()
+    _check(load().iga_select_degree(C.byref(mac), float(nu), float(tol), int(m_extra), int(n_samples), int(q_max),
+                                    q, C.byref(e), _stream_ptr(stream)))
+    return tuple(q[k] for k in range(macro.dim)), e.value
+
+
 class Assembler:
     """Handle around iga_build_tables for a problem description (synth.Problem-like:
     .tile (patches), .interfaces, .macro (degree/knots), .q, .n_gauss).
@@ -165,12 +203,13 @@ class Assembler:
         mac = _spline(prob.macro, keep)
         sh = C.byref(iga_shard(int(shard[0]), int(shard[1]))) if shard is not None else None
         h = C.c_void_p()
+        qv = _qvec(prob.q, prob.macro.dim)   # one projection degree per direction (iga_build_tables_q)
         if topology_only:
-            _check(lib.iga_build_topology(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), prob.q,
-                                          n_gauss, sh, C.byref(h)))
+            _check(lib.iga_build_topology_q(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), qv,
+                                            n_gauss, sh, C.byref(h)))
         else:
-            _check(lib.iga_build_tables(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), prob.q,
-                                        n_gauss, sh, _stream_ptr(stream), C.byref(h)))
+            _check(lib.iga_build_tables_q(arr, len(prob.tile), ifs, len(prob.interfaces), C.byref(mac), qv,
+                                          n_gauss, sh, _stream_ptr(stream), C.byref(h)))
         self._h = h
         self.sizes = iga_sizes()
         _check(lib.iga_get_sizes(h, C.byref(self.sizes)))
@@ -240,8 +279,10 @@ class Assembler:
         return out
 
     def set_projection(self, m):
-        """L2 projection with an m-point Gauss rule per direction (m = q+1: interpolation)."""
+        """L2 projection with an m-point Gauss rule per direction (m = 0, or q+1 when
+        isotropic: interpolation at the q_k+1 Gauss nodes)."""
         _check(load().iga_set_projection(self._h, int(m)))
+        _check(load().iga_get_sizes(self._h, C.byref(self.sizes)))   # m_dir
 
     def projection(self):
         m = C.c_int32()

@@ -172,15 +172,59 @@ struct UF {
   }
 };
 
+// the macro map ℳ = F (Eq. 4): knots, elements per direction, NURBS weights
+iga_status parse_macro(Handle &h, const iga_spline *macro, int d) {
+  if (!macro) { set_error("no macro topology"); return IGA_EINVAL; }
+  if (macro->dim != d) { set_error("macro dim %d != tile dim %d", macro->dim, d); return IGA_EINVAL; }
+  h.n_cp = 1;
+  h.n_tiles = 1;
+  for (int k = 0; k < 3; ++k) { h.pm[k] = 0; h.mn[k] = 1; h.mel[k] = 1; }
+  for (int k = 0; k < d; ++k) {
+    if (!check_knots(*macro, k, "macro", 0, h.mknots[k], h.mel_span[k])) return IGA_EINVAL;
+    h.pm[k] = macro->degree[k];
+    h.mn[k] = macro->n_knots[k] - macro->degree[k] - 1;
+    h.mel[k] = (int)h.mel_span[k].size();
+    h.n_cp *= h.mn[k];
+    h.n_tiles *= h.mel[k];
+  }
+  h.mweights.clear();
+  if (macro->weights) {   // NURBS macro map (NEXT N4)
+    h.mweights.assign(macro->weights, macro->weights + h.n_cp);
+    for (double w : h.mweights)
+      if (!(w > 0.0)) { set_error("macro weights must be positive"); return IGA_EINVAL; }
+  }
+  return IGA_OK;
+}
+
+// projection degrees per direction (Eq. 21 with p_π per direction, the twist's 3, 3, 4)
+iga_status set_degrees(Handle &h, const int *q) {
+  h.q = 0;
+  h.iso = true;
+  h.npi = 1;
+  for (int k = 0; k < 3; ++k) h.qv[k] = 0;
+  for (int k = 0; k < h.d; ++k) {
+    if (q[k] < 0 || q[k] > IGA_MAXQ) { set_error("q[%d]=%d outside [0,%d]", k, q[k], IGA_MAXQ); return IGA_EINVAL; }
+    h.qv[k] = q[k];
+    h.q = std::max(h.q, q[k]);
+    h.iso = h.iso && q[k] == q[0];
+    h.npi *= q[k] + 1;
+  }
+  h.nk = h.d * h.d * h.npi;
+  h.kstride = (h.nk + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK;
+  return IGA_OK;
+}
+
 iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const iga_interface *ifc,
-                      int n_ifc, const iga_spline *macro, int q, int n_gauss, const iga_shard *shard) {
-  if (!tile || n_patches <= 0 || !macro) { set_error("no tile patches or no macro topology"); return IGA_EINVAL; }
+                      int n_ifc, const iga_spline *macro, const int *q, int n_gauss, const iga_shard *shard) {
+  if (!tile || n_patches <= 0 || !macro || !q) { set_error("no tile patches, macro topology or q"); return IGA_EINVAL; }
   const int d = tile[0].dim;
   if (d != 2 && d != 3) { set_error("dim must be 2 or 3 (got %d)", d); return IGA_EINVAL; }
   if (macro->dim != d) { set_error("macro dim %d != tile dim %d", macro->dim, d); return IGA_EINVAL; }
-  if (q < 0 || q > IGA_MAXQ) { set_error("q=%d outside [0,%d]", q, IGA_MAXQ); return IGA_EINVAL; }
   h.d = d;
-  h.q = q;
+  {
+    const iga_status st = set_degrees(h, q);
+    if (st != IGA_OK) return st;
+  }
   h.p = tile[0].degree[0];
   h.n_patches = n_patches;
   h.patches.resize(n_patches);
@@ -210,28 +254,12 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     off += P.n_ctrl;
   }
   h.n_local_ctrl = off;
-  h.n_cp = 1;
-  h.n_tiles = 1;
-  for (int k = 0; k < d; ++k) {
-    if (!check_knots(*macro, k, "macro", 0, h.mknots[k], h.mel_span[k])) return IGA_EINVAL;
-    h.pm[k] = macro->degree[k];
-    h.mn[k] = macro->n_knots[k] - macro->degree[k] - 1;
-    h.mel[k] = (int)h.mel_span[k].size();
-    h.n_cp *= h.mn[k];
-    h.n_tiles *= h.mel[k];
+  {
+    const iga_status st = parse_macro(h, macro, d);
+    if (st != IGA_OK) return st;
   }
-  h.mweights.clear();
-  if (macro->weights) {   // NURBS macro map (NEXT N4)
-    h.mweights.assign(macro->weights, macro->weights + h.n_cp);
-    for (double w : h.mweights)
-      if (!(w > 0.0)) { set_error("macro weights must be positive"); return IGA_EINVAL; }
-  }
-  h.n_g = n_gauss > 0 ? n_gauss : h.p + (q + 2) / 2;
+  h.n_g = n_gauss > 0 ? n_gauss : h.p + (h.q + 2) / 2;   // R3 with the largest q_k
   if (h.n_g > 12) { set_error("n_gauss=%d > 12", h.n_g); return IGA_EINVAL; }
-  h.npi = 1;
-  for (int k = 0; k < d; ++k) h.npi *= (q + 1);
-  h.nk = d * d * h.npi;
-  h.kstride = (h.nk + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK;
 
   // ---- I_coo per patch (Eq. 56; R8: supports share a knot span) -------------
   h.M = 0;
@@ -638,51 +666,86 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   h.k5_rows = (h.kstride + IGA_K5_BM - 1) / IGA_K5_BM * IGA_K5_BM;
   if (k5x_smem_bytes(d, h.max_patch_ctrl) > 227 * 1024) { set_error("tile patch too large for the K5 shared-memory staging (%d control points)", h.max_patch_ctrl); return IGA_ELIMIT; }
 
-  // ---- projection operator (R1: interpolation at the q+1 Gauss nodes) -------------
+  // ---- projection operator (R1: interpolation at the q_k+1 Gauss nodes) -----------
   {
-    const iga_status st = set_projection(h, q + 1);
+    const iga_status st = set_projection(h, 0);
     if (st != IGA_OK) return st;
   }
   return IGA_OK;
 }
 
-// Π1 for an m-point Gauss rule per direction (Eqs. 23-24: M_π d = r_π with
+// Π1 for an m-point Gauss rule in one direction (Eqs. 23-24: M_π d = r_π with
 // [M_π]_kl = Σ_i w_i N_k(x_i) N_l(x_i), (r_π)_k = Σ_i w_i N_k(x_i) f(x_i), tensorised):
 // Pi1 = (VᵀWV)⁻¹VᵀW, V[i][c] = B_c^q(x_i).  m = q+1 reduces to V⁻¹ (interpolation at the
 // Gauss nodes, reading R1), computed directly.
-iga_status set_projection(Handle &h, int m) {
-  const int q = h.q, q1 = q + 1;
-  if (m < q1 || m > IGA_MAXM) { set_error("projection points m=%d outside [q+1=%d, %d]", m, q1, IGA_MAXM); return IGA_EINVAL; }
-  if (macro_smem_bytes(h.d, q, m, true) > 227 * 1024 || macro_smem_bytes(h.d, q, m, false) > 227 * 1024) {
-    set_error("projection points m=%d: per-tile staging exceeds shared memory", m);
-    return IGA_ELIMIT;
-  }
-  double x[IGA_MAXM], w[IGA_MAXM], V[IGA_MAXM * (IGA_MAXQ + 1)];
+static iga_status projection_1d(int q, int m, double *x, double *P) {
+  const int q1 = q + 1;
+  double w[IGA_MAXM], V[IGA_MAXM * (IGA_MAXQ + 1)];
   gauss_legendre01(m, x, w);
   for (int i = 0; i < m; ++i)
     for (int c = 0; c <= q; ++c) V[i * q1 + c] = binom(q, c) * std::pow(x[i], c) * std::pow(1.0 - x[i], q - c);
-  double P[(IGA_MAXQ + 1) * IGA_MAXM];
   if (m == q1) {
     if (!invert(q1, V, P)) { set_error("singular interpolation matrix"); return IGA_EINVAL; }
-  } else {
-    double Mpi[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)], Minv[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
-    for (int k = 0; k < q1; ++k)
-      for (int l = 0; l < q1; ++l) {
-        double v = 0.0;
-        for (int i = 0; i < m; ++i) v += w[i] * V[i * q1 + k] * V[i * q1 + l];
-        Mpi[k * q1 + l] = v;
-      }
-    if (!invert(q1, Mpi, Minv)) { set_error("singular projection mass matrix"); return IGA_EINVAL; }
-    for (int c = 0; c < q1; ++c)
-      for (int i = 0; i < m; ++i) {
-        double v = 0.0;
-        for (int k = 0; k < q1; ++k) v += Minv[c * q1 + k] * V[i * q1 + k];
-        P[c * m + i] = v * w[i];
-      }
+    return IGA_OK;
   }
-  h.m_proj = m;
-  for (int i = 0; i < m; ++i) h.interp_x[i] = x[i];
-  for (int i = 0; i < q1 * m; ++i) h.Pi1[i] = P[i];
+  double Mpi[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)], Minv[(IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
+  for (int k = 0; k < q1; ++k)
+    for (int l = 0; l < q1; ++l) {
+      double v = 0.0;
+      for (int i = 0; i < m; ++i) v += w[i] * V[i * q1 + k] * V[i * q1 + l];
+      Mpi[k * q1 + l] = v;
+    }
+  if (!invert(q1, Mpi, Minv)) { set_error("singular projection mass matrix"); return IGA_EINVAL; }
+  for (int c = 0; c < q1; ++c)
+    for (int i = 0; i < m; ++i) {
+      double v = 0.0;
+      for (int k = 0; k < q1; ++k) v += Minv[c * q1 + k] * V[i * q1 + k];
+      P[c * m + i] = v * w[i];
+    }
+  return IGA_OK;
+}
+
+iga_status set_projection_v(Handle &h, const int *mv) {
+  int ns = 1;
+  bool iso = true;
+  for (int k = 0; k < h.d; ++k) {
+    if (mv[k] < h.qv[k] + 1 || mv[k] > IGA_MAXM) {
+      set_error("projection points m=%d outside [q+1=%d, %d] (direction %d)", mv[k], h.qv[k] + 1, IGA_MAXM, k);
+      return IGA_EINVAL;
+    }
+    ns *= mv[k];
+    iso = iso && mv[k] == mv[0] && h.qv[k] == h.qv[0];
+  }
+  if (macro_smem_bytes(h.d, ns, true) > 227 * 1024 || macro_smem_bytes(h.d, ns, false) > 227 * 1024) {
+    set_error("projection with %d sample nodes per tile: per-tile staging exceeds shared memory", ns);
+    return IGA_ELIMIT;
+  }
+  double x[3][IGA_MAXM], P[3][(IGA_MAXQ + 1) * IGA_MAXM];
+  for (int k = 0; k < h.d; ++k) {
+    const iga_status st = projection_1d(h.qv[k], mv[k], x[k], P[k]);
+    if (st != IGA_OK) return st;
+  }
+  for (int k = 0; k < 3; ++k) {
+    h.mv[k] = k < h.d ? mv[k] : 1;
+    for (int i = 0; i < IGA_MAXM; ++i) h.interp_x[k][i] = (k < h.d && i < mv[k]) ? x[k][i] : 0.0;
+    for (int i = 0; i < (IGA_MAXQ + 1) * IGA_MAXM; ++i)
+      h.Pi1[k][i] = (k < h.d && i < (h.qv[k] + 1) * mv[k]) ? P[k][i] : (k >= h.d && i == 0 ? 1.0 : 0.0);
+  }
+  h.ns = ns;
+  h.iso = iso;
+  return IGA_OK;
+}
+
+// m = 0: interpolation at the q_k+1 Gauss nodes per direction (R1); else the L2 projection
+// with an m-point rule in every direction (m >= max_k q_k + 1)
+iga_status set_projection(Handle &h, int m) {
+  int mv[3];
+  for (int k = 0; k < h.d; ++k) mv[k] = m == 0 ? h.qv[k] + 1 : m;
+  const iga_status st = set_projection_v(h, mv);
+  if (st != IGA_OK) return st;
+  bool iso_q = true;
+  for (int k = 0; k < h.d; ++k) iso_q = iso_q && h.qv[k] == h.qv[0];
+  h.m_proj = m == 0 ? (iso_q ? h.q + 1 : 0) : m;
   return IGA_OK;
 }
 

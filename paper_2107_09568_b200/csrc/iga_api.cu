@@ -168,6 +168,14 @@ const char *iga_version(void) { return "libiga 0.1 (sm_100a, FP64 DMMA)"; }
 iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
                             int32_t n_interfaces, const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
                             const iga_shard *shard, void *stream, iga_handle **out) {
+  const int32_t qv[3] = {q, q, q};
+  return iga_build_tables_q(tile_patches, n_patches, interfaces, n_interfaces, macro_topology, qv, n_gauss, shard,
+                            stream, out);
+}
+
+iga_status iga_build_tables_q(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
+                              int32_t n_interfaces, const iga_spline *macro_topology, const int32_t *q,
+                              int32_t n_gauss, const iga_shard *shard, void *stream, iga_handle **out) {
   if (!out) { set_error("out is NULL"); return IGA_EINVAL; }
   *out = nullptr;
   if (n_patches > 64) { set_error("at most 64 tile patches"); return IGA_EINVAL; }
@@ -290,6 +298,14 @@ iga_status iga_build_tables(const iga_spline *tile_patches, int32_t n_patches, c
 iga_status iga_build_topology(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
                               int32_t n_interfaces, const iga_spline *macro_topology, int32_t q, int32_t n_gauss,
                               const iga_shard *shard, iga_handle **out) {
+  const int32_t qv[3] = {q, q, q};
+  return iga_build_topology_q(tile_patches, n_patches, interfaces, n_interfaces, macro_topology, qv, n_gauss, shard,
+                              out);
+}
+
+iga_status iga_build_topology_q(const iga_spline *tile_patches, int32_t n_patches, const iga_interface *interfaces,
+                                int32_t n_interfaces, const iga_spline *macro_topology, const int32_t *q,
+                                int32_t n_gauss, const iga_shard *shard, iga_handle **out) {
   if (!out) { set_error("out is NULL"); return IGA_EINVAL; }
   *out = nullptr;
   iga_handle *H = new (std::nothrow) iga_handle();
@@ -315,6 +331,10 @@ iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
   o->dim = h.d;
   o->q = h.q;
   o->n_pi = h.npi;
+  for (int k = 0; k < 3; ++k) {
+    o->q_dir[k] = h.qv[k];
+    o->m_dir[k] = h.mv[k];
+  }
   o->n_k = h.nk;
   o->k_stride = h.kstride;
   o->n_patches = h.n_patches;
@@ -606,6 +626,151 @@ iga_status iga_assemble_sensitivity(const iga_handle *Hc, const double *macro_ct
   st = check_flag(h, s);
   pf.collect();
   return st;
+}
+
+// ---- a-priori projection error and degree selection (Eqs. 59, 65) ----
+namespace {
+struct MacroOnly {   // the macro map on the device, no tile (iga_projection_error / iga_select_degree)
+  Handle h;
+  double *d_ctrl = nullptr, *d_e = nullptr;
+  ~MacroOnly() {
+    if (d_ctrl) cudaFree(d_ctrl);
+    if (d_e) cudaFree(d_e);
+  }
+};
+
+iga_status macro_only_setup(MacroOnly &mo, const iga_spline *macro, int32_t n_samples, cudaStream_t s) {
+  if (!macro || !macro->ctrl) { set_error("macro spline with control points required"); return IGA_EINVAL; }
+  if (macro->dim != 2 && macro->dim != 3) { set_error("dim must be 2 or 3"); return IGA_EINVAL; }
+  if (n_samples < 2 || n_samples > IGA_MAXM) { set_error("n_samples=%d outside [2,%d]", n_samples, IGA_MAXM); return IGA_EINVAL; }
+  Handle &h = mo.h;
+  h.d = macro->dim;
+  iga_status st = parse_macro(h, macro, h.d);
+  if (st != IGA_OK) return st;
+  h.n_tiles_glob = h.n_tiles;
+  h.n_tiles_own = h.n_tiles;
+  std::vector<double> mk;
+  std::vector<int> ms;
+  for (int k = 0; k < h.d; ++k) {
+    mk.insert(mk.end(), h.mknots[k].begin(), h.mknots[k].end());
+    ms.insert(ms.end(), h.mel_span[k].begin(), h.mel_span[k].end());
+  }
+  if (cudaMalloc((void **)&h.d_mknots, sizeof(double) * mk.size()) || cudaMalloc((void **)&h.d_mspan, sizeof(int) * ms.size()) ||
+      cudaMalloc((void **)&h.d_flag, 4 * sizeof(int)) || cudaMalloc((void **)&mo.d_ctrl, sizeof(double) * h.n_cp * h.d) ||
+      cudaMalloc((void **)&mo.d_e, sizeof(double) * h.n_tiles)) {
+    set_error("device allocation failed");
+    return IGA_ENOMEM;
+  }
+  if (!h.mweights.empty()) {
+    if (cudaMalloc((void **)&h.d_mweights, sizeof(double) * h.mweights.size())) { set_error("device allocation failed"); return IGA_ENOMEM; }
+    CU(cudaMemcpyAsync(h.d_mweights, h.mweights.data(), sizeof(double) * h.mweights.size(), cudaMemcpyHostToDevice, s));
+  }
+  CU(cudaMemcpyAsync(h.d_mknots, mk.data(), sizeof(double) * mk.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(h.d_mspan, ms.data(), sizeof(int) * ms.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(mo.d_ctrl, macro->ctrl, sizeof(double) * h.n_cp * h.d, cudaMemcpyHostToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return IGA_OK;
+}
+
+// E_proj for degrees q (d values) with q_k + 1 + m_extra projection points per direction
+iga_status macro_only_error(MacroOnly &mo, const int32_t *q, int32_t m_extra, double nu, int32_t n_samples,
+                            double *e_max, std::vector<double> *e_host, cudaStream_t s) {
+  Handle &h = mo.h;
+  iga_status st = set_degrees(h, q);
+  if (st != IGA_OK) return st;
+  int mv[3] = {1, 1, 1};
+  for (int k = 0; k < h.d; ++k) mv[k] = h.qv[k] + 1 + m_extra;
+  st = set_projection_v(h, mv);
+  if (st != IGA_OK) return st;
+  if (projection_error_smem_bytes(h.d, h.ns, n_samples, h.npi) > 227 * 1024) {
+    set_error("projection error: per-tile staging exceeds shared memory (reduce n_samples or m_extra)");
+    return IGA_ELIMIT;
+  }
+  CU(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
+  CU(launch_projection_error(h, mo.d_ctrl, nu, n_samples, mo.d_e, s));
+  std::vector<double> e((size_t)h.n_tiles);
+  CU(cudaMemcpyAsync(e.data(), mo.d_e, sizeof(double) * e.size(), cudaMemcpyDeviceToHost, s));
+  st = check_flag(h, s);
+  if (st != IGA_OK) return st;
+  double mx = 0.0;
+  for (double x : e) mx = std::max(mx, x);
+  *e_max = mx;
+  if (e_host) e_host->swap(e);
+  return IGA_OK;
+}
+}  // namespace
+
+iga_status iga_projection_error(const iga_spline *macro, const int32_t *q, int32_t m_extra, double nu,
+                                int32_t n_samples, double *e_max, double *e_tile, void *stream) {
+  if (!q || !e_max) { set_error("NULL argument"); return IGA_EINVAL; }
+  if (m_extra < 0) { set_error("m_extra < 0"); return IGA_EINVAL; }
+  if (!(nu > -1.0 && nu < 0.5)) { set_error("nu=%g outside (-1, 0.5)", nu); return IGA_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  MacroOnly mo;
+  iga_status st = macro_only_setup(mo, macro, n_samples ? n_samples : 8, s);
+  if (st != IGA_OK) return st;
+  std::vector<double> e;
+  st = macro_only_error(mo, q, m_extra, nu, n_samples ? n_samples : 8, e_max, &e, s);
+  if (st != IGA_OK) return st;
+  if (e_tile) CU(cudaMemcpy(e_tile, e.data(), sizeof(double) * e.size(), cudaMemcpyDefault));
+  return IGA_OK;
+}
+
+iga_status iga_select_degree(const iga_spline *macro, double nu, double tol, int32_t m_extra, int32_t n_samples,
+                             int32_t q_max, int32_t *q_out, double *e_out, void *stream) {
+  if (!q_out || !(tol > 0.0)) { set_error("NULL q_out or tol <= 0"); return IGA_EINVAL; }
+  if (!(nu > -1.0 && nu < 0.5)) { set_error("nu=%g outside (-1, 0.5)", nu); return IGA_EINVAL; }
+  if (q_max <= 0 || q_max > IGA_MAXQ) q_max = IGA_MAXQ;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int ns_ = n_samples ? n_samples : 8;
+  MacroOnly mo;
+  iga_status st = macro_only_setup(mo, macro, ns_, s);
+  if (st != IGA_OK) return st;
+  const int d = mo.h.d;
+  // reading R19: q(s) = max(p_M,k + s, 0), uniform enrichment / coarsening from the macro degrees
+  auto q_of = [&](int sh, int32_t *q) {
+    int mx = 0;
+    for (int k = 0; k < d; ++k) {
+      q[k] = std::max(mo.h.pm[k] + sh, 0);
+      mx = std::max(mx, q[k]);
+    }
+    return mx;
+  };
+  int32_t q[3] = {0, 0, 0};
+  int sh = 0;
+  if (q_of(0, q) > q_max) { set_error("macro degree exceeds q_max=%d", q_max); return IGA_EINVAL; }
+  double e = 0.0;
+  st = macro_only_error(mo, q, m_extra, nu, ns_, &e, nullptr, s);
+  if (st != IGA_OK) return st;
+  if (e <= tol) {
+    while (q_of(sh, q) > 0) {
+      double e_down = 0.0;
+      q_of(sh - 1, q);
+      st = macro_only_error(mo, q, m_extra, nu, ns_, &e_down, nullptr, s);
+      if (st != IGA_OK) return st;
+      if (e_down > tol) break;
+      --sh;
+      e = e_down;
+    }
+  } else {
+    for (;;) {
+      if (q_of(sh + 1, q) > q_max) {
+        q_of(sh, q);
+        for (int k = 0; k < d; ++k) q_out[k] = q[k];
+        if (e_out) *e_out = e;
+        set_error("E_proj = %.3e > tol = %.1e at the largest admissible degree (q_max = %d)", e, tol, q_max);
+        return IGA_ELIMIT;
+      }
+      ++sh;
+      st = macro_only_error(mo, q, m_extra, nu, ns_, &e, nullptr, s);
+      if (st != IGA_OK) return st;
+      if (e <= tol) break;
+    }
+  }
+  q_of(sh, q);
+  for (int k = 0; k < d; ++k) q_out[k] = q[k];
+  if (e_out) *e_out = e;
+  return IGA_OK;
 }
 
 iga_status iga_get_pattern(const iga_handle *Hc, int64_t *row_ptr, int32_t *col_idx) {

@@ -58,6 +58,8 @@ struct MultiBlock {
 
 struct Handle {
   int d = 0, p = 0, q = 0, n_g = 0, npi = 0, nk = 0, kstride = 0;
+  int qv[3] = {0, 0, 0};         // per-direction projection degrees (anisotropic Q); q = max
+  bool iso = true;               // all qv equal and (after set_projection) all mv equal
   int n_patches = 0;
   std::vector<PatchInfo> patches;
   int n_local_ctrl = 0;
@@ -109,11 +111,13 @@ struct Handle {
   std::vector<int64_t> inv_ptr;      // [n_nodes+1] owned node -> its (tile, A) occurrences
   std::vector<int32_t> inv_ent;      // lt*nl + A, sorted
   bool on_device = false;
-  // projection operator (Eqs. 23-24 with an m-point Gauss rule per direction; m = q+1:
-  // interpolation at the Gauss nodes, reading R1): coef_c = Σ_i Pi1[c*m + i] f(x_i)
-  int m_proj = 0;
-  double interp_x[IGA_MAXM];
-  double Pi1[(IGA_MAXQ + 1) * IGA_MAXM];
+  // projection operator (Eqs. 23-24 with an m_k-point Gauss rule in direction k; m_k = q_k+1:
+  // interpolation at the Gauss nodes, reading R1): coef_c = Σ_i Pi1[k][c*m_k + i] f(x_i)
+  int m_proj = 0;                // as requested: q+1 (isotropic interpolation), 0 (anisotropic interpolation) or m
+  int mv[3] = {1, 1, 1};
+  int ns = 1;                    // Π_k m_k sample nodes per tile
+  double interp_x[3][IGA_MAXM];
+  double Pi1[3][(IGA_MAXQ + 1) * IGA_MAXM];
   // device buffers
   double *d_table = nullptr;     // [M][kstride] row-major (K1 output, accessor)
   double *d_tabA = nullptr;      // FM [Mpad][kstride], BR = IGA_K3_BM (K3 A operand)
@@ -172,9 +176,11 @@ struct InterpConst {
   int64_t t_base;        // global id of local tile 0
   const double *mweights;   // NURBS macro weights (nullptr: B-spline)
   int64_t n_own;         // owned local tiles (sensitivity reduction)
-  int m;                 // projection points per direction (q+1: interpolation)
-  double Pi1[(IGA_MAXQ + 1) * IGA_MAXM];   // [(q+1) x m]
-  double x[IGA_MAXM];
+  int m;                 // isotropic case: projection points per direction (q+1: interpolation)
+  int qv[3], mv[3];      // per-direction degrees and sample points (directions >= d: 0 and 1)
+  int npi, ns, iso;      // Π (q_k+1), Π m_k, all directions equal
+  double Pi1[3][(IGA_MAXQ + 1) * IGA_MAXM];   // [k][(q_k+1) x m_k]
+  double x[3][IGA_MAXM];
 };
 
 // --- kernel launchers (kernels_*.cu) ---
@@ -202,10 +208,18 @@ InterpConst make_interp_const(const Handle &h);
 
 // host build steps (host_build.cpp)
 iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const iga_interface *ifc,
-                      int n_ifc, const iga_spline *macro, int q, int n_gauss, const iga_shard *shard);
+                      int n_ifc, const iga_spline *macro, const int *q, int n_gauss, const iga_shard *shard);
+iga_status parse_macro(Handle &h, const iga_spline *macro, int d);   // macro knots / elements / weights
+iga_status set_degrees(Handle &h, const int *q);                      // qv, q, iso, npi, nk, kstride
 void gauss_legendre01(int n, double *x, double *w);
-iga_status set_projection(Handle &h, int m);   // host: Pi1, x for m points per direction
-size_t macro_smem_bytes(int d, int q, int m, bool reverse);
+// host: Pi1, x per direction; m = 0: interpolation (m_k = q_k+1), else m_k = m for every k
+iga_status set_projection(Handle &h, int m);
+iga_status set_projection_v(Handle &h, const int *mv);
+size_t macro_smem_bytes(int d, int ns, bool reverse);
+// a-priori projection error (Eq. 59) per tile of the macro map in h (device work)
+cudaError_t launch_projection_error(const Handle &h, const double *ctrl, double nu, int n_s, double *e_tile,
+                                    cudaStream_t s);
+size_t projection_error_smem_bytes(int d, int ns, int n_s, int npi);
 iga_status upload_topology(Handle &h);
 
 }  // namespace iga

@@ -12,6 +12,8 @@
 //   chained to the macro control points through ∂J/∂P = h_β ∂_β N_k.
 // K5c: deterministic reduction of the per-tile partials over the tiles sharing a
 //   control point (fixed tile order, no atomics).
+#include <algorithm>
+#include <cmath>
 #include "device_common.cuh"
 
 namespace iga {
@@ -33,9 +35,16 @@ InterpConst make_interp_const(const Handle &h) {
   ic.t_base = h.t_base;
   ic.mweights = h.d_mweights;
   ic.n_own = h.n_tiles_own;
-  ic.m = h.m_proj;
-  for (int i = 0; i < (IGA_MAXQ + 1) * IGA_MAXM; ++i) ic.Pi1[i] = h.Pi1[i];
-  for (int i = 0; i < IGA_MAXM; ++i) ic.x[i] = h.interp_x[i];
+  ic.m = h.mv[0];
+  ic.npi = h.npi;
+  ic.ns = h.ns;
+  ic.iso = h.iso ? 1 : 0;
+  for (int k = 0; k < 3; ++k) {
+    ic.qv[k] = h.qv[k];
+    ic.mv[k] = h.mv[k];
+    for (int i = 0; i < (IGA_MAXQ + 1) * IGA_MAXM; ++i) ic.Pi1[k][i] = h.Pi1[k][i];
+    for (int i = 0; i < IGA_MAXM; ++i) ic.x[k][i] = h.interp_x[k][i];
+  }
   return ic;
 }
 
@@ -54,17 +63,17 @@ template <int D>
 __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64_t t, const double *__restrict__ ctrl,
                                 const double *__restrict__ mknots, const int *__restrict__ mspan,
                                 int tid = threadIdx.x, int nthr = blockDim.x) {
-  const int m1 = c_ip.m;   // sample points per direction
   int e[3] = {0, 0, 0};
   int64_t tmp = t;
   for (int k = 0; k < D; ++k) { e[k] = (int)(tmp % c_ip.mel[k]); tmp /= c_ip.mel[k]; }
-  if (tid < D * m1) {
-    int k = tid / m1, m = tid % m1;
+  for (int idx = tid; idx < D * IGA_MAXM; idx += nthr) {   // sample point m of direction k
+    const int k = idx / IGA_MAXM, m = idx % IGA_MAXM;
+    if (m >= c_ip.mv[k]) continue;
     const double *U = mknots + c_ip.moff[k];
     int s = mspan[c_ip.soff[k] + e[k]];
     double h = U[s + 1] - U[s];
     double N[IGA_MAXP + 1], dN[IGA_MAXP + 1];
-    bspline_eval(U, c_ip.pm[k], s, U[s] + h * c_ip.x[m], N, dN);
+    bspline_eval(U, c_ip.pm[k], s, U[s] + h * c_ip.x[k][m], N, dN);
     for (int r = 0; r <= c_ip.pm[k]; ++r) {
       mt.B1[k][m][r] = N[r];
       mt.D1[k][m][r] = dN[r] * h;
@@ -95,8 +104,7 @@ __device__ void macro_W(const InterpConst &c_ip, const MacroTile<D> &mt, int m, 
   W = 1.0;
   for (int be = 0; be < D; ++be) dW[be] = 0.0;
   if (!mt.rational) return;
-  const int q1 = c_ip.m;
-  int mm[3] = {m % q1, (m / q1) % q1, m / (q1 * q1)};
+  const int mm[3] = {m % c_ip.mv[0], (m / c_ip.mv[0]) % c_ip.mv[1], m / (c_ip.mv[0] * c_ip.mv[1])};
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   W = 0.0;
   for (int ra = 0; ra < mt.nact; ++ra) {
@@ -116,8 +124,7 @@ __device__ void macro_W(const InterpConst &c_ip, const MacroTile<D> &mt, int m, 
 template <int D>
 __device__ __forceinline__ void basis_grad(const InterpConst &c_ip, const MacroTile<D> &mt, int m, int ra, double W,
                                            const double *dW, double g[D]) {
-  const int q1 = c_ip.m;
-  int mm[3] = {m % q1, (m / q1) % q1, m / (q1 * q1)};
+  const int mm[3] = {m % c_ip.mv[0], (m / c_ip.mv[0]) % c_ip.mv[1], m / (c_ip.mv[0] * c_ip.mv[1])};
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   int r[3] = {ra % n1[0], (ra / n1[0]) % n1[1], ra / (n1[0] * n1[1])};
   double N = 1.0;
@@ -132,8 +139,7 @@ __device__ __forceinline__ void basis_grad(const InterpConst &c_ip, const MacroT
 // J[a][β] = ∂F_a/∂ξ_β at tensor sample node m (m^d nodes, direction-0 fastest)
 template <int D>
 __device__ void macro_J(const InterpConst &c_ip, const MacroTile<D> &mt, int m, double J[D][D]) {
-  const int q1 = c_ip.m;
-  int mm[3] = {m % q1, (m / q1) % q1, m / (q1 * q1)};
+  const int mm[3] = {m % c_ip.mv[0], (m / c_ip.mv[0]) % c_ip.mv[1], m / (c_ip.mv[0] * c_ip.mv[1])};
   int n1[3] = {c_ip.pm[0] + 1, D > 1 ? c_ip.pm[1] + 1 : 1, D > 2 ? c_ip.pm[2] + 1 : 1};
   for (int a = 0; a < D; ++a)
     for (int b = 0; b < D; ++b) J[a][b] = 0.0;
@@ -165,11 +171,12 @@ __device__ __forceinline__ void lame(double E, double nu, double &lam, double &m
 
 // one 1D pass of the projection along direction `dir` of an n[0]×n[1]×n[2] array of
 // NCOMP-vectors in shared memory: forward (samples -> coefficients) out[..c..] =
-// Σ_i Π1[c][i] in[..i..] (n[dir]: m -> q+1); transposed out[..i..] = Σ_c Π1[c][i] in[..c..]
-// (n[dir]: q+1 -> m).  Updates n[] to the output shape.
+// Σ_i Π1[dir][c][i] in[..i..] (n[dir]: m_dir -> q_dir+1); transposed out[..i..] =
+// Σ_c Π1[dir][c][i] in[..c..] (n[dir]: q_dir+1 -> m_dir).  Updates n[] to the output shape.
 template <int NCOMP>
 __device__ void proj_pass(const InterpConst &c_ip, const double *in, double *out, int n[3], int dir, bool transpose) {
-  const int q1 = c_ip.q + 1, m1 = c_ip.m;
+  const int q1 = c_ip.qv[dir] + 1, m1 = c_ip.mv[dir];
+  const double *Pi1 = c_ip.Pi1[dir];
   const int nin = n[dir], nout = transpose ? m1 : q1;
   int o[3] = {n[0], n[1], n[2]};
   o[dir] = nout;
@@ -184,17 +191,18 @@ __device__ void proj_pass(const InterpConst &c_ip, const double *in, double *out
     const double *src = in + ((hi * nin) * stride_in + lo) * NCOMP + comp;
     double acc = 0.0;
     for (int k = 0; k < nin; ++k)
-      acc = fma(transpose ? c_ip.Pi1[k * m1 + c] : c_ip.Pi1[c * m1 + k], src[k * stride_in * NCOMP], acc);
+      acc = fma(transpose ? Pi1[k * m1 + c] : Pi1[c * m1 + k], src[k * stride_in * NCOMP], acc);
     out[idx] = acc;
   }
   n[dir] = nout;
 }
 
-// the m = q+1 case with every index a compile-time constant
+// the isotropic m = q+1 case with every index a compile-time constant
 template <int D, int Q, int DIR, bool TRANSPOSE, int NCOMP>
 __device__ __forceinline__ void tensor_pass(const InterpConst &c_ip, const double *in, double *out) {
   constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
   constexpr int STRIDE = DIR == 0 ? 1 : (DIR == 1 ? Q1 : Q1 * Q1);
+  const double *Pi1 = c_ip.Pi1[DIR];
   for (int idx = threadIdx.x; idx < NPI * NCOMP; idx += blockDim.x) {
     const int C = idx / NCOMP, comp = idx - C * NCOMP;
     const int c = (C / STRIDE) % Q1;
@@ -202,7 +210,7 @@ __device__ __forceinline__ void tensor_pass(const InterpConst &c_ip, const doubl
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < Q1; ++k)
-      acc = fma(TRANSPOSE ? c_ip.Pi1[k * Q1 + c] : c_ip.Pi1[c * Q1 + k], src[k * STRIDE * NCOMP], acc);
+      acc = fma(TRANSPOSE ? Pi1[k * Q1 + c] : Pi1[c * Q1 + k], src[k * STRIDE * NCOMP], acc);
     out[idx] = acc;
   }
 }
@@ -222,8 +230,8 @@ __device__ const double *tensor_apply(const InterpConst &c_ip, double *a, double
 // all d passes; a, b: the two buffers; returns the one holding the result
 template <int D, int NCOMP>
 __device__ const double *proj_apply(const InterpConst &c_ip, double *a, double *b, bool transpose) {
-  const int n0 = transpose ? c_ip.q + 1 : c_ip.m;
-  int n[3] = {n0, n0, D == 3 ? n0 : 1};
+  int n[3] = {1, 1, 1};
+  for (int k = 0; k < D; ++k) n[k] = transpose ? c_ip.qv[k] + 1 : c_ip.mv[k];
   double *in = a, *out = b;
   for (int dir = 0; dir < D; ++dir) {
     proj_pass<NCOMP>(c_ip, in, out, n, dir, transpose);
@@ -243,7 +251,7 @@ struct NodeGeo {
 template <int D>
 __device__ __forceinline__ void node_geometry(const InterpConst &c_ip, const MacroTile<D> &mt, NodeGeo<D> *geo,
                                               int64_t t, int *flag) {
-  const int ns = D == 2 ? c_ip.m * c_ip.m : c_ip.m * c_ip.m * c_ip.m;
+  const int ns = c_ip.ns;
   for (int m = threadIdx.x; m < ns; m += blockDim.x) {
     double J[D][D], G[D][D];
     macro_J<D>(c_ip, mt, m, J);
@@ -324,7 +332,7 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
     const int c = C % Q1, base = C - c;
     double acc = 0.0;
 #pragma unroll
-    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[c * Q1 + m], x[base + m], acc);
+    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[0][c * Q1 + m], x[base + m], acc);
     y[C] = acc;
   }
 #pragma unroll
@@ -332,7 +340,7 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
     const int c = (C / Q1) % Q1, base = C - c * Q1;
     double acc = 0.0;
 #pragma unroll
-    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[c * Q1 + m], y[base + m * Q1], acc);
+    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[1][c * Q1 + m], y[base + m * Q1], acc);
     x[C] = acc;
   }
   if (D == 3) {
@@ -341,7 +349,7 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
       const int c = C / (Q1 * Q1), base = C - c * Q1 * Q1;
       double acc = 0.0;
 #pragma unroll
-      for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[c * Q1 + m], x[base + m * Q1 * Q1], acc);
+      for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[2][c * Q1 + m], x[base + m * Q1 * Q1], acc);
       y[C] = acc;
     }
   }
@@ -357,24 +365,39 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
 }
 
 // shared memory of the one-CTA-per-tile macro kernels (K2 projection path, K5b):
-// two ns×d⁴ buffers (+ ∂S/∂J ns×d² for K5b) and the ns node geometries, ns = m^d
-size_t macro_smem_bytes(int d, int q, int m, bool reverse) {
-  (void)q;
-  const size_t ns = d == 2 ? (size_t)m * m : (size_t)m * m * m, nc = (size_t)d * d * d * d;
+// two ns×d⁴ buffers (+ ∂S/∂J ns×d² for K5b) and the ns node geometries, ns = Π m_k
+size_t macro_smem_bytes(int d, int ns_, bool reverse) {
+  const size_t ns = (size_t)ns_, nc = (size_t)d * d * d * d;
   const size_t geo = d == 2 ? sizeof(NodeGeo<2>) : sizeof(NodeGeo<3>);
   return sizeof(double) * (2 * ns * nc + (reverse ? ns * d * d : 0)) + ns * geo;
 }
 
-// K2 for (q+1)^d > 27 or an L2 projection with m > q+1 points (NEXT N2): one CTA per tile,
-// Ā sampled at the m^d Gauss nodes into shared memory, d projection passes.
+// compile-time n_π for an isotropic degree Q; Q = -1: anisotropic (runtime c_ip.npi)
+template <int D, int Q>
+__device__ __forceinline__ int npi_of(const InterpConst &c_ip) {
+  if constexpr (Q >= 0) return D == 2 ? (Q + 1) * (Q + 1) : (Q + 1) * (Q + 1) * (Q + 1);
+  else return c_ip.npi;
+}
+
+// Ŵ = Πᵀ W or coef = Π samples: compile-time passes when isotropic with m = q+1
+template <int D, int Q, bool TRANSPOSE, int NCOMP>
+__device__ const double *apply_projection(const InterpConst &c_ip, double *a, double *b) {
+  if constexpr (Q >= 0) {
+    if (c_ip.iso && c_ip.m == Q + 1) return tensor_apply<D, Q, TRANSPOSE, NCOMP>(c_ip, a, b);
+  }
+  return proj_apply<D, NCOMP>(c_ip, a, b, TRANSPOSE);
+}
+
+// K2 for (q+1)^d > 27, an L2 projection with m > q+1 points or anisotropic degrees (NEXT
+// N2): one CTA per tile, Ā sampled at the Π m_k Gauss nodes into shared memory, d passes.
 template <int D, int Q>
 __global__ void __launch_bounds__(256)
 k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl,
                     const double *__restrict__ mknots, const int *__restrict__ mspan, const double *__restrict__ young,
                     int ypt, double nu, double *__restrict__ coef, int kstride, int fm, int64_t n_tiles, int *flag) {
-  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
-  constexpr int DD = D * D, NC = DD * DD, NK = DD * NPI;
-  const int ns = D == 2 ? c_ip.m * c_ip.m : c_ip.m * c_ip.m * c_ip.m;
+  constexpr int DD = D * D, NC = DD * DD;
+  const int NPI = npi_of<D, Q>(c_ip), NK = DD * NPI;
+  const int ns = c_ip.ns;
   extern __shared__ double dyn[];
   double *S0 = dyn, *S1 = dyn + (size_t)ns * NC;
   NodeGeo<D> *geo = reinterpret_cast<NodeGeo<D> *>(dyn + 2 * (size_t)ns * NC);
@@ -397,7 +420,7 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
         o[a * D + b] = g.det * (lam * g.G[i][a] * g.G[j][b] + mu * g.G[j][a] * g.G[i][b] + (a == b ? mu * g.gg[i][j] : 0.0));
   }
   __syncthreads();
-  const double *res = c_ip.m == Q + 1 ? tensor_apply<D, Q, false, NC>(c_ip, S0, S1) : proj_apply<D, NC>(c_ip, S0, S1, false);
+  const double *res = apply_projection<D, Q, false, NC>(c_ip, S0, S1);
   for (int idx = threadIdx.x; idx < DD * NK; idx += blockDim.x) {
     const int ab = idx / NK, kap = idx % NK, ij = kap / NPI, C = kap % NPI;
     const int64_t n = t * DD + ab;
@@ -413,9 +436,9 @@ __global__ void __launch_bounds__(256)
 k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
             const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
             const double *__restrict__ W, int kstride, double *__restrict__ gpart, int *flag) {
-  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
-  constexpr int DD = D * D, NC = DD * DD, NK = DD * NPI;
-  const int m1 = c_ip.m, ns = D == 2 ? m1 * m1 : m1 * m1 * m1;
+  constexpr int DD = D * D, NC = DD * DD;
+  const int NPI = npi_of<D, Q>(c_ip), NK = DD * NPI;
+  const int ns = c_ip.ns;
   extern __shared__ double dyn[];
   double *S0 = dyn, *S1 = dyn + (size_t)ns * NC, *dSdJ = dyn + 2 * (size_t)ns * NC;
   NodeGeo<D> *geo = reinterpret_cast<NodeGeo<D> *>(dSdJ + (size_t)ns * DD);
@@ -430,7 +453,7 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
   __syncthreads();
   node_geometry<D>(c_ip, mt, geo, tg, flag);
   // Ŵ = Πᵀ W (also syncs geo)
-  const double *Wh_all = m1 == Q + 1 ? tensor_apply<D, Q, true, NC>(c_ip, S0, S1) : proj_apply<D, NC>(c_ip, S0, S1, true);
+  const double *Wh_all = apply_projection<D, Q, true, NC>(c_ip, S0, S1);
   double lam, mu;
   lame(young[ypt ? tg : 0], nu, lam, mu);
   for (int m = threadIdx.x; m < ns; m += blockDim.x) {
@@ -509,7 +532,7 @@ kv_tile(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctr
   __shared__ double sW[MAXNS], sdW[MAXNS][D];
   __shared__ double sd[(IGA_MAXQ + 1) * (IGA_MAXQ + 1) * (IGA_MAXQ + 1)];
   const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
-  const int q1 = c_ip.q + 1, m1 = c_ip.m, ns = D == 2 ? m1 * m1 : m1 * m1 * m1;
+  const int ns = c_ip.ns;
   load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
   __syncthreads();
   for (int m = threadIdx.x; m < ns; m += blockDim.x) {
@@ -523,13 +546,14 @@ kv_tile(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctr
     macro_W<D>(c_ip, mt, m, sW[m], sdW[m]);
   }
   __syncthreads();
-  // Π[C][m] = Π_k Pi1[c_k][m_k]
+  // Π[C][m] = Π_k Pi1[k][c_k][m_k]
   auto Pi = [&](int C, int m) {
     double v = 1.0;
     for (int k = 0; k < D; ++k) {
-      const int c = (C / (k == 0 ? 1 : (k == 1 ? q1 : q1 * q1))) % q1;
-      const int mk = (m / (k == 0 ? 1 : (k == 1 ? m1 : m1 * m1))) % m1;
-      v *= c_ip.Pi1[c * m1 + mk];
+      const int q1 = c_ip.qv[k] + 1, m1 = c_ip.mv[k];
+      v *= c_ip.Pi1[k][(C % q1) * m1 + m % m1];
+      C /= q1;
+      m /= m1;
     }
     return v;
   };
@@ -626,6 +650,136 @@ cudaError_t launch_load(const Handle &h, const double *b, double *f, cudaStream_
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------
+// A-priori projection error (Eq. 59, sampled as on P:362-364):
+//   e_t = max_{ξ ∈ S} ‖Ā(ξ) − Π^H Ā(ξ)‖_F / ‖Ā(ξ)‖_F,   S = n_s^d equispaced points (R18).
+// One CTA per tile.  Per component block ij (d² components a,b at a time): Ā at the
+// projection nodes -> coefficients (the K2 passes) -> Π^H Ā at the samples (d evaluation
+// passes with B_c^{q_k}(x_s)) -> squared differences accumulated per sample in a fixed
+// order; the tile value is an exact max.  Ā ∝ E, so E = 1.
+// c_ip: projection (nodes, Π1); c_sm: the same macro tile sampled at S; c_ev: evaluation
+// matrices in the Pi1 slots, stored as a (n_s × (q_k+1)) "projection" (qv = n_s-1, mv = q_k+1).
+template <int D>
+__global__ void __launch_bounds__(256)
+kp_error(const __grid_constant__ InterpConst c_ip, const __grid_constant__ InterpConst c_sm,
+         const __grid_constant__ InterpConst c_ev, const double *__restrict__ ctrl, const double *__restrict__ mknots,
+         const int *__restrict__ mspan, double nu, double *__restrict__ e_tile, int *flag) {
+  constexpr int DD = D * D;
+  const int ns = c_ip.ns, nss = c_sm.ns;
+  const int nbuf = max(max(ns, c_ip.npi), nss);
+  extern __shared__ double dyn[];
+  double *gN = dyn;                                   // [ns][1 + DD]: det, G
+  double *gS = gN + (size_t)ns * (1 + DD);            // [nss][1 + DD]
+  double *S0 = gS + (size_t)nss * (1 + DD), *S1 = S0 + (size_t)nbuf * DD;
+  double *num2 = S1 + (size_t)nbuf * DD, *den2 = num2 + nss;
+  __shared__ MacroTile<D> mt, mts;
+  __shared__ double red[256];
+  const int64_t t = blockIdx.x;
+  load_macro_tile<D>(c_ip, mt, t, ctrl, mknots, mspan);
+  load_macro_tile<D>(c_sm, mts, t, ctrl, mknots, mspan);
+  __syncthreads();
+  for (int m = threadIdx.x; m < ns + nss; m += blockDim.x) {
+    const bool node = m < ns;
+    const int k = node ? m : m - ns;
+    double J[D][D], G[D][D];
+    if (node) macro_J<D>(c_ip, mt, k, J); else macro_J<D>(c_sm, mts, k, J);
+    const double det = det_inv<D>(J, G);
+    if (!(det > 0.0)) raise_flag(flag, 2, (int)t, k);
+    double *o = (node ? gN : gS) + (size_t)k * (1 + DD);
+    o[0] = det;
+    for (int i = 0; i < D; ++i)
+      for (int j = 0; j < D; ++j) o[1 + i * D + j] = G[i][j];
+    if (!node) { num2[k] = 0.0; den2[k] = 0.0; }
+  }
+  __syncthreads();
+  double lam, mu;
+  lame(1.0, nu, lam, mu);
+  // Ā_ij[a,b] (Eq. 37, closed form) from (det, G)
+  auto Abar = [&](const double *g, int i, int j, int a, int b) {
+    const double *G = g + 1;
+    double gg = 0.0;
+    for (int c = 0; c < D; ++c) gg += G[i * D + c] * G[j * D + c];
+    return g[0] * (lam * G[i * D + a] * G[j * D + b] + mu * G[j * D + a] * G[i * D + b] + (a == b ? mu * gg : 0.0));
+  };
+  for (int ij = 0; ij < DD; ++ij) {
+    const int i = ij / D, j = ij % D;
+    for (int it = threadIdx.x; it < ns * DD; it += blockDim.x) {
+      const int m = it / DD, ab = it % DD;
+      S0[it] = Abar(gN + (size_t)m * (1 + DD), i, j, ab / D, ab % D);
+    }
+    __syncthreads();
+    double *coef = const_cast<double *>(proj_apply<D, DD>(c_ip, S0, S1, false));   // [npi][DD]
+    double *other = coef == S0 ? S1 : S0;
+    const double *val = proj_apply<D, DD>(c_ev, coef, other, false);                // [nss][DD]
+    for (int sp = threadIdx.x; sp < nss; sp += blockDim.x) {
+      const double *g = gS + (size_t)sp * (1 + DD);
+      double n2 = num2[sp], d2 = den2[sp];
+      for (int ab = 0; ab < DD; ++ab) {
+        const double ex = Abar(g, i, j, ab / D, ab % D), df = ex - val[sp * DD + ab];
+        n2 = fma(df, df, n2);
+        d2 = fma(ex, ex, d2);
+      }
+      num2[sp] = n2;
+      den2[sp] = d2;
+    }
+    __syncthreads();
+  }
+  double e = 0.0;
+  for (int sp = threadIdx.x; sp < nss; sp += blockDim.x) e = fmax(e, sqrt(num2[sp]) / sqrt(den2[sp]));
+  red[threadIdx.x] = e;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) e_tile[t] = red[0];
+}
+
+size_t projection_error_smem_bytes(int d, int ns, int n_s, int npi) {
+  const size_t dd = (size_t)d * d, nss = d == 2 ? (size_t)n_s * n_s : (size_t)n_s * n_s * n_s;
+  const size_t nbuf = std::max(std::max((size_t)ns, (size_t)npi), nss);
+  return sizeof(double) * ((ns + nss) * (1 + dd) + 2 * nbuf * dd + 2 * nss);
+}
+
+cudaError_t launch_projection_error(const Handle &h, const double *ctrl, double nu, int n_s, double *e_tile,
+                                    cudaStream_t s) {
+  const InterpConst ic = make_interp_const(h);
+  InterpConst sm = ic, ev = ic;
+  int nss = 1;
+  for (int k = 0; k < 3; ++k) {
+    const bool act = k < h.d;
+    sm.mv[k] = act ? n_s : 1;
+    ev.qv[k] = act ? n_s - 1 : 0;       // output points of the evaluation pass
+    ev.mv[k] = act ? h.qv[k] + 1 : 1;   // input coefficients
+    for (int i = 0; i < IGA_MAXM; ++i) sm.x[k][i] = act && i < n_s ? (double)i / (n_s - 1) : 0.0;
+    for (int i = 0; i < (IGA_MAXQ + 1) * IGA_MAXM; ++i) ev.Pi1[k][i] = 0.0;
+    if (!act) { ev.Pi1[k][0] = 1.0; continue; }
+    nss *= n_s;
+    const int q = h.qv[k];
+    for (int sp = 0; sp < n_s; ++sp) {
+      const double x = (double)sp / (n_s - 1);
+      for (int c = 0; c <= q; ++c) {
+        double b = 1.0;
+        for (int r = 1; r <= c; ++r) b = b * (q - c + r) / r;
+        ev.Pi1[k][sp * (q + 1) + c] = b * std::pow(x, c) * std::pow(1.0 - x, q - c);
+      }
+    }
+  }
+  sm.ns = nss;
+  ev.ns = nss;
+  const size_t smem = projection_error_smem_bytes(h.d, h.ns, n_s, h.npi);
+  if (h.d == 2) {
+    cudaError_t e = cudaFuncSetAttribute(kp_error<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    kp_error<2><<<(unsigned)h.n_tiles, 256, smem, s>>>(ic, sm, ev, ctrl, h.d_mknots, h.d_mspan, nu, e_tile, h.d_flag);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(kp_error<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    kp_error<3><<<(unsigned)h.n_tiles, 256, smem, s>>>(ic, sm, ev, ctrl, h.d_mknots, h.d_mspan, nu, e_tile, h.d_flag);
+  }
+  return cudaGetLastError();
+}
+
 template <int D>
 __global__ void k5c_reduce(const __grid_constant__ InterpConst c_ip, const int *__restrict__ mspan, const double *__restrict__ gpart, int nact,
                            int64_t n_cp, double *__restrict__ grad) {
@@ -667,9 +821,9 @@ __global__ void k5c_reduce(const __grid_constant__ InterpConst c_ip, const int *
 template <int D, int Q>
 static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
                              double *coef, bool fm, cudaStream_t s) {
-  using S = K2Shape<D, Q>;
-  if constexpr (S::REG) {
-    if (h.m_proj == Q + 1) {   // interpolation: register path (else L2 projection, m > q+1)
+  if constexpr (Q >= 0 && K2Shape<D, (Q >= 0 ? Q : 0)>::REG) {
+    using S = K2Shape<D, Q>;
+    if (h.iso && h.mv[0] == Q + 1) {   // interpolation: register path (else L2 projection, m > q+1)
       const unsigned grid = (unsigned)((h.n_tiles + S::TPB - 1) / S::TPB);
       k2_interpolate<D, Q><<<grid, S::THREADS, 0, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt,
                                                        nu, coef, h.kstride, (int)fm, h.n_tiles, h.d_flag);
@@ -677,7 +831,7 @@ static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *
     }
   }
   {
-    const size_t sm = macro_smem_bytes(D, Q, h.m_proj, false);
+    const size_t sm = macro_smem_bytes(D, h.ns, false);
     cudaError_t e = cudaFuncSetAttribute(k2_interpolate_smem<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     k2_interpolate_smem<D, Q><<<(unsigned)h.n_tiles, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan,
@@ -690,7 +844,7 @@ static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *
 template <int D, int Q>
 static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
                               const double *W, double *gpart, cudaStream_t s) {
-  const size_t sm = macro_smem_bytes(D, Q, h.m_proj, true);
+  const size_t sm = macro_smem_bytes(D, h.ns, true);
   cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
@@ -698,8 +852,10 @@ static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double 
   return cudaGetLastError();
 }
 
-// dispatch on (d, q): every index of the macro kernels is a compile-time constant
+// dispatch on (d, q): every index of the macro kernels is a compile-time constant;
+// anisotropic degrees (Q = -1) take the runtime shared-memory path
 #define IGA_DISPATCH_DQ(F, ...)                                                          \
+  if (!h.iso) return h.d == 2 ? F<2, -1>(__VA_ARGS__) : F<3, -1>(__VA_ARGS__);           \
   switch (h.d * 10 + h.q) {                                                               \
     case 20: return F<2, 0>(__VA_ARGS__);                                                 \
     case 21: return F<2, 1>(__VA_ARGS__);                                                 \

@@ -17,7 +17,7 @@ __constant__ DevPatch c_patches[64];
 __constant__ double c_gx[16], c_gw[16];
 
 template <int D>
-__global__ void k1_point_data(int n_patches, int n_g, int p, int q, const double *__restrict__ tile_ctrl,
+__global__ void k1_point_data(int n_patches, int n_g, int p, int3 qv, const double *__restrict__ tile_ctrl,
                               const double *__restrict__ knots, const int *__restrict__ elspan, int total_pts,
                               double *__restrict__ wD, double *__restrict__ G, double *__restrict__ Nc,
                               double *__restrict__ Rv, int *flag) {
@@ -95,15 +95,16 @@ __global__ void k1_point_data(int n_patches, int n_g, int p, int q, const double
       Gp[la * D + a] = v;
     }
   }
-  const int q1 = q + 1;
+  // N_C(ξ) = Π_k B_{c_k}^{q_k}(ξ_k) with per-direction degrees (anisotropic Q)
+  const int q[3] = {qv.x, qv.y, qv.z};
   int npi = 1;
-  for (int k = 0; k < D; ++k) npi *= q1;
+  for (int k = 0; k < D; ++k) npi *= q[k] + 1;
   double B1[3][IGA_MAXQ + 1];
   for (int k = 0; k < D; ++k)
-    for (int c = 0; c <= q; ++c) B1[k][c] = bernstein1(q, c, xi[k]);
+    for (int c = 0; c <= q[k]; ++c) B1[k][c] = bernstein1(q[k], c, xi[k]);
   double *Np = Nc + (size_t)gp * npi;
   for (int C = 0; C < npi; ++C) {
-    int c[3] = {C % q1, (C / q1) % q1, C / (q1 * q1)};
+    int c[3] = {C % (q[0] + 1), (C / (q[0] + 1)) % (q[1] + 1), C / ((q[0] + 1) * (q[1] + 1))};
     double v = 1.0;
     for (int k = 0; k < D; ++k) v *= B1[k][c[k]];
     Np[C] = v;
@@ -111,7 +112,7 @@ __global__ void k1_point_data(int n_patches, int n_g, int p, int q, const double
 }
 
 template <int D>
-__global__ void k1_table_rows(int n_patches, int n_g, int p, int q, int nk, int kstride, int64_t M, int64_t ldT,
+__global__ void k1_table_rows(int n_patches, int n_g, int p, int npi, int nk, int kstride, int64_t M, int64_t ldT,
                               const int *__restrict__ row_patch, const int *__restrict__ pairA,
                               const int *__restrict__ pairB, const int *__restrict__ elspan,
                               const double *__restrict__ wD, const double *__restrict__ G,
@@ -122,9 +123,9 @@ __global__ void k1_table_rows(int n_patches, int n_g, int p, int q, int nk, int 
   int A = pairA[row] - P.ctrl_off, B = pairB[row] - P.ctrl_off;
   int a[3] = {A % P.n[0], (A / P.n[0]) % P.n[1], A / (P.n[0] * P.n[1])};
   int b[3] = {B % P.n[0], (B / P.n[0]) % P.n[1], B / (P.n[0] * P.n[1])};
-  const int n1 = p + 1, q1 = q + 1;
-  int nact = 1, npi = 1, ng_d = 1;
-  for (int k = 0; k < D; ++k) { nact *= n1; npi *= q1; ng_d *= n_g; }
+  const int n1 = p + 1;
+  int nact = 1, ng_d = 1;
+  for (int k = 0; k < D; ++k) { nact *= n1; ng_d *= n_g; }
   // element ranges per direction where both functions are nonzero: knot span s in
   // [max(a,b), min(a,b)+p]
   int elo[3], ehi[3];
@@ -259,18 +260,18 @@ cudaError_t launch_tables(const Handle &h, const DevPatch *dpatches, int n_patch
   if ((e = cudaMemcpyAsync(row_patch, rp.data(), sizeof(int) * h.M, cudaMemcpyHostToDevice, s))) return e;
   int threads = 128, blocks = (total_pts + threads - 1) / threads;
   if (h.d == 2)
-    k1_point_data<2><<<blocks, threads, 0, s>>>(n_patches, h.n_g, h.p, h.q, d_tile_ctrl, d_tile_knots, d_tile_elspan,
+    k1_point_data<2><<<blocks, threads, 0, s>>>(n_patches, h.n_g, h.p, make_int3(h.qv[0], h.qv[1], h.qv[2]), d_tile_ctrl, d_tile_knots, d_tile_elspan,
                                                 total_pts, wD, G, Nc, Rv, h.d_flag);
   else
-    k1_point_data<3><<<blocks, threads, 0, s>>>(n_patches, h.n_g, h.p, h.q, d_tile_ctrl, d_tile_knots, d_tile_elspan,
+    k1_point_data<3><<<blocks, threads, 0, s>>>(n_patches, h.n_g, h.p, make_int3(h.qv[0], h.qv[1], h.qv[2]), d_tile_ctrl, d_tile_knots, d_tile_elspan,
                                                 total_pts, wD, G, Nc, Rv, h.d_flag);
   if ((e = cudaGetLastError())) return e;
   int tpb = h.nk >= 256 ? 256 : 128;
   if (h.d == 2)
-    k1_table_rows<2><<<(unsigned)h.M, tpb, 0, s>>>(n_patches, h.n_g, h.p, h.q, h.nk, h.kstride, h.M, (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK, row_patch,
+    k1_table_rows<2><<<(unsigned)h.M, tpb, 0, s>>>(n_patches, h.n_g, h.p, h.npi, h.nk, h.kstride, h.M, (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK, row_patch,
                                                    h.d_pairA, h.d_pairB, d_tile_elspan, wD, G, Nc, h.d_table);
   else
-    k1_table_rows<3><<<(unsigned)h.M, tpb, 0, s>>>(n_patches, h.n_g, h.p, h.q, h.nk, h.kstride, h.M, (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK, row_patch,
+    k1_table_rows<3><<<(unsigned)h.M, tpb, 0, s>>>(n_patches, h.n_g, h.p, h.npi, h.nk, h.kstride, h.M, (h.M + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK, row_patch,
                                                    h.d_pairA, h.d_pairB, d_tile_elspan, wD, G, Nc, h.d_table);
   if ((e = cudaGetLastError())) return e;
   if (h.d == 2)
