@@ -47,30 +47,32 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 // KS k-steps (≤ 4) of a k-chunk of a warp's 16×72 tile; sA/sB are FM chunks, g0 = first
 // 8-row group of the warp in sA.  KS is a template parameter so that the loop is fully
 // unrolled and the fragment loads of step kk+1 are scheduled under the DMMAs of step kk.
-template <int KS>
+// MIC <= MI: only the first MIC 8-row groups (the rest of the warp's rows are padding)
+template <int KS, int MIC = MI>
 __device__ __forceinline__ void mma_chunk_fm(const double *__restrict__ sA, const double *__restrict__ sB, int g0,
                                              int lane, double (&acc)[MI][NI][2]) {
 #pragma unroll
   for (int kk = 0; kk < KS; ++kk) {
     double a[MI], b[NI];
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) a[mi] = sA[((g0 + mi) * 4 + kk) * 32 + lane];
+    for (int mi = 0; mi < MIC; ++mi) a[mi] = sA[((g0 + mi) * 4 + kk) * 32 + lane];
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) b[ni] = sB[(ni * 4 + kk) * 32 + lane];
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi)
+    for (int mi = 0; mi < MIC; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
   }
 }
 
+template <int MIC = MI>
 __device__ __forceinline__ void mma_chunk_tail(const double *__restrict__ sA, const double *__restrict__ sB, int g0,
                                                int lane, int ks, double (&acc)[MI][NI][2]) {
   switch (ks) {
-    case 1: mma_chunk_fm<1>(sA, sB, g0, lane, acc); break;
-    case 2: mma_chunk_fm<2>(sA, sB, g0, lane, acc); break;
-    case 3: mma_chunk_fm<3>(sA, sB, g0, lane, acc); break;
-    default: mma_chunk_fm<4>(sA, sB, g0, lane, acc); break;
+    case 1: mma_chunk_fm<1, MIC>(sA, sB, g0, lane, acc); break;
+    case 2: mma_chunk_fm<2, MIC>(sA, sB, g0, lane, acc); break;
+    case 3: mma_chunk_fm<3, MIC>(sA, sB, g0, lane, acc); break;
+    default: mma_chunk_fm<4, MIC>(sA, sB, g0, lane, acc); break;
   }
 }
 
@@ -165,13 +167,20 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  // 8-row groups of this warp that hold table rows < M (the rest is the zero padding of
+  // the last row block: no DMMA is issued for it)
+  const int nmi = m0 + warp * 16 >= M ? 0 : (m0 + warp * 16 + 8 >= M ? 1 : 2);
   for (int kc = 0; kc < nkc; ++kc) {
     const int st = kc % K3_STAGES;
     mbar_wait(&full[st], (kc / K3_STAGES) & 1);
-    if (kc + 1 < nkc)
-      mma_chunk_fm<BK / 4>(sA + st * K3_A_CHUNK, sB + st * K3_B_CHUNK, warp * MI, lane, acc);
-    else
-      mma_chunk_tail(sA + st * K3_A_CHUNK, sB + st * K3_B_CHUNK, warp * MI, lane, ksteps - kc * (BK / 4), acc);
+    const double *a_st = sA + st * K3_A_CHUNK, *b_st = sB + st * K3_B_CHUNK;
+    if (nmi == 2) {
+      if (kc + 1 < nkc) mma_chunk_fm<BK / 4>(a_st, b_st, warp * MI, lane, acc);
+      else mma_chunk_tail(a_st, b_st, warp * MI, lane, ksteps - kc * (BK / 4), acc);
+    } else if (nmi == 1) {
+      if (kc + 1 < nkc) mma_chunk_fm<BK / 4, 1>(a_st, b_st, warp * MI, lane, acc);
+      else mma_chunk_tail<1>(a_st, b_st, warp * MI, lane, ksteps - kc * (BK / 4), acc);
+    }
     __syncwarp();
     if (lane == 0) {   // the last warp to release a stage refills it
       __threadfence_block();
@@ -491,7 +500,7 @@ static_assert(sizeof(double) * BN * K5_WP <= K5_OFF_BAR, "W staging must fit in 
 // 16×72; warp 0 lane 0 refills the 4-stage ring once all warps released a stage.
 __global__ void __launch_bounds__(K5_THREADS, 1)
 k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nkc, int64_t N,
-          double *__restrict__ Wout, int kstride) {
+          double *__restrict__ Wout, int kstride, int nk) {
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K5_STAGES * K5_A_CHUNK;
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5_OFF_BAR);
@@ -499,6 +508,10 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t kb = blockIdx.x, nb = blockIdx.y;
   const double *gA = tabAT + kb * (int64_t)nkc * K5_A_CHUNK, *gB = X + nb * (int64_t)nkc * K5_B_CHUNK;
+  // 8-row groups of this warp that hold table columns κ < n_k (the rest is zero padding:
+  // 13 of 256 rows at q = 2, 64 of 640 at q = 3 — no DMMA is issued for them)
+  const int row0 = (int)kb * BM + warp * 16;
+  const int nmi = row0 >= nk ? 0 : (row0 + 8 >= nk ? 1 : 2);
   if (tid == 0) {
     for (int s = 0; s < K5_STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -523,7 +536,10 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   for (int kc = 0; kc < nkc; ++kc) {
     const int st = kc % K5_STAGES;
     mbar_wait(&full[st], (kc / K5_STAGES) & 1);
-    mma_chunk_fm<BK / 4>(sA + st * K5_A_CHUNK, sB + st * K5_B_CHUNK, warp * MI, lane, acc);
+    if (nmi == 2)
+      mma_chunk_fm<BK / 4>(sA + st * K5_A_CHUNK, sB + st * K5_B_CHUNK, warp * MI, lane, acc);
+    else if (nmi == 1)
+      mma_chunk_fm<BK / 4, 1>(sA + st * K5_A_CHUNK, sB + st * K5_B_CHUNK, warp * MI, lane, acc);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -580,7 +596,7 @@ cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s) {
   dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)((h.n_tiles_own * h.d * h.d + BN - 1) / BN));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   k5a_wgemm<<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), h.n_tiles_own * h.d * h.d, W,
-                                              h.kstride);
+                                              h.kstride, h.nk);
   return cudaGetLastError();
 }
 
