@@ -34,6 +34,45 @@ __device__ __forceinline__ void bspline_eval(const double *U, int p, int s, doub
   }
 }
 
+// the same values with every loop fully unrolled up to IGA_MAXP and guarded by p, so the
+// triangle lives in registers (no local-memory arrays); N, dN must hold IGA_MAXP+1 values
+__device__ __forceinline__ void bspline_eval_reg(const double *U, int p, int s, double u, double *N, double *dN) {
+  double left[IGA_MAXP + 1], right[IGA_MAXP + 1], Nd[IGA_MAXP + 1], Nm1[IGA_MAXP + 1];
+#pragma unroll
+  for (int r = 0; r <= IGA_MAXP; ++r) Nd[r] = Nm1[r] = left[r] = right[r] = 0.0;
+  Nd[0] = 1.0;
+  Nm1[0] = 1.0;
+#pragma unroll
+  for (int j = 1; j <= IGA_MAXP; ++j) {
+    if (j <= p) {
+      left[j] = u - U[s + 1 - j];
+      right[j] = U[s + j] - u;
+      double saved = 0.0;
+#pragma unroll
+      for (int r = 0; r < j; ++r) {
+        double temp = Nd[r] / (right[r + 1] + left[j - r]);
+        Nd[r] = saved + right[r + 1] * temp;
+        saved = left[j - r] * temp;
+      }
+      Nd[j] = saved;
+      if (j == p - 1) {
+#pragma unroll
+        for (int r = 0; r < j + 1; ++r) Nm1[r] = Nd[r];
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r <= IGA_MAXP; ++r) {
+    if (r <= p) {
+      N[r] = Nd[r];
+      const int i = s - p + r;
+      const double t1 = (r >= 1) ? Nm1[r - 1] / (U[i + p] - U[i]) : 0.0;
+      const double t2 = (r <= p - 1) ? Nm1[r] / (U[i + p + 1] - U[i + 1]) : 0.0;
+      dN[r] = p * (t1 - t2);
+    }
+  }
+}
+
 template <int D>
 __device__ __forceinline__ double det_inv(const double J[D][D], double G[D][D]) {
   if (D == 2) {

@@ -73,7 +73,7 @@ __device__ void load_macro_tile(const InterpConst &c_ip, MacroTile<D> &mt, int64
     int s = mspan[c_ip.soff[k] + e[k]];
     double h = U[s + 1] - U[s];
     double N[IGA_MAXP + 1], dN[IGA_MAXP + 1];
-    bspline_eval(U, c_ip.pm[k], s, U[s] + h * c_ip.x[k][m], N, dN);
+    bspline_eval_reg(U, c_ip.pm[k], s, U[s] + h * c_ip.x[k][m], N, dN);
     for (int r = 0; r <= c_ip.pm[k]; ++r) {
       mt.B1[k][m][r] = N[r];
       mt.D1[k][m][r] = dN[r] * h;
@@ -160,6 +160,62 @@ __device__ void macro_J(const InterpConst &c_ip, const MacroTile<D> &mt, int m, 
     for (int a = 0; a < D; ++a) {
       double x = mt.P[ra * D + a];
       for (int be = 0; be < D; ++be) J[a][be] += x * g[be];
+    }
+  }
+}
+
+// J at sample node m for a B-spline (non-rational) macro tile: nested loops over the
+// (p+1)^d active functions with the 1D values hoisted per direction (no div/mod per
+// control point); ∂_β N_r = Π_k (k == β ? D1 : B1)[k][m_k][r_k] (K2's hot loop)
+template <int D>
+__device__ __forceinline__ void macro_J_bspline(const InterpConst &c_ip, const MacroTile<D> &mt, int m, double J[D][D]) {
+  const int mm[3] = {m % c_ip.mv[0], (m / c_ip.mv[0]) % c_ip.mv[1], m / (c_ip.mv[0] * c_ip.mv[1])};
+  const int n0 = c_ip.pm[0] + 1, n1 = c_ip.pm[1] + 1, n2 = D == 3 ? c_ip.pm[2] + 1 : 1;
+  const double *B0 = mt.B1[0][mm[0]], *D0 = mt.D1[0][mm[0]];
+  const double *B1 = mt.B1[1][mm[1]], *D1 = mt.D1[1][mm[1]];
+  const double *B2 = mt.B1[D - 1][mm[D - 1]], *D2 = mt.D1[D - 1][mm[D - 1]];
+  for (int a = 0; a < D; ++a)
+    for (int b = 0; b < D; ++b) J[a][b] = 0.0;
+  const double *P = mt.P;
+  for (int r2 = 0; r2 < n2; ++r2) {
+    const double b2 = D == 3 ? B2[r2] : 1.0, d2 = D == 3 ? D2[r2] : 0.0;
+    for (int r1 = 0; r1 < n1; ++r1) {
+      const double b12 = B1[r1] * b2, d12 = D1[r1] * b2, b1d2 = B1[r1] * d2;
+      for (int r0 = 0; r0 < n0; ++r0, P += D) {
+        const double b0 = B0[r0], g0 = D0[r0] * b12, g1 = b0 * d12, g2 = b0 * b1d2;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const double x = P[a];
+          J[a][0] = fma(x, g0, J[a][0]);
+          J[a][1] = fma(x, g1, J[a][1]);
+          if (D == 3) J[a][D - 1] = fma(x, g2, J[a][D - 1]);
+        }
+      }
+    }
+  }
+}
+
+// column β of J at sample node m for a B-spline macro tile: col[a] = Σ_r P_r[a] ∂_β N_r
+template <int D>
+__device__ __forceinline__ void macro_Jcol_bspline(const InterpConst &c_ip, const MacroTile<D> &mt, int m, int be,
+                                                   double col[D]) {
+  const int mm[3] = {m % c_ip.mv[0], (m / c_ip.mv[0]) % c_ip.mv[1], m / (c_ip.mv[0] * c_ip.mv[1])};
+  const int n0 = c_ip.pm[0] + 1, n1 = c_ip.pm[1] + 1, n2 = D == 3 ? c_ip.pm[2] + 1 : 1;
+  const double *F0 = be == 0 ? mt.D1[0][mm[0]] : mt.B1[0][mm[0]];
+  const double *F1 = be == 1 ? mt.D1[1][mm[1]] : mt.B1[1][mm[1]];
+  const double *F2 = be == D - 1 && D == 3 ? mt.D1[D - 1][mm[D - 1]] : mt.B1[D - 1][mm[D - 1]];
+#pragma unroll
+  for (int a = 0; a < D; ++a) col[a] = 0.0;
+  const double *P = mt.P;
+  for (int r2 = 0; r2 < n2; ++r2) {
+    const double f2 = D == 3 ? F2[r2] : 1.0;
+    for (int r1 = 0; r1 < n1; ++r1) {
+      const double f12 = F1[r1] * f2;
+      for (int r0 = 0; r0 < n0; ++r0, P += D) {
+        const double g = F0[r0] * f12;
+#pragma unroll
+        for (int a = 0; a < D; ++a) col[a] = fma(P[a], g, col[a]);
+      }
     }
   }
 }
@@ -299,10 +355,25 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   const int64_t tg = t + c_ip.t_base;   // global tile id (macro element, E, error report)
   if (live) load_macro_tile<D>(c_ip, mt[tl], tg, ctrl, mknots, mspan, comp, NC);
   __syncthreads();
+  // ∇F at the nodes: B-spline maps one column J[:, β] per thread (NPI·D threads of the
+  // tile, staged in the node's G slot), then det / J⁻¹ per node; NURBS maps the whole
+  // quotient-rule J per node
+  if (live && !mt[tl].rational)
+    for (int w = comp; w < NPI * D; w += NC) {
+      const int m = w / D, be = w % D;
+      double col[D];
+      macro_Jcol_bspline<D>(c_ip, mt[tl], m, be, col);
+#pragma unroll
+      for (int a = 0; a < D; ++a) geo[tl][m].G[a][be] = col[a];
+    }
+  __syncthreads();
   if (live)
     for (int m = comp; m < NPI; m += NC) {
       double J[D][D], G[D][D];
-      macro_J<D>(c_ip, mt[tl], m, J);
+      if (mt[tl].rational) macro_J<D>(c_ip, mt[tl], m, J);
+      else
+        for (int a = 0; a < D; ++a)
+          for (int be = 0; be < D; ++be) J[a][be] = geo[tl][m].G[a][be];
       const double det = det_inv<D>(J, G);
       if (!(det > 0.0)) raise_flag(flag, 2, (int)tg, m);
       NodeGeo<D> &o = geo[tl][m];
@@ -320,47 +391,50 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   double lam, mu;
   lame(young[ypt ? tg : 0], nu, lam, mu);
   const int ij = comp / DD, ab = comp % DD, i = ij / D, j = ij % D, a = ab / D, b = ab % D;
-  double x[NPI], y[NPI];
+  double x[NPI];
 #pragma unroll
   for (int m = 0; m < NPI; ++m) {
     const NodeGeo<D> &g = geo[tl][m];
     x[m] = g.det * (lam * g.G[i][a] * g.G[j][b] + mu * g.G[j][a] * g.G[i][b] + (a == b ? mu * g.gg[i][j] : 0.0));
   }
-  // direction 0, 1 (, 2): out[c] = Σ_m Π1[c][m] in[m] along the direction
+  // direction 0, 1 (, 2), in place one line of Q1 values at a time (few live registers):
+  // out[c] = Σ_m Π1[dir][c][m] in[m] along the direction
 #pragma unroll
-  for (int C = 0; C < NPI; ++C) {
-    const int c = C % Q1, base = C - c;
-    double acc = 0.0;
+  for (int dir = 0; dir < D; ++dir) {
+    constexpr int L = NPI / Q1;
+    const int stride = dir == 0 ? 1 : (dir == 1 ? Q1 : Q1 * Q1);
 #pragma unroll
-    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[0][c * Q1 + m], x[base + m], acc);
-    y[C] = acc;
-  }
+    for (int l = 0; l < L; ++l) {
+      const int base = dir == 0 ? l * Q1 : (dir == 1 ? (l % Q1) + (l / Q1) * Q1 * Q1 : l);
+      double v[Q1];
 #pragma unroll
-  for (int C = 0; C < NPI; ++C) {
-    const int c = (C / Q1) % Q1, base = C - c * Q1;
-    double acc = 0.0;
+      for (int m = 0; m < Q1; ++m) v[m] = x[base + m * stride];
 #pragma unroll
-    for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[1][c * Q1 + m], y[base + m * Q1], acc);
-    x[C] = acc;
-  }
-  if (D == 3) {
+      for (int c = 0; c < Q1; ++c) {
+        double acc = 0.0;
 #pragma unroll
-    for (int C = 0; C < NPI; ++C) {
-      const int c = C / (Q1 * Q1), base = C - c * Q1 * Q1;
-      double acc = 0.0;
-#pragma unroll
-      for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[2][c * Q1 + m], x[base + m * Q1 * Q1], acc);
-      y[C] = acc;
+        for (int m = 0; m < Q1; ++m) acc = fma(c_ip.Pi1[dir][c * Q1 + m], v[m], acc);
+        x[base + c * stride] = acc;
+      }
     }
   }
-  const double *res = D == 3 ? y : x;
+  const double *res = x;
   // coefficient row n = t*DD + ab, column κ = ij*npi + C: row-major coef[n*kstride + κ]
-  // (parity accessor) or the fragment-major K3 B operand (fm_index, BR = IGA_GEMM_BN)
+  // (parity accessor) or the fragment-major K3 B operand (fm_index, BR = IGA_GEMM_BN) with
+  // the row part hoisted and 32-bit column offsets
   const int64_t n = t * DD + ab;
+  if (fm) {
+    const int64_t rb = n / IGA_GEMM_BN;
+    const int rr = (int)(n - rb * IGA_GEMM_BN);
+    double *base = coef + rb * (int64_t)kstride * IGA_GEMM_BN + (rr & ~7) * 16 + ((rr & 7) << 2);
 #pragma unroll
-  for (int C = 0; C < NPI; ++C) {
-    const int kap = ij * NPI + C;
-    coef[fm ? fm_index(n, kap, IGA_GEMM_BN, kstride / IGA_KCHUNK) : n * kstride + kap] = res[C];
+    for (int C = 0; C < NPI; ++C) {
+      const int k = ij * NPI + C;
+      base[(k >> 4) * (IGA_GEMM_BN * 16) + ((k >> 2) & 3) * 32 + (k & 3)] = res[C];
+    }
+  } else {
+#pragma unroll
+    for (int C = 0; C < NPI; ++C) coef[n * kstride + ij * NPI + C] = res[C];
   }
 }
 
