@@ -111,6 +111,27 @@ __device__ __forceinline__ double bernstein1(int q, int k, double x) {
   return r;
 }
 
+// ---- Eq. 38 (Ā_ij[a,b] = Ā_ji[b,a]) reduced contraction ("sym" layout) ----
+// Part 1 pairs / outputs: the d(d+1)/2 index pairs (a,b), a <= b, diagonal first then
+// (0,1), (0,2), (1,2); part 2: the d(d-1)/2 pairs a < b in the same order.
+__host__ __device__ __forceinline__ int sym_index(int D, int a, int b) {   // a <= b
+  return a == b ? a : (D == 2 ? 2 : (a == 0 ? 2 + b : 5));
+}
+__host__ __device__ __forceinline__ int anti_index(int D, int a, int b) {  // a < b
+  return D == 2 ? 0 : (a == 0 ? b - 1 : 2);
+}
+__host__ __device__ __forceinline__ void sym_pair(int D, int o, int &a, int &b) {
+  if (o < D) { a = b = o; return; }
+  if (D == 2) { a = 0; b = 1; return; }
+  a = o == 5 ? 1 : 0;
+  b = o == 3 ? 1 : 2;
+}
+__host__ __device__ __forceinline__ void anti_pair(int D, int o, int &a, int &b) {
+  if (D == 2) { a = 0; b = 1; return; }
+  a = o == 2 ? 1 : 0;
+  b = o == 0 ? 1 : 2;
+}
+
 // record the first degeneracy (flag[0] = code, flag[1] = tile/patch, flag[2] = node/point)
 __device__ __forceinline__ void raise_flag(int *flag, int code, int a, int b) {
   if (atomicCAS(flag, 0, code) == 0) {

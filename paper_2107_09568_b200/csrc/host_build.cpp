@@ -211,6 +211,17 @@ iga_status set_degrees(Handle &h, const int *q) {
   }
   h.nk = h.d * h.d * h.npi;
   h.kstride = (h.nk + IGA_KCHUNK - 1) / IGA_KCHUNK * IGA_KCHUNK;
+  // Eq. 38-reduced contraction layout
+  auto up = [](int x, int m) { return (x + m - 1) / m * m; };
+  h.n_p1 = h.d * (h.d + 1) / 2;
+  h.n_p2 = h.d * (h.d - 1) / 2;
+  h.tpc = h.d == 3 ? 8 : 16;
+  const int k1 = up(h.n_p1 * h.npi, 4), k2 = up(h.n_p2 * h.npi, 4);
+  h.k3_split = k1 / 4;
+  h.k3_steps = (k1 + k2) / 4;
+  h.ks3 = up(k1 + k2, IGA_KCHUNK);
+  h.k5_split = up(h.n_p1 * h.npi, 8);
+  h.k5_kap = h.k5_split + up(h.n_p2 * h.npi, 8);
   return IGA_OK;
 }
 
@@ -586,7 +597,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
 
   // ---- operand layouts: K3 A rows, coefficient rows, K5a padded reduction columns --
   h.Mpad = (h.M + IGA_K3_BM - 1) / IGA_K3_BM * IGA_K3_BM;
-  h.Npad = (lnt * d * d + IGA_GEMM_BN - 1) / IGA_GEMM_BN * IGA_GEMM_BN;
+  h.Npad = (lnt + h.tpc - 1) / h.tpc * IGA_GEMM_BN;   // blocks of tpc tiles (sym layout)
   h.pcol.assign(n_patches + 1, 0);
   h.max_patch_ctrl = 0;
   for (int pi = 0; pi < n_patches; ++pi) {
@@ -663,7 +674,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     }
   }
   // K5a CTA height IGA_K3_BM κ rows
-  h.k5_rows = (h.kstride + IGA_K5_BM - 1) / IGA_K5_BM * IGA_K5_BM;
+  h.k5_rows = (h.k5_kap + IGA_K5_BM - 1) / IGA_K5_BM * IGA_K5_BM;
   if (k5x_smem_bytes(d, h.max_patch_ctrl) > 227 * 1024) { set_error("tile patch too large for the K5 shared-memory staging (%d control points)", h.max_patch_ctrl); return IGA_ELIMIT; }
 
   // ---- projection operator (R1: interpolation at the q_k+1 Gauss nodes) -----------

@@ -205,19 +205,18 @@ iga_status iga_build_tables_q(const iga_spline *tile_patches, int32_t n_patches,
   if (st != IGA_OK) return fail(st);
   h.on_device = true;
   const int d = h.d;
-  const int64_t N = h.n_tiles * d * d;
   CUB(cudaMalloc((void **)&h.d_flag, 4 * sizeof(int)));
   CUB(cudaMemsetAsync(h.d_flag, 0, 4 * sizeof(int), s));
   CUB(cudaMalloc((void **)&h.d_table, sizeof(double) * h.M * h.kstride));
   CUB(cudaMemsetAsync(h.d_table, 0, sizeof(double) * h.M * h.kstride, s));
   // fragment-major operands; the zero padding (rows, κ >= n_k, patch columns) is never rewritten
-  CUB(cudaMalloc((void **)&h.d_tabA, sizeof(double) * h.Mpad * h.kstride));
-  CUB(cudaMemsetAsync(h.d_tabA, 0, sizeof(double) * h.Mpad * h.kstride, s));
+  CUB(cudaMalloc((void **)&h.d_tabA, sizeof(double) * h.Mpad * h.ks3));
+  CUB(cudaMemsetAsync(h.d_tabA, 0, sizeof(double) * h.Mpad * h.ks3, s));
   CUB(cudaMalloc((void **)&h.d_tabAT, sizeof(double) * h.k5_rows * h.Kp));
   CUB(cudaMemsetAsync(h.d_tabAT, 0, sizeof(double) * h.k5_rows * h.Kp, s));
-  CUB(cudaMalloc((void **)&h.d_coef, sizeof(double) * h.Npad * h.kstride));
-  CUB(cudaMemsetAsync(h.d_coef, 0, sizeof(double) * h.Npad * h.kstride, s));
-  CUB(cudaMalloc((void **)&h.d_W, sizeof(double) * N * h.kstride));
+  CUB(cudaMalloc((void **)&h.d_coef, sizeof(double) * h.Npad * h.ks3));
+  CUB(cudaMemsetAsync(h.d_coef, 0, sizeof(double) * h.Npad * h.ks3, s));
+  CUB(cudaMalloc((void **)&h.d_W, sizeof(double) * h.Npad * h.k5_rows));
   CUB(cudaMalloc((void **)&h.d_F, sizeof(double) * h.n_local_ctrl * h.npi));
   CUB(cudaMalloc((void **)&h.d_th, sizeof(double) * h.npi));
   CUB(cudaMalloc((void **)&h.d_det, sizeof(double) * h.n_tiles * h.npi));

@@ -94,8 +94,18 @@ struct Handle {
   std::vector<uint8_t> slot_tr;      // [n_slots] 1 = slot holds the (J,I)-oriented block
   // operand layouts (fragment-major, device_common.cuh fm_index)
   int64_t Mpad = 0;                  // rows of d_tabA (multiple of IGA_K3_BM)
-  int64_t Npad = 0;                  // rows of d_coef (multiple of IGA_GEMM_BN)
+  int64_t Npad = 0;                  // rows of d_coef / d_X (IGA_GEMM_BN per block of tpc tiles)
   int64_t k5_rows = 0;               // κ rows of d_tabAT (multiple of IGA_K5_BM)
+  // Eq. 38-reduced contraction (device_common.cuh sym_index): the GEMM
+  // columns are part 1 = P1 pairs × n_π (T_ii, T_ij + T_ji) against the symmetric outputs
+  // and part 2 = P2 pairs × n_π (T_ij − T_ji) against the antisymmetric ones; an N-block
+  // holds tpc tiles, block column n = o*tpc + tl (o < n_p1: symmetric output o, else the
+  // antisymmetric output o - n_p1)
+  int n_p1 = 0, n_p2 = 0;            // d(d+1)/2, d(d-1)/2
+  int tpc = 8;                       // tiles per N-block: 8 (3D), 16 (2D)
+  int ks3 = 0;                       // K3 k stride of d_tabA / d_coef (multiple of 16)
+  int k3_split = 0, k3_steps = 0;    // K3 k-step where part 2 starts; k-steps (parts padded to 4)
+  int k5_split = 0, k5_kap = 0;      // K5a κ row where part 2 starts; rows used (parts padded to 8)
   int64_t Kp = 0;                    // K5a reduction length: table rows, each patch padded to 16
   int max_patch_ctrl = 0;
   std::vector<int32_t> pcol;         // [n_patches+1] first padded column of each patch
@@ -120,11 +130,11 @@ struct Handle {
   double Pi1[3][(IGA_MAXQ + 1) * IGA_MAXM];
   // device buffers
   double *d_table = nullptr;     // [M][kstride] row-major (K1 output, accessor)
-  double *d_tabA = nullptr;      // FM [Mpad][kstride], BR = IGA_K3_BM (K3 A operand)
-  double *d_tabAT = nullptr;     // FM [k5_rows][Kp], BR = IGA_K5_BM (K5a A operand)
-  double *d_coef = nullptr;      // FM [Npad][kstride], BR = IGA_GEMM_BN (K3 B operand)
+  double *d_tabA = nullptr;      // FM [Mpad][ks3], BR = IGA_K3_BM (K3 A operand, sym columns)
+  double *d_tabAT = nullptr;     // FM [k5_rows][Kp], BR = IGA_K5_BM (K5a A operand, sym rows)
+  double *d_coef = nullptr;      // FM [Npad][ks3], BR = IGA_GEMM_BN (K3 B operand, sym coefficients)
   double *d_side = nullptr;      // [n_slots][d*d] multi-contribution blocks (K3 -> K4)
-  double *d_W = nullptr;         // [N][kstride]
+  double *d_W = nullptr;         // [Npad][k5_rows] K5a output Y (block column order, sym κ rows)
   double *d_X = nullptr;         // FM [Npad][Kp], BR = IGA_GEMM_BN (K5a B operand, from u, v)
   double *d_gpart = nullptr;     // [n_tiles][n_el_cp][d]
   int32_t *d_node_map = nullptr;

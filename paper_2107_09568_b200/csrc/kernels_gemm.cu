@@ -76,6 +76,65 @@ __device__ __forceinline__ void mma_chunk_tail(const double *__restrict__ sA, co
   }
 }
 
+// Eq. 38-reduced contraction: the GEMM columns are part 1 (P1 pairs × n_π,
+// against the symmetric outputs = DMMA column tiles [0, 6)) then part 2 (P2 pairs × n_π,
+// against the antisymmetric outputs = column tiles [6, NE), NE = 9 in 3D, 8 in 2D).
+// KS k-steps from step kk0 of a chunk, row groups [MI0, MI0 + MIC), column tiles [LO, HI).
+template <int KS, int MI0, int MIC, int LO, int HI>
+__device__ __forceinline__ void mma_steps(const double *__restrict__ sA, const double *__restrict__ sB, int g0,
+                                          int lane, int kk0, double (&acc)[MI][NI][2]) {
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int k = kk0 + kk;
+    double a[MI], b[NI];
+#pragma unroll
+    for (int mi = MI0; mi < MI0 + MIC; ++mi) a[mi] = sA[((g0 + mi) * 4 + k) * 32 + lane];
+#pragma unroll
+    for (int ni = LO; ni < HI; ++ni) b[ni] = sB[(ni * 4 + k) * 32 + lane];
+#pragma unroll
+    for (int mi = MI0; mi < MI0 + MIC; ++mi)
+#pragma unroll
+      for (int ni = LO; ni < HI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+  }
+}
+
+template <int MI0, int MIC, int LO, int HI>
+__device__ __forceinline__ void mma_steps_n(const double *__restrict__ sA, const double *__restrict__ sB, int g0,
+                                            int lane, int kk0, int n, double (&acc)[MI][NI][2]) {
+  switch (n) {
+    case 1: mma_steps<1, MI0, MIC, LO, HI>(sA, sB, g0, lane, kk0, acc); break;
+    case 2: mma_steps<2, MI0, MIC, LO, HI>(sA, sB, g0, lane, kk0, acc); break;
+    case 3: mma_steps<3, MI0, MIC, LO, HI>(sA, sB, g0, lane, kk0, acc); break;
+    case 4: mma_steps<4, MI0, MIC, LO, HI>(sA, sB, g0, lane, kk0, acc); break;
+    default: break;
+  }
+}
+
+// one K3 chunk: ns k-steps of which [0, j) belong to part 1 and [j, ns) to part 2
+template <int MIC, int NE>
+__device__ __forceinline__ void k3_chunk(const double *__restrict__ sA, const double *__restrict__ sB, int g0, int lane,
+                                         int ns, int j, double (&acc)[MI][NI][2]) {
+  if (j >= 4 && ns == 4) {
+    mma_steps<4, 0, MIC, 0, 6>(sA, sB, g0, lane, 0, acc);
+  } else if (j == 0 && ns == 4) {
+    mma_steps<4, 0, MIC, 6, NE>(sA, sB, g0, lane, 0, acc);
+  } else {
+    mma_steps_n<0, MIC, 0, 6>(sA, sB, g0, lane, 0, j < ns ? j : ns, acc);
+    if (j < ns) mma_steps_n<0, MIC, 6, NE>(sA, sB, g0, lane, j, ns - j, acc);
+  }
+}
+
+// L_t[a][b] of tile tl from a staged row of the sym-layout output (column o*TPC + tl):
+// L⁺'_ab + L⁻'_ab (a < b), L⁺'_ba − L⁻'_ba (a > b), L⁺'_aa (a = b)
+template <int D>
+__device__ __forceinline__ double lval(const double *row, int tl, int a, int b) {
+  constexpr int TPC = D == 3 ? 8 : 16, NP1 = D * (D + 1) / 2;
+  if (a == b) return row[a * TPC + tl];
+  const int lo = a < b ? a : b, hi = a < b ? b : a;
+  const double sp = row[sym_index(D, lo, hi) * TPC + tl], am = row[(NP1 + anti_index(D, lo, hi)) * TPC + tl];
+  return a < b ? sp + am : sp - am;
+}
+
 // one d-double row segment of a CSR block row: the 16-B aligned pair goes out as one
 // 128-bit store (2 store instructions per 3D row instead of 3)
 template <int D>
@@ -129,11 +188,12 @@ struct ApplyArgs {
 // EPI = 2: matrix-free apply y = K^π u (Eq. 74): block products summed into partial slots
 template <int D, int EPI>
 __global__ void __launch_bounds__(K3_THREADS, 4)
-k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int64_t M,
+k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int ksplit, int64_t M,
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
             int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm, const ApplyArgs ap) {
-  constexpr int DD = D * D, TPC = BN / DD, TPT = TPC / 2;   // tiles per CTA, per epilogue thread
+  // tiles per CTA (sym layout: 8 in 3D, 16 in 2D), per epilogue thread; part-2 column tiles end
+  constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, TPT = TPC / 2, NE = D == 3 ? 9 : 8;
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K3_STAGES * K3_A_CHUNK;
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K3_OFF_BAR);
@@ -174,13 +234,10 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int st = kc % K3_STAGES;
     mbar_wait(&full[st], (kc / K3_STAGES) & 1);
     const double *a_st = sA + st * K3_A_CHUNK, *b_st = sB + st * K3_B_CHUNK;
-    if (nmi == 2) {
-      if (kc + 1 < nkc) mma_chunk_fm<BK / 4>(a_st, b_st, warp * MI, lane, acc);
-      else mma_chunk_tail(a_st, b_st, warp * MI, lane, ksteps - kc * (BK / 4), acc);
-    } else if (nmi == 1) {
-      if (kc + 1 < nkc) mma_chunk_fm<BK / 4, 1>(a_st, b_st, warp * MI, lane, acc);
-      else mma_chunk_tail<1>(a_st, b_st, warp * MI, lane, ksteps - kc * (BK / 4), acc);
-    }
+    // k-steps of this chunk and the first one of part 2 (Eq. 38-reduced contraction)
+    const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), j = max(0, min(ksplit - s0, ns));
+    if (nmi == 2) k3_chunk<2, NE>(a_st, b_st, warp * MI, lane, ns, j, acc);
+    else if (nmi == 1) k3_chunk<1, NE>(a_st, b_st, warp * MI, lane, ns, j, acc);
     __syncwarp();
     if (lane == 0) {   // the last warp to release a stage refills it
       __threadfence_block();
@@ -214,12 +271,26 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
       }
   }
   __syncthreads();
-  if (EPI == 0) {
-    const int64_t N = n_tiles * DD, n0 = nb * BN;
-    for (int i = tid; i < K3_BM * BN; i += K3_THREADS) {
-      const int rr = i / BN, c = i % BN;
-      const int64_t gr = m0 + rr, gc = n0 + c;
-      if (gr < M && gc < N) out[gr * N + gc] = sC[rr * K3_CROW + c];
+  {   // sym layout (column o·TPC + tl) -> tile-major L_t[a][b] (column tl·DD + a·D + b), in
+      // place: each thread holds its row's TPT tiles in registers across the barrier
+    double v[TPT * DD];
+#pragma unroll
+    for (int k = 0; k < TPT; ++k)
+#pragma unroll
+      for (int ab = 0; ab < DD; ++ab) v[k * DD + ab] = lval<D>(sC + er * K3_CROW, et0 + k, ab / D, ab % D);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < TPT; ++k)
+#pragma unroll
+      for (int ab = 0; ab < DD; ++ab) sC[er * K3_CROW + (et0 + k) * DD + ab] = v[k * DD + ab];
+    __syncthreads();
+  }
+  if (EPI == 0) {   // nzdata (Eq. 58): local[row][t*DD + a*D + b]
+    const int64_t N = n_tiles * DD;
+    for (int i = tid; i < K3_BM * TPC * DD; i += K3_THREADS) {
+      const int rr = i / (TPC * DD), c = i % (TPC * DD), tl = c / DD, ab = c % DD;
+      const int64_t gr = m0 + rr, t = t0 + tl;
+      if (gr < M && t < n_tiles) out[gr * N + t * DD + ab] = sC[rr * K3_CROW + c];
     }
     return;
   }
@@ -245,7 +316,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
 #pragma unroll
       for (int a = 0; a < D; ++a) c1[a] = c2[a] = 0.0;
       if (tv && live) {
-        const double *L = sC + er * K3_CROW + tl * DD;
+        const double *L = sC + er * K3_CROW;
         const int64_t I = ap.node_map[t * nl + A], J = ap.node_map[t * nl + B];
         double uv[D];
 #pragma unroll
@@ -253,10 +324,10 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
-          for (int b = 0; b < D; ++b) c1[a] += (A == B && a > b ? L[b * D + a] : L[a * D + b]) * uv[b];
+          for (int b = 0; b < D; ++b) c1[a] += (A == B && a > b ? L[tl * DD + b * D + a] : L[tl * DD + a * D + b]) * uv[b];
       }
       if (tv && live_t && At != Bt) {
-        const double *L = sC + et * K3_CROW + tl * DD;
+        const double *L = sC + et * K3_CROW;
         const int64_t I = ap.node_map[t * nl + At];
         double uv[D];
 #pragma unroll
@@ -264,7 +335,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
 #pragma unroll
         for (int b = 0; b < D; ++b)
 #pragma unroll
-          for (int a = 0; a < D; ++a) c2[b] += L[a * D + b] * uv[a];
+          for (int a = 0; a < D; ++a) c2[b] += L[tl * DD + a * D + b] * uv[a];
       }
 #pragma unroll
       for (int a = 0; a < D; ++a) { my1[a] = c1[a]; my2[a] = c2[a]; }
@@ -341,10 +412,10 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     if (ev != 12345) continue;
 #endif
     if (live && ev < 0) {   // one of several contributions: side slot, summed by K4
-      const double *L = sC + er * K3_CROW + tl * DD;
+      const double *L = sC + er * K3_CROW;
       double *o = side + (int64_t)(-ev - 1) * DD;
 #pragma unroll
-      for (int q = 0; q < DD; ++q) o[q] = L[q];
+      for (int q = 0; q < DD; ++q) o[q] = L[tl * DD + q];
     }
     const bool w1 = live && ev >= 0 && riA[k] >= 0;   // riA < 0: row of another shard
     const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff), str1 = D * (riA[k] & 0xffffff);
@@ -364,7 +435,7 @@ static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, Apply
   if (e) return e;
   dim3 grid((unsigned)(h.Mpad / K3_BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k3_contract<D, EPI><<<grid, K3_THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.kstride / BK, (h.nk + 3) / 4, h.M,
+  k3_contract<D, EPI><<<grid, K3_THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
                                                         h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,
                                                         h.n_local_ctrl, h.d_side, h.d_tperm, ap);
   return cudaGetLastError();
@@ -425,9 +496,13 @@ cudaError_t launch_contraction(const Handle &h, double *vals, double *local, cud
 // more: its DMUL/DFMA share the FP64 datapath with DMMA and starve behind it
 // (measured: 27.9 ms vs 22.7 ms for the GEMM alone at cfg5, profiles/r01_*).
 
-// X[col][(t,a,b)] for the tile patch of grid.x and the 72 columns of N-block grid.y;
-// chunk kc of the patch is written as one contiguous FM chunk (coalesced).  Thread
-// (warp w, lane) owns row k = 4w + lane%4 of every chunk and the 9 columns
+// X̃[col][n] for the tile patch of grid.x and the 72 columns of N-block grid.y in the
+// sym layout of the Eq. 38-reduced contraction: block column n = o·TPC + tl
+// holds X̃⁺ = X_aa or X_ab + X_ba (o < n_p1: symmetric output (a,b), a <= b) or
+// X̃⁻ = X_ab − X_ba (antisymmetric output a < b), X_ab the coefficient of L[a][b] in uᵀK^πv
+// (R9/R13; diagonal rows: X_ab = u_a v_b + u_b v_a for a < b, u_a v_a for a = b, 0 for
+// a > b).  Chunk kc of the patch is written as one contiguous FM chunk (coalesced).
+// Thread (warp w, lane) owns row k = 4w + lane%4 of every chunk and the 9 columns
 // n_j = 8j + lane/4, i.e. FM elements e = 128j + 32w + lane: one pair per chunk, the
 // per-column offsets are loop invariants.
 template <int D>
@@ -435,7 +510,7 @@ __global__ void __launch_bounds__(128)
 k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, const int32_t *__restrict__ node_map,
         int nl, const double *__restrict__ u, const double *__restrict__ v, int64_t n_tiles, int nkc,
         double *__restrict__ X) {
-  constexpr int DD = D * D, TPC = BN / DD;
+  constexpr int TPC = D == 3 ? 8 : 16, NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2;
   extern __shared__ __align__(128) double smem[];
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const int64_t nb = blockIdx.y, t0 = nb * TPC;
@@ -455,14 +530,16 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
     }
   }
   const int k = 4 * (tid >> 5) + (lane & 3);
-  int cA[NI], cB[NI];
-  double fdiag[NI];
+  int cA[NI], cB[NI], mode[NI];   // mode 0: X_aa, 1: X_ab + X_ba, 2: X_ab − X_ba, 3: unused column
 #pragma unroll
   for (int j = 0; j < NI; ++j) {
-    const int n = 8 * j + (lane >> 2), tl = n / DD, ab = n % DD, a = ab / D, b = ab % D;
-    cA[j] = tl * nc * D + a;
-    cB[j] = tl * nc * D + b;
-    fdiag[j] = a < b ? 1.0 : (a == b ? 0.5 : 0.0);
+    const int n = 8 * j + (lane >> 2), o = n / TPC, tl = n % TPC;
+    int a = 0, b = 0;
+    if (o < NP1) sym_pair(D, o, a, b);
+    else if (o < NP1 + NP2) anti_pair(D, o - NP1, a, b);
+    mode[j] = o < NP1 ? (a == b ? 0 : 1) : (o < NP1 + NP2 ? 2 : 3);
+    cA[j] = (mode[j] == 3 ? 0 : tl) * nc * D + a;
+    cB[j] = (mode[j] == 3 ? 0 : tl) * nc * D + b;
   }
   __syncthreads();
   int32_t pr = k5_pair[(int64_t)kc0 * BK + k];
@@ -473,10 +550,15 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
     if (pr >= 0) {
       const int A = (pr & 0xffff) * D, B = (pr >> 16) * D;
 #pragma unroll
-      for (int j = 0; j < NI; ++j) x[j] = fma(us[cB[j] + B], vs[cA[j] + A], us[cA[j] + A] * vs[cB[j] + B]);
-      if (A == B) {
-#pragma unroll
-        for (int j = 0; j < NI; ++j) x[j] *= fdiag[j];
+      for (int j = 0; j < NI; ++j) {
+        const double xab = fma(us[cB[j] + B], vs[cA[j] + A], us[cA[j] + A] * vs[cB[j] + B]);
+        if (mode[j] == 3) x[j] = 0.0;
+        else if (A == B) x[j] = mode[j] == 0 ? 0.5 * xab : xab;   // diagonal row: X_ba = 0 (a < b)
+        else if (mode[j] == 0) x[j] = xab;
+        else {
+          const double xba = fma(us[cA[j] + B], vs[cB[j] + A], us[cB[j] + A] * vs[cA[j] + B]);
+          x[j] = mode[j] == 1 ? xab + xba : xab - xba;
+        }
       }
     } else {
 #pragma unroll
@@ -496,11 +578,15 @@ constexpr size_t K5_OFF_BAR = sizeof(double) * (size_t)K5_STAGES * (K5_A_CHUNK +
 constexpr size_t K5_SMEM = K5_OFF_BAR + K5_STAGES * (sizeof(uint64_t) + sizeof(int));
 static_assert(sizeof(double) * BN * K5_WP <= K5_OFF_BAR, "W staging must fit in the stages");
 
-// W[n][κ] = Σ_col tabAT[κ][col] X[col][n]: CTA = 128 κ rows × 72 columns, 8 MMA warps of
-// 16×72; warp 0 lane 0 refills the 4-stage ring once all warps released a stage.
+// Y[n][κ] = Σ_col tabAT[κ][col] X̃[col][n]: CTA = 128 κ rows × 72 columns, 8 MMA warps of
+// 16×72; the last MMA warp to release a stage refills it.  Eq. 38-reduced:
+// κ rows of part 1 (< k5s) meet the symmetric columns (tiles [0, 6)), part 2 rows
+// (< k5k) the antisymmetric ones ([6, NE)); no DMMA for the other pairings or padding.
+template <int D>
 __global__ void __launch_bounds__(K5_THREADS, 1)
 k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nkc, int64_t N,
-          double *__restrict__ Wout, int kstride, int nk) {
+          double *__restrict__ Wout, int ldw, int k5s, int k5k) {
+  constexpr int NE = D == 3 ? 9 : 8;
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K5_STAGES * K5_A_CHUNK;
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5_OFF_BAR);
@@ -508,10 +594,10 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t kb = blockIdx.x, nb = blockIdx.y;
   const double *gA = tabAT + kb * (int64_t)nkc * K5_A_CHUNK, *gB = X + nb * (int64_t)nkc * K5_B_CHUNK;
-  // 8-row groups of this warp that hold table columns κ < n_k (the rest is zero padding:
-  // 13 of 256 rows at q = 2, 64 of 640 at q = 3 — no DMMA is issued for them)
+  // part (1, 2; 0 = padding) of each of the warp's two 8-row groups
   const int row0 = (int)kb * BM + warp * 16;
-  const int nmi = row0 >= nk ? 0 : (row0 + 8 >= nk ? 1 : 2);
+  auto part = [&](int r) { return r < k5s ? 1 : (r < k5k ? 2 : 0); };
+  const int mode = part(row0) * 3 + part(row0 + 8);
   if (tid == 0) {
     for (int s = 0; s < K5_STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -536,10 +622,18 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   for (int kc = 0; kc < nkc; ++kc) {
     const int st = kc % K5_STAGES;
     mbar_wait(&full[st], (kc / K5_STAGES) & 1);
-    if (nmi == 2)
-      mma_chunk_fm<BK / 4>(sA + st * K5_A_CHUNK, sB + st * K5_B_CHUNK, warp * MI, lane, acc);
-    else if (nmi == 1)
-      mma_chunk_fm<BK / 4, 1>(sA + st * K5_A_CHUNK, sB + st * K5_B_CHUNK, warp * MI, lane, acc);
+    const double *a_st = sA + st * K5_A_CHUNK, *b_st = sB + st * K5_B_CHUNK;
+    switch (mode) {
+      case 4: mma_steps<4, 0, 2, 0, 6>(a_st, b_st, warp * MI, lane, 0, acc); break;    // (1, 1)
+      case 8: mma_steps<4, 0, 2, 6, NE>(a_st, b_st, warp * MI, lane, 0, acc); break;   // (2, 2)
+      case 5:                                                                          // (1, 2)
+        mma_steps<4, 0, 1, 0, 6>(a_st, b_st, warp * MI, lane, 0, acc);
+        mma_steps<4, 1, 1, 6, NE>(a_st, b_st, warp * MI, lane, 0, acc);
+        break;
+      case 3: mma_steps<4, 0, 1, 0, 6>(a_st, b_st, warp * MI, lane, 0, acc); break;    // (1, pad)
+      case 6: mma_steps<4, 0, 1, 6, NE>(a_st, b_st, warp * MI, lane, 0, acc); break;   // (2, pad)
+      default: break;
+    }
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -565,12 +659,12 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   for (int i = tid; i < BN * BM; i += K5_THREADS) {
     const int n = i / BM, kap = i % BM;
     const int64_t gn = nb * BN + n, gk = kb * BM + kap;
-    if (gn < N && gk < kstride) Wout[gn * kstride + gk] = sW[n * K5_WP + kap];
+    if (gn < N && gk < ldw) Wout[gn * ldw + gk] = sW[n * K5_WP + kap];
   }
 }
 
 size_t k5x_smem_bytes(int d, int max_patch_ctrl) {
-  return sizeof(double) * (size_t)2 * (BN / (d * d)) * max_patch_ctrl * d;
+  return sizeof(double) * (size_t)2 * (d == 3 ? 8 : 16) * max_patch_ctrl * d;
 }
 
 template <int D>
@@ -579,7 +673,7 @@ static cudaError_t launch_k5x(const Handle &h, const double *u, const double *v,
   cudaError_t e = cudaFuncSetAttribute(k5x_gen<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
   // the sensitivity runs over the owned tiles (the first n_tiles_own local tiles)
-  dim3 grid((unsigned)h.n_patches, (unsigned)((h.n_tiles_own * D * D + BN - 1) / BN));
+  dim3 grid((unsigned)h.n_patches, (unsigned)((h.n_tiles_own + h.tpc - 1) / h.tpc));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   k5x_gen<D><<<grid, 128, smem, s>>>(h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, u, v, h.n_tiles_own,
                                      (int)(h.Kp / BK), h.d_X);
@@ -590,14 +684,20 @@ cudaError_t launch_sens_X(const Handle &h, const double *u, const double *v, cud
   return h.d == 2 ? launch_k5x<2>(h, u, v, s) : launch_k5x<3>(h, u, v, s);
 }
 
-cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k5a_wgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM);
+template <int D>
+static cudaError_t launch_k5a(const Handle &h, double *W, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k5a_wgemm<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM);
   if (e) return e;
-  dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)((h.n_tiles_own * h.d * h.d + BN - 1) / BN));
+  const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc;   // N-blocks of the owned tiles
+  dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)nblk);
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k5a_wgemm<<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), h.n_tiles_own * h.d * h.d, W,
-                                              h.kstride, h.nk);
+  k5a_wgemm<D><<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), nblk * BN, W, (int)h.k5_rows,
+                                                 h.k5_split, h.k5_kap);
   return cudaGetLastError();
+}
+
+cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s) {
+  return h.d == 2 ? launch_k5a<2>(h, W, s) : launch_k5a<3>(h, W, s);
 }
 
 }  // namespace iga

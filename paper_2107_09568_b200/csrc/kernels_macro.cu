@@ -331,35 +331,75 @@ __device__ __forceinline__ void node_geometry(const InterpConst &c_ip, const Mac
 // of Ā (Eq. 37, closed form) at the (q+1)^d nodes into registers, applies (V1⁻¹)^{⊗d}
 // by D 1D passes in registers (all indices compile-time) and writes its (q+1)^d
 // interpolation coefficients.
-template <int D, int Q>
+template <int D, int Q, bool SYM = false>
 struct K2Shape {
   static constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, DD = D * D, NC = DD * DD;
-  static constexpr int TPB = D == 2 ? (Q <= 2 ? 16 : 8) : 4;   // tiles per CTA: 256 (128) / 324 threads
-  static constexpr int THREADS = TPB * NC;
+  // SYM (the K3 operand of the Eq. 38-reduced contraction): one thread per distinct
+  // component, n_p1² symmetric + n_p2² antisymmetric (45 in 3D, 10 in 2D); else all d⁴
+  static constexpr int NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2, NS = NP1 * NP1 + NP2 * NP2;
+  static constexpr int NT = SYM ? NS : NC;
+  static constexpr int TPB = D == 2 ? (Q <= 2 ? 16 : 8) : 4;   // tiles per CTA (static shared memory < 48 KB)
+  static constexpr int THREADS = TPB * NT;
   static constexpr bool REG = NPI <= 27;        // register path; larger q: shared-memory passes
 };
 
-template <int D, int Q>
-__global__ void __launch_bounds__(K2Shape<D, Q>::THREADS)
+// Ā_ij[a,b] at a node (Eq. 37, closed form)
+template <int D>
+__device__ __forceinline__ double abar(const NodeGeo<D> &g, double lam, double mu, int i, int j, int a, int b) {
+  return g.det * (lam * g.G[i][a] * g.G[j][b] + mu * g.G[j][a] * g.G[i][b] + (a == b ? mu * g.gg[i][j] : 0.0));
+}
+
+// the K3 B operand of the Eq. 38-reduced contraction: symmetric part
+// ½(⟨Ā_ij[a,b]⟩ + ⟨Ā_ij[b,a]⟩) of P1 pair p = (i,j) at output o = (a,b), a <= b (column
+// p·n_π + C, block row o·tpc + tl), antisymmetric part ½(⟨Ā_ij[a,b]⟩ − ⟨Ā_ij[b,a]⟩) of P2 pair
+// (column k1 + p'·n_π + C, block row (n_p1 + o')·tpc + tl).  comp < n_p1²: (p, o); else (p', o').
+template <int D>
+__device__ __forceinline__ void sym_component(int comp, bool &part2, int &i, int &j, int &a, int &b, int &p, int &o) {
+  constexpr int NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2;
+  part2 = comp >= NP1 * NP1;
+  if (!part2) {
+    p = comp / NP1;
+    o = comp % NP1;
+    sym_pair(D, p, i, j);
+    sym_pair(D, o, a, b);
+  } else {
+    const int c2 = comp - NP1 * NP1;
+    p = c2 / NP2;
+    o = c2 % NP2;
+    anti_pair(D, p, i, j);
+    anti_pair(D, o, a, b);
+  }
+}
+
+// FM offset of the sym-layout K3 B operand entry (tile t, block row o_col, column k)
+__device__ __forceinline__ int64_t sym_b_index(int64_t t, int o_col, int k, int tpc, int ks3) {
+  const int64_t nb = t / tpc;
+  const int rr = o_col * tpc + (int)(t - nb * tpc);
+  return (nb * (ks3 / 16) + (k >> 4)) * (int64_t)(IGA_GEMM_BN * 16) + (rr & ~7) * 16 + ((k >> 2) & 3) * 32 +
+         ((rr & 7) << 2) + (k & 3);
+}
+
+template <int D, int Q, bool SYM>
+__global__ void __launch_bounds__(K2Shape<D, Q, SYM>::THREADS)
 k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
                const int *__restrict__ mspan, const double *__restrict__ young, int ypt,
-               double nu, double *__restrict__ coef, int kstride, int fm, int64_t n_tiles, int *flag) {
-  using S = K2Shape<D, Q>;
+               double nu, double *__restrict__ coef, int kstride, int k1, int tpc, int64_t n_tiles, int *flag) {
+  using S = K2Shape<D, Q, SYM>;
   static_assert(S::REG, "register path only for (q+1)^d <= 27");
-  constexpr int Q1 = S::Q1, NPI = S::NPI, DD = S::DD, NC = S::NC, TPB = S::TPB;
+  constexpr int Q1 = S::Q1, NPI = S::NPI, DD = S::DD, NT = S::NT, TPB = S::TPB;
   __shared__ MacroTile<D> mt[TPB];
   __shared__ NodeGeo<D> geo[TPB][NPI];
-  const int tl = threadIdx.x / NC, comp = threadIdx.x % NC;
+  const int tl = threadIdx.x / NT, comp = threadIdx.x % NT;
   const int64_t t = (int64_t)blockIdx.x * TPB + tl;
   const bool live = t < n_tiles;
   const int64_t tg = t + c_ip.t_base;   // global tile id (macro element, E, error report)
-  if (live) load_macro_tile<D>(c_ip, mt[tl], tg, ctrl, mknots, mspan, comp, NC);
+  if (live) load_macro_tile<D>(c_ip, mt[tl], tg, ctrl, mknots, mspan, comp, NT);
   __syncthreads();
   // ∇F at the nodes: B-spline maps one column J[:, β] per thread (NPI·D threads of the
   // tile, staged in the node's G slot), then det / J⁻¹ per node; NURBS maps the whole
   // quotient-rule J per node
   if (live && !mt[tl].rational)
-    for (int w = comp; w < NPI * D; w += NC) {
+    for (int w = comp; w < NPI * D; w += NT) {
       const int m = w / D, be = w % D;
       double col[D];
       macro_Jcol_bspline<D>(c_ip, mt[tl], m, be, col);
@@ -368,7 +408,7 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
     }
   __syncthreads();
   if (live)
-    for (int m = comp; m < NPI; m += NC) {
+    for (int m = comp; m < NPI; m += NT) {
       double J[D][D], G[D][D];
       if (mt[tl].rational) macro_J<D>(c_ip, mt[tl], m, J);
       else
@@ -390,12 +430,26 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   if (!live) return;
   double lam, mu;
   lame(young[ypt ? tg : 0], nu, lam, mu);
-  const int ij = comp / DD, ab = comp % DD, i = ij / D, j = ij % D, a = ab / D, b = ab % D;
   double x[NPI];
+  int i, j, a, b, ij = 0, ab = 0, p = 0, o = 0;
+  bool part2 = false;
+  if (SYM) {
+    sym_component<D>(comp, part2, i, j, a, b, p, o);
 #pragma unroll
-  for (int m = 0; m < NPI; ++m) {
-    const NodeGeo<D> &g = geo[tl][m];
-    x[m] = g.det * (lam * g.G[i][a] * g.G[j][b] + mu * g.G[j][a] * g.G[i][b] + (a == b ? mu * g.gg[i][j] : 0.0));
+    for (int m = 0; m < NPI; ++m) {
+      const double xab = abar<D>(geo[tl][m], lam, mu, i, j, a, b);
+      const double xba = a == b ? xab : abar<D>(geo[tl][m], lam, mu, i, j, b, a);
+      x[m] = 0.5 * (part2 ? xab - xba : xab + xba);
+    }
+  } else {
+    ij = comp / DD;
+    ab = comp % DD;
+    i = ij / D;
+    j = ij % D;
+    a = ab / D;
+    b = ab % D;
+#pragma unroll
+    for (int m = 0; m < NPI; ++m) x[m] = abar<D>(geo[tl][m], lam, mu, i, j, a, b);
   }
   // direction 0, 1 (, 2), in place one line of Q1 values at a time (few live registers):
   // out[c] = Σ_m Π1[dir][c][m] in[m] along the direction
@@ -418,23 +472,20 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
       }
     }
   }
-  const double *res = x;
-  // coefficient row n = t*DD + ab, column κ = ij*npi + C: row-major coef[n*kstride + κ]
-  // (parity accessor) or the fragment-major K3 B operand (fm_index, BR = IGA_GEMM_BN) with
-  // the row part hoisted and 32-bit column offsets
-  const int64_t n = t * DD + ab;
-  if (fm) {
-    const int64_t rb = n / IGA_GEMM_BN;
-    const int rr = (int)(n - rb * IGA_GEMM_BN);
-    double *base = coef + rb * (int64_t)kstride * IGA_GEMM_BN + (rr & ~7) * 16 + ((rr & 7) << 2);
+  if (SYM) {
+    // the sym-layout K3 B operand (row part hoisted, 32-bit column offsets)
+    const int o_col = part2 ? D * (D + 1) / 2 + o : o;
+    const int kb = part2 ? k1 + p * NPI : p * NPI;
+    double *base = coef + sym_b_index(t, o_col, 0, tpc, kstride);
 #pragma unroll
     for (int C = 0; C < NPI; ++C) {
-      const int k = ij * NPI + C;
-      base[(k >> 4) * (IGA_GEMM_BN * 16) + ((k >> 2) & 3) * 32 + (k & 3)] = res[C];
+      const int k = kb + C;
+      base[(k >> 4) * (IGA_GEMM_BN * 16) + ((k >> 2) & 3) * 32 + (k & 3)] = x[C];
     }
-  } else {
+  } else {   // full coefficients, row-major coef[(t*DD + ab)*kstride + ij*npi + C] (iga_interpolate)
+    const int64_t n = t * DD + ab;
 #pragma unroll
-    for (int C = 0; C < NPI; ++C) coef[n * kstride + ij * NPI + C] = res[C];
+    for (int C = 0; C < NPI; ++C) coef[n * kstride + ij * NPI + C] = x[C];
   }
 }
 
@@ -468,7 +519,8 @@ template <int D, int Q>
 __global__ void __launch_bounds__(256)
 k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl,
                     const double *__restrict__ mknots, const int *__restrict__ mspan, const double *__restrict__ young,
-                    int ypt, double nu, double *__restrict__ coef, int kstride, int fm, int64_t n_tiles, int *flag) {
+                    int ypt, double nu, double *__restrict__ coef, int kstride, int fm, int k1, int tpc,
+                    int64_t n_tiles, int *flag) {
   constexpr int DD = D * D, NC = DD * DD;
   const int NPI = npi_of<D, Q>(c_ip), NK = DD * NPI;
   const int ns = c_ip.ns;
@@ -495,11 +547,23 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
   }
   __syncthreads();
   const double *res = apply_projection<D, Q, false, NC>(c_ip, S0, S1);
-  for (int idx = threadIdx.x; idx < DD * NK; idx += blockDim.x) {
+  for (int idx = fm ? DD * NK : threadIdx.x; idx < DD * NK; idx += blockDim.x) {   // full (iga_interpolate)
     const int ab = idx / NK, kap = idx % NK, ij = kap / NPI, C = kap % NPI;
     const int64_t n = t * DD + ab;
-    const int64_t o = fm ? fm_index(n, kap, IGA_GEMM_BN, kstride / IGA_KCHUNK) : n * kstride + kap;
-    coef[o] = res[C * NC + ij * DD + ab];
+    if (!fm) coef[n * kstride + kap] = res[C * NC + ij * DD + ab];
+  }
+  if (!fm) return;
+  // the sym-layout K3 B operand (Eq. 38-reduced contraction)
+  constexpr int NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2, NS = NP1 * NP1 + NP2 * NP2;
+  for (int idx = threadIdx.x; idx < NS * NPI; idx += blockDim.x) {
+    const int comp = idx / NPI, C = idx % NPI;
+    bool part2;
+    int i, j, a, b, p, o;
+    sym_component<D>(comp, part2, i, j, a, b, p, o);
+    const double *r = res + C * NC + (i * D + j) * DD;
+    const double v = 0.5 * (part2 ? r[a * D + b] - r[b * D + a] : r[a * D + b] + r[b * D + a]);
+    const int o_col = part2 ? NP1 + o : o, k = part2 ? k1 + p * NPI + C : p * NPI + C;
+    coef[sym_b_index(t, o_col, k, tpc, kstride)] = a == b && !part2 ? r[a * D + a] : v;
   }
 }
 
@@ -509,7 +573,7 @@ template <int D, int Q>
 __global__ void __launch_bounds__(256)
 k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
             const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
-            const double *__restrict__ W, int kstride, double *__restrict__ gpart, int *flag) {
+            const double *__restrict__ W, int ldw, int tpc, int k5s, double *__restrict__ gpart, int *flag) {
   constexpr int DD = D * D, NC = DD * DD;
   const int NPI = npi_of<D, Q>(c_ip), NK = DD * NPI;
   const int ns = c_ip.ns;
@@ -519,10 +583,29 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
   __shared__ MacroTile<D> mt;
   const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
   load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
-  const double *src = W + (size_t)t * DD * kstride;
-  for (int idx = threadIdx.x; idx < DD * NK; idx += blockDim.x) {
-    const int ab = idx / NK, kap = idx % NK, ij = kap / NPI, C = kap % NPI;
-    S0[C * NC + ij * DD + ab] = src[(size_t)ab * kstride + kap];
+  // W' from K5a's Y (Eq. 38-reduced contraction): ⟨W', Ā⟩ = Σ Y⁺ Ā⁺' + Σ Y⁻ Ā⁻'
+  // with Ā^±'_ij[a,b] = ½(Ā_ij[a,b] ± Ā_ij[b,a]) for i <= j, so W'_ij[a,b] = ½Y⁺_ij[ab]
+  // (Y⁺_ij[aa] on the diagonal) ± ½Y⁻_ij[ab] (i < j, + for a < b), W'_ij = 0 for i > j
+  (void)NK;
+  constexpr int NP1 = D * (D + 1) / 2;
+  const int64_t nbk = t / tpc;
+  const int tl = (int)(t - nbk * tpc);
+  for (int idx = threadIdx.x; idx < NC * NPI; idx += blockDim.x) {
+    const int C = idx / NC, comp = idx % NC, ij = comp / DD, ab = comp % DD;
+    const int i = ij / D, j = ij % D, a = ab / D, b = ab % D;
+    double w = 0.0;
+    if (i <= j) {
+      const int lo = min(a, b), hi = max(a, b);
+      const int o1 = sym_index(D, lo, hi), p1 = sym_index(D, i, j);
+      const double y1 = W[(size_t)(nbk * IGA_GEMM_BN + o1 * tpc + tl) * ldw + p1 * NPI + C];
+      w = a == b ? y1 : 0.5 * y1;
+      if (i < j && a != b) {
+        const int o2 = anti_index(D, lo, hi), p2 = anti_index(D, i, j);
+        const double y2 = W[(size_t)(nbk * IGA_GEMM_BN + (NP1 + o2) * tpc + tl) * ldw + k5s + p2 * NPI + C];
+        w = fma(a < b ? 0.5 : -0.5, y2, w);
+      }
+    }
+    S0[C * NC + comp] = w;
   }
   __syncthreads();
   node_geometry<D>(c_ip, mt, geo, tg, flag);
@@ -896,11 +979,20 @@ template <int D, int Q>
 static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
                              double *coef, bool fm, cudaStream_t s) {
   if constexpr (Q >= 0 && K2Shape<D, (Q >= 0 ? Q : 0)>::REG) {
-    using S = K2Shape<D, Q>;
     if (h.iso && h.mv[0] == Q + 1) {   // interpolation: register path (else L2 projection, m > q+1)
-      const unsigned grid = (unsigned)((h.n_tiles + S::TPB - 1) / S::TPB);
-      k2_interpolate<D, Q><<<grid, S::THREADS, 0, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt,
-                                                       nu, coef, h.kstride, (int)fm, h.n_tiles, h.d_flag);
+      if (fm) {   // the K3 operand (sym layout)
+        using S = K2Shape<D, Q, true>;
+        const unsigned grid = (unsigned)((h.n_tiles + S::TPB - 1) / S::TPB);
+        k2_interpolate<D, Q, true><<<grid, S::THREADS, 0, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan,
+                                                               young, ypt, nu, coef, h.ks3, 4 * h.k3_split, h.tpc,
+                                                               h.n_tiles, h.d_flag);
+      } else {    // full coefficients, row-major (iga_interpolate)
+        using S = K2Shape<D, Q, false>;
+        const unsigned grid = (unsigned)((h.n_tiles + S::TPB - 1) / S::TPB);
+        k2_interpolate<D, Q, false><<<grid, S::THREADS, 0, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan,
+                                                                young, ypt, nu, coef, h.kstride, 0, h.tpc,
+                                                                h.n_tiles, h.d_flag);
+      }
       return cudaGetLastError();
     }
   }
@@ -909,8 +1001,9 @@ static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *
     cudaError_t e = cudaFuncSetAttribute(k2_interpolate_smem<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     k2_interpolate_smem<D, Q><<<(unsigned)h.n_tiles, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan,
-                                                                   young, ypt, nu, coef, h.kstride, (int)fm,
-                                                                   h.n_tiles, h.d_flag);
+                                                                   young, ypt, nu, coef, fm ? h.ks3 : h.kstride,
+                                                                   (int)fm, 4 * h.k3_split, h.tpc, h.n_tiles,
+                                                                   h.d_flag);
   }
   return cudaGetLastError();
 }
@@ -922,7 +1015,8 @@ static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double 
   cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
-                                                        ypt, nu, W, h.kstride, gpart, h.d_flag);
+                                                        ypt, nu, W, (int)h.k5_rows, h.tpc, h.k5_split, gpart,
+                                                        h.d_flag);
   return cudaGetLastError();
 }
 

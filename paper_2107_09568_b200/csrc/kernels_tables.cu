@@ -216,25 +216,47 @@ __global__ void k1_volume_table(int total_pts, int npi, const double *__restrict
 }
 
 // Offline re-layout of the row-major table into the two fragment-major GEMM operands
-// (device_common.cuh fm_index): K3's A (rows = table rows, BR = IGA_K3_BM) and K5a's A
-// (rows = κ, reduction columns = table rows with each patch padded to 16, BR = 32W).
-__global__ void k1_pack(const double *__restrict__ table, int64_t M, int nk, int kstride,
-                        const int32_t *__restrict__ k5_col, double *__restrict__ tabA, int nkcA,
-                        double *__restrict__ tabAT, int brT, int nkcT) {
+// (device_common.cuh fm_index) of the Eq. 38-reduced contraction: K3's A
+// (rows = table rows, BR = IGA_K3_BM; columns part 1 = [T_ii | T_ij + T_ji] per P1 pair and
+// C, part 2 = [T_ij − T_ji] per P2 pair and C starting at k1) and K5a's A (the same
+// quantities as rows κ, part 2 from k5s; reduction columns = table rows with each patch
+// padded to 16, BR = IGA_K5_BM).
+template <int D>
+__global__ void k1_pack(const double *__restrict__ table, int64_t M, int npi, int kstride,
+                        const int32_t *__restrict__ k5_col, double *__restrict__ tabA, int nkcA, int k1,
+                        double *__restrict__ tabAT, int brT, int nkcT, int k5s) {
+  constexpr int NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2;
+  const int ns = (NP1 + NP2) * npi;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= M * nk) return;
-  const int64_t r = idx / nk;
-  const int kap = (int)(idx % nk);
-  const double v = table[r * kstride + kap];
-  tabA[fm_index(r, kap, IGA_K3_BM, nkcA)] = v;
-  tabAT[fm_index(kap, k5_col[r], brT, nkcT)] = v;
+  if (idx >= M * ns) return;
+  const int64_t r = idx / ns;
+  const int sk = (int)(idx % ns), p = sk / npi, C = sk % npi;
+  const double *T = table + r * kstride;
+  int i, j, kA, kT;
+  double v;
+  if (p < NP1) {
+    sym_pair(D, p, i, j);
+    v = i == j ? T[(i * D + i) * npi + C] : T[(i * D + j) * npi + C] + T[(j * D + i) * npi + C];
+    kA = kT = sk;
+  } else {
+    anti_pair(D, p - NP1, i, j);
+    v = T[(i * D + j) * npi + C] - T[(j * D + i) * npi + C];
+    kA = k1 + (sk - NP1 * npi);
+    kT = k5s + (sk - NP1 * npi);
+  }
+  tabA[fm_index(r, kA, IGA_K3_BM, nkcA)] = v;
+  tabAT[fm_index(kT, k5_col[r], brT, nkcT)] = v;
 }
 
 cudaError_t launch_pack_tables(const Handle &h, cudaStream_t s) {
-  const int64_t n = h.M * h.nk;
-  k1_pack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.d_table, h.M, h.nk, h.kstride, h.d_k5_col, h.d_tabA,
-                                                      h.kstride / IGA_KCHUNK, h.d_tabAT, IGA_K5_BM,
-                                                      (int)(h.Kp / IGA_KCHUNK));
+  const int64_t n = h.M * (h.n_p1 + h.n_p2) * h.npi;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (h.d == 2)
+    k1_pack<2><<<blocks, 256, 0, s>>>(h.d_table, h.M, h.npi, h.kstride, h.d_k5_col, h.d_tabA, h.ks3 / IGA_KCHUNK,
+                                      4 * h.k3_split, h.d_tabAT, IGA_K5_BM, (int)(h.Kp / IGA_KCHUNK), h.k5_split);
+  else
+    k1_pack<3><<<blocks, 256, 0, s>>>(h.d_table, h.M, h.npi, h.kstride, h.d_k5_col, h.d_tabA, h.ks3 / IGA_KCHUNK,
+                                      4 * h.k3_split, h.d_tabAT, IGA_K5_BM, (int)(h.Kp / IGA_KCHUNK), h.k5_split);
   return cudaGetLastError();
 }
 
