@@ -132,12 +132,18 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------
 def algorithmic(prob, s, sens):
-    """Algorithmic work per launch."""
+    """Algorithmic work per launch.  The contraction is
+    the Eq. 38-reduced one: per table row and tile, n_π·(n_p1² + n_p2²) multiply-adds (45 n_π
+    in 3D: the distinct components of Ā, Eq. 38) instead of Eq. 58's d² n_π · d² = 81 n_π;
+    `eq58_flops` is the unreduced count of SURVEY §8(d), reported for reference only."""
     d = prob.d
     dd = d * d
     N = s.n_tiles * dd
-    gemm = 2.0 * s.n_local_rows * s.n_k * N                       # unpadded K = d² n_pi
-    k2_bytes = 8.0 * (s.n_tiles * s.n_k * dd + s.n_tiles + s.n_macro_cp * d)
+    n_pi = s.n_k // dd
+    n_sym = (d * (d + 1) // 2) ** 2 + (d * (d - 1) // 2) ** 2          # 45 (3D), 10 (2D)
+    gemm = 2.0 * s.n_local_rows * s.n_tiles * n_sym * n_pi            # reduced, unpadded
+    eq58 = 2.0 * s.n_local_rows * s.n_k * N
+    k2_bytes = 8.0 * (s.n_tiles * n_sym * n_pi + s.n_tiles + s.n_macro_cp * d)
     # K3 epilogue: CSR writes of the single-contribution blocks, side-slot writes, rank map
     multi_vals = 2.0 * s.n_multi_blocks * dd                      # (I,J) and (J,I) (diag: once, ignored)
     k3_bytes = 8.0 * (s.nnz - multi_vals) + 8.0 * dd * s.n_side_slots + 4.0 * s.n_local_rows * s.n_tiles
@@ -146,7 +152,7 @@ def algorithmic(prob, s, sens):
     # K5x: X writes (rows x tiles x d²) + u, v reads
     k5x_bytes = 8.0 * s.n_local_rows * N + 16.0 * s.n_dof
     return dict(k3_flops=gemm, k5a_flops=gemm if sens else 0.0, k2_bytes=k2_bytes, k3_bytes=k3_bytes,
-                k4_bytes=k4_bytes, k5x_bytes=k5x_bytes if sens else 0.0)
+                k4_bytes=k4_bytes, k5x_bytes=k5x_bytes if sens else 0.0, eq58_flops=eq58)
 
 
 def load_traffic():
@@ -348,7 +354,10 @@ def run_ours(args, rank, world):
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": dom["frac"],
                 "traffic": traffic.get("K3_dram_bytes_per_launch"),
                 "peak_source": "measured DMMA ceiling, profiles/r01_fp64_ceiling.md (MEASURED_PEAKS.json has no FP64 entry)",
-                "algorithmic_flops_per_launch": alg["k3_flops"]}
+                "algorithmic_flops_per_launch": alg["k3_flops"],
+                "flops_note": "Eq. 38-reduced contraction (45 n_pi MACs per table row and tile in 3D); "
+                              "the unreduced Eq. 58 product would be %.4g flop, i.e. %.2f TFLOP/s equivalent"
+                              % (alg["eq58_flops"], alg["eq58_flops"] / (k3_ms * 1e-3) / 1e12)}
 
     line = {"metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

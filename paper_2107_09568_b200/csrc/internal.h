@@ -12,7 +12,9 @@
 #define IGA_MAXQ 4          // max interpolation degree
 #define IGA_MAXM 8          // max L2-projection points per direction (NEXT N2)
 #define IGA_KCHUNK 16       // GEMM k-chunk; k_stride is a multiple of it
+#ifndef IGA_K3_BM
 #define IGA_K3_BM 64        // K3 CTA rows (table rows): 4 MMA warps, 4 CTAs per SM
+#endif
 #define IGA_K5_BM 128       // K5a CTA rows (κ)
 #define IGA_GEMM_BN 72      // K3/K5a CTA columns (tiles × d²): 8 tiles in 3D, 18 in 2D
 

@@ -163,7 +163,10 @@ __device__ __forceinline__ void store_row(double *p, double x0, double x1, doubl
 // pipe stays fed while co-resident CTAs run their epilogues; measured 128-row/2-CTA
 // 22.1 ms, 96-row/3-CTA 21.8 ms, 64-row/4-CTA 21.3 ms at cfg5).  After the main loop the
 // same warps stage the tile in shared memory and scatter it.
-constexpr int K3_STAGES = 3;
+#ifndef IGA_K3_STAGES
+#define IGA_K3_STAGES 3
+#endif
+constexpr int K3_STAGES = IGA_K3_STAGES;
 constexpr int K3_A_CHUNK = K3_BM * BK, K3_B_CHUNK = BN * BK;          // doubles
 constexpr int K3_CROW = BN + 1;                                        // epilogue pitch (odd)
 constexpr int K3_THREADS = 32 * K3_WARPS;
@@ -187,7 +190,7 @@ struct ApplyArgs {
 // EPI = 0: local[M][N] (nzdata, Eq. 58) ; EPI = 1: fused CSR scatter (+ side slots);
 // EPI = 2: matrix-free apply y = K^π u (Eq. 74): block products summed into partial slots
 template <int D, int EPI>
-__global__ void __launch_bounds__(K3_THREADS, 4)
+__global__ void __launch_bounds__(K3_THREADS, 256 / K3_BM)
 k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int ksplit, int64_t M,
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
