@@ -258,8 +258,13 @@ def tile_coefficients(prob, ctrl, t, E=None, route=A_closed, m=None):
     d = prob.d
     E = prob.young[t] if E is None else E
     lam, mu = lame(E, prob.nu)
-    return project_field(lambda X: route(macro_jacobian(prob.macro, ctrl, t, X), lam, mu), prob.q, d,
-                         m or getattr(prob, "n_proj", 0), check_tile=t, ctrl=ctrl, macro=prob.macro)
+
+    def field(X):
+        J = macro_jacobian(prob.macro, ctrl, t, X)
+        if np.any(np.real(np.linalg.det(J)) <= 0):
+            raise ValueError(f"degenerate macro element: tile {t}")
+        return route(J, lam, mu)
+    return project_field(field, prob.q, d, m or getattr(prob, "n_proj", 0))
 
 
 def projection_points(q, d, m=0):

@@ -59,8 +59,12 @@ def load_tables(prob):
 def det_coefficients(prob, ctrl, t, m=None):
     """d^(t): projection coefficients of |det J_ℳ(t)| (Eq. 15; interpolation at the
     q+1 Gauss nodes, reading R1, or the m-point L2 projection of Eqs. 23-24)."""
-    return M.project_field(lambda X: np.linalg.det(M.macro_jacobian(prob.macro, ctrl, t, X)), prob.q, prob.d,
-                           m or getattr(prob, "n_proj", 0), check_tile=t, ctrl=ctrl, macro=prob.macro)
+    def det(X):
+        D = np.linalg.det(M.macro_jacobian(prob.macro, ctrl, t, X))
+        if np.any(np.real(D) <= 0):
+            raise ValueError(f"degenerate macro element: tile {t}")
+        return D
+    return M.project_field(det, prob.q, prob.d, m or getattr(prob, "n_proj", 0))
 
 
 def volume_lookup(prob, ctrl=None, tiles=None, th=None):

@@ -60,7 +60,9 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_sA_slot, h.sA_slot.data(), h.sA_slot.size() * 4) ||
       !up((void **)&h.d_inv_ptr, h.inv_ptr.data(), h.inv_ptr.size() * 8) ||
       !up((void **)&h.d_inv_ent, h.inv_ent.data(), h.inv_ent.size() * 4) ||
-      !up((void **)&h.d_patch_info, pinfo.data(), pinfo.size() * 4))
+      !up((void **)&h.d_patch_info, pinfo.data(), pinfo.size() * 4) ||
+      !up((void **)&h.d_k5_gphys, h.k5_gphys.data(), h.k5_gphys.size() * 4) ||
+      !up((void **)&h.d_k5_mode, h.k5_mode.data(), h.k5_mode.size()))
     return IGA_ENOMEM;
   if (cudaMalloc((void **)&h.d_side, std::max<size_t>(8, (size_t)h.n_slots * h.d * h.d * 8)) != cudaSuccess) {
     set_error("cudaMalloc of the multi-contribution slots failed");
@@ -675,6 +677,48 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   }
   // K5a CTA height IGA_K3_BM κ rows
   h.k5_rows = (h.k5_kap + IGA_K5_BM - 1) / IGA_K5_BM * IGA_K5_BM;
+  {   // K5a κ-group placement (longest-processing-time first over blocks, then sub-partitions):
+      // block b, sub-partition q holds the warps q + 4h (h < W/4), two 8-row groups each
+    constexpr int W = IGA_K5_BM / 16, SL = 2 * (W / 4);   // warps per block, slots per sub-partition
+    const int G1 = h.k5_split / 8, G2 = (h.k5_kap - h.k5_split) / 8, nbk = (int)(h.k5_rows / IGA_K5_BM);
+    std::vector<int> sload(nbk * 4, 0), bload(nbk, 0);
+    std::vector<std::vector<int>> slot(nbk * 4);
+    for (int g = 0; g < G1 + G2; ++g) {
+      const int w = g < G1 ? 2 : 1;
+      int bb = -1, ss = -1;
+      for (int b = 0; b < nbk; ++b) {
+        bool free_ = false;
+        for (int q = 0; q < 4; ++q) free_ = free_ || (int)slot[b * 4 + q].size() < SL;
+        if (free_ && (bb < 0 || bload[b] < bload[bb])) bb = b;
+      }
+      for (int q = 0; q < 4; ++q)
+        if ((int)slot[bb * 4 + q].size() < SL && (ss < 0 || sload[bb * 4 + q] < sload[bb * 4 + ss])) ss = q;
+      slot[bb * 4 + ss].push_back(g);
+      sload[bb * 4 + ss] += w;
+      bload[bb] += w;
+    }
+    h.k5_gphys.assign(G1 + G2, 0);
+    h.k5_mode.assign(nbk * W, 0);
+    auto part = [&](int g) { return g < 0 ? 0 : (g < G1 ? 1 : 2); };
+    for (int b = 0; b < nbk; ++b)
+      for (int q = 0; q < 4; ++q) {
+        std::vector<int> v = slot[b * 4 + q];   // part-1 groups first (heavier), empty slots last
+        while ((int)v.size() < SL) v.push_back(-1);
+        std::stable_sort(v.begin(), v.end(), [&](int x, int y) {
+          const int px = part(x) == 0 ? 3 : part(x), py = part(y) == 0 ? 3 : part(y);
+          return px < py;
+        });
+        for (int hh = 0; hh < W / 4; ++hh) {   // warp q + 4hh: the hh-th heaviest with the hh-th lightest
+          const int warp = q + 4 * hh;
+          int g0 = v[hh], g1 = v[SL - 1 - hh];
+          if (part(g1) != 0 && (part(g0) == 0 || part(g1) < part(g0))) std::swap(g0, g1);
+          h.k5_mode[b * W + warp] = (uint8_t)(part(g0) * 3 + part(g1));
+          if (g0 >= 0) h.k5_gphys[g0] = (b * W + warp) * 2;
+          if (g1 >= 0) h.k5_gphys[g1] = (b * W + warp) * 2 + 1;
+        }
+      }
+  }
+
   if (k5x_smem_bytes(d, h.max_patch_ctrl) > 227 * 1024) { set_error("tile patch too large for the K5 shared-memory staging (%d control points)", h.max_patch_ctrl); return IGA_ELIMIT; }
 
   // ---- projection operator (R1: interpolation at the q_k+1 Gauss nodes) -----------

@@ -15,7 +15,7 @@
 #ifndef IGA_K3_BM
 #define IGA_K3_BM 64        // K3 CTA rows (table rows): 4 MMA warps, 4 CTAs per SM
 #endif
-#define IGA_K5_BM 128       // K5a CTA rows (κ)
+#define IGA_K5_BM 256       // K5a CTA rows (κ): 16 MMA warps, all κ rows of a 3D q = 2 problem in one CTA
 #define IGA_GEMM_BN 72      // K3/K5a CTA columns (tiles × d²): 8 tiles in 3D, 18 in 2D
 
 namespace iga {
@@ -108,6 +108,13 @@ struct Handle {
   int ks3 = 0;                       // K3 k stride of d_tabA / d_coef (multiple of 16)
   int k3_split = 0, k3_steps = 0;    // K3 k-step where part 2 starts; k-steps (parts padded to 4)
   int k5_split = 0, k5_kap = 0;      // K5a κ row where part 2 starts; rows used (parts padded to 8)
+  // K5a balance: logical 8-row κ group g -> physical group (block·16 + warp·2 + mi), chosen so
+  // that every CTA and sub-partition carries a similar DMMA load (part-1 groups cost 6 column
+  // tiles, part-2 groups 3); per (κ-block, warp) the parts of its two groups (mode p0·3 + p1)
+  std::vector<int32_t> k5_gphys;
+  std::vector<uint8_t> k5_mode;
+  int32_t *d_k5_gphys = nullptr;
+  uint8_t *d_k5_mode = nullptr;
   int64_t Kp = 0;                    // K5a reduction length: table rows, each patch padded to 16
   int max_patch_ctrl = 0;
   std::vector<int32_t> pcol;         // [n_patches+1] first padded column of each patch

@@ -36,8 +36,8 @@ constexpr int BK = IGA_KCHUNK;     // 16
 constexpr int BN = IGA_GEMM_BN;    // 72
 constexpr int NI = BN / 8;         // 9 DMMA column tiles per warp
 constexpr int MI = 2;              // 2 DMMA row tiles per warp (16 rows)
-constexpr int N_MMA_WARPS = 8;                                              // K5a
-constexpr int BM = 16 * N_MMA_WARPS;                                        // 128 (K5a κ rows)
+constexpr int N_MMA_WARPS = IGA_K5_BM / 16;                                // K5a: 16
+constexpr int BM = 16 * N_MMA_WARPS;                                        // 256 (K5a κ rows)
 constexpr int K3_BM = IGA_K3_BM, K3_WARPS = K3_BM / 16;                     // K3: 64 rows, 4 MMA warps
 static_assert(BM == IGA_K5_BM, "K5a CTA rows");
 constexpr int K5_X_CHUNK_ = BN * BK;                                        // doubles per X chunk
@@ -588,7 +588,7 @@ static_assert(sizeof(double) * BN * K5_WP <= K5_OFF_BAR, "W staging must fit in 
 template <int D>
 __global__ void __launch_bounds__(K5_THREADS, 1)
 k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nkc, int64_t N,
-          double *__restrict__ Wout, int ldw, int k5s, int k5k) {
+          double *__restrict__ Wout, int ldw, const uint8_t *__restrict__ k5_mode) {
   constexpr int NE = D == 3 ? 9 : 8;
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K5_STAGES * K5_A_CHUNK;
@@ -597,10 +597,9 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t kb = blockIdx.x, nb = blockIdx.y;
   const double *gA = tabAT + kb * (int64_t)nkc * K5_A_CHUNK, *gB = X + nb * (int64_t)nkc * K5_B_CHUNK;
-  // part (1, 2; 0 = padding) of each of the warp's two 8-row groups
-  const int row0 = (int)kb * BM + warp * 16;
-  auto part = [&](int r) { return r < k5s ? 1 : (r < k5k ? 2 : 0); };
-  const int mode = part(row0) * 3 + part(row0 + 8);
+  // part (1, 2; 0 = padding) of each of the warp's two 8-row groups: part(mi0)·3 + part(mi1)
+  // (host-balanced placement of the κ groups, Handle::k5_gphys)
+  const int mode = k5_mode[kb * N_MMA_WARPS + warp];
   if (tid == 0) {
     for (int s = 0; s < K5_STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -695,7 +694,7 @@ static cudaError_t launch_k5a(const Handle &h, double *W, cudaStream_t s) {
   dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)nblk);
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   k5a_wgemm<D><<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), nblk * BN, W, (int)h.k5_rows,
-                                                 h.k5_split, h.k5_kap);
+                                                 h.d_k5_mode);
   return cudaGetLastError();
 }
 

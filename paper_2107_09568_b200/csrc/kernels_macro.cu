@@ -573,7 +573,8 @@ template <int D, int Q>
 __global__ void __launch_bounds__(256)
 k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
             const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
-            const double *__restrict__ W, int ldw, int tpc, int k5s, double *__restrict__ gpart, int *flag) {
+            const double *__restrict__ W, int ldw, int tpc, int k5s, const int32_t *__restrict__ gphys,
+            double *__restrict__ gpart, int *flag) {
   constexpr int DD = D * D, NC = DD * DD;
   const int NPI = npi_of<D, Q>(c_ip), NK = DD * NPI;
   const int ns = c_ip.ns;
@@ -597,11 +598,13 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
     if (i <= j) {
       const int lo = min(a, b), hi = max(a, b);
       const int o1 = sym_index(D, lo, hi), p1 = sym_index(D, i, j);
-      const double y1 = W[(size_t)(nbk * IGA_GEMM_BN + o1 * tpc + tl) * ldw + p1 * NPI + C];
+      const int k1 = p1 * NPI + C;   // logical κ row -> its balanced physical row
+      const double y1 = W[(size_t)(nbk * IGA_GEMM_BN + o1 * tpc + tl) * ldw + gphys[k1 >> 3] * 8 + (k1 & 7)];
       w = a == b ? y1 : 0.5 * y1;
       if (i < j && a != b) {
         const int o2 = anti_index(D, lo, hi), p2 = anti_index(D, i, j);
-        const double y2 = W[(size_t)(nbk * IGA_GEMM_BN + (NP1 + o2) * tpc + tl) * ldw + k5s + p2 * NPI + C];
+        const int k2 = k5s + p2 * NPI + C;
+        const double y2 = W[(size_t)(nbk * IGA_GEMM_BN + (NP1 + o2) * tpc + tl) * ldw + gphys[k2 >> 3] * 8 + (k2 & 7)];
         w = fma(a < b ? 0.5 : -0.5, y2, w);
       }
     }
@@ -1015,8 +1018,8 @@ static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double 
   cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
-                                                        ypt, nu, W, (int)h.k5_rows, h.tpc, h.k5_split, gpart,
-                                                        h.d_flag);
+                                                        ypt, nu, W, (int)h.k5_rows, h.tpc, h.k5_split,
+                                                        h.d_k5_gphys, gpart, h.d_flag);
   return cudaGetLastError();
 }
 

@@ -224,7 +224,7 @@ __global__ void k1_volume_table(int total_pts, int npi, const double *__restrict
 template <int D>
 __global__ void k1_pack(const double *__restrict__ table, int64_t M, int npi, int kstride,
                         const int32_t *__restrict__ k5_col, double *__restrict__ tabA, int nkcA, int k1,
-                        double *__restrict__ tabAT, int brT, int nkcT, int k5s) {
+                        double *__restrict__ tabAT, int brT, int nkcT, int k5s, const int32_t *__restrict__ gphys) {
   constexpr int NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2;
   const int ns = (NP1 + NP2) * npi;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -245,7 +245,7 @@ __global__ void k1_pack(const double *__restrict__ table, int64_t M, int npi, in
     kT = k5s + (sk - NP1 * npi);
   }
   tabA[fm_index(r, kA, IGA_K3_BM, nkcA)] = v;
-  tabAT[fm_index(kT, k5_col[r], brT, nkcT)] = v;
+  tabAT[fm_index(gphys[kT >> 3] * 8 + (kT & 7), k5_col[r], brT, nkcT)] = v;   // balanced κ placement
 }
 
 cudaError_t launch_pack_tables(const Handle &h, cudaStream_t s) {
@@ -253,10 +253,12 @@ cudaError_t launch_pack_tables(const Handle &h, cudaStream_t s) {
   const unsigned blocks = (unsigned)((n + 255) / 256);
   if (h.d == 2)
     k1_pack<2><<<blocks, 256, 0, s>>>(h.d_table, h.M, h.npi, h.kstride, h.d_k5_col, h.d_tabA, h.ks3 / IGA_KCHUNK,
-                                      4 * h.k3_split, h.d_tabAT, IGA_K5_BM, (int)(h.Kp / IGA_KCHUNK), h.k5_split);
+                                      4 * h.k3_split, h.d_tabAT, IGA_K5_BM, (int)(h.Kp / IGA_KCHUNK), h.k5_split,
+                                      h.d_k5_gphys);
   else
     k1_pack<3><<<blocks, 256, 0, s>>>(h.d_table, h.M, h.npi, h.kstride, h.d_k5_col, h.d_tabA, h.ks3 / IGA_KCHUNK,
-                                      4 * h.k3_split, h.d_tabAT, IGA_K5_BM, (int)(h.Kp / IGA_KCHUNK), h.k5_split);
+                                      4 * h.k3_split, h.d_tabAT, IGA_K5_BM, (int)(h.Kp / IGA_KCHUNK), h.k5_split,
+                                      h.d_k5_gphys);
   return cudaGetLastError();
 }
 
