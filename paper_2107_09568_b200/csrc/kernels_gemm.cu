@@ -533,16 +533,18 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
     }
   }
   const int k = 4 * (tid >> 5) + (lane & 3);
-  int cA[NI], cB[NI], mode[NI];   // mode 0: X_aa, 1: X_ab + X_ba, 2: X_ab − X_ba, 3: unused column
+  // column tile j holds output o = j (3D) or j/2 (2D): its mode is a compile-time constant
+  auto o_of = [](int j) { return D == 3 ? j : j >> 1; };
+  auto mode_of = [&](int j) { const int o = o_of(j); return o < D ? 0 : (o < NP1 ? 1 : (o < NP1 + NP2 ? 2 : 3)); };
+  int cA[NI], cB[NI];   // mode 0: X_aa, 1: X_ab + X_ba, 2: X_ab − X_ba, 3: unused column
 #pragma unroll
   for (int j = 0; j < NI; ++j) {
-    const int n = 8 * j + (lane >> 2), o = n / TPC, tl = n % TPC;
+    const int o = o_of(j), tl = D == 3 ? (lane >> 2) : (j & 1) * 8 + (lane >> 2);
     int a = 0, b = 0;
     if (o < NP1) sym_pair(D, o, a, b);
     else if (o < NP1 + NP2) anti_pair(D, o - NP1, a, b);
-    mode[j] = o < NP1 ? (a == b ? 0 : 1) : (o < NP1 + NP2 ? 2 : 3);
-    cA[j] = (mode[j] == 3 ? 0 : tl) * nc * D + a;
-    cB[j] = (mode[j] == 3 ? 0 : tl) * nc * D + b;
+    cA[j] = (mode_of(j) == 3 ? 0 : tl) * nc * D + a;
+    cB[j] = (mode_of(j) == 3 ? 0 : tl) * nc * D + b;
   }
   __syncthreads();
   int32_t pr = k5_pair[(int64_t)kc0 * BK + k];
@@ -554,13 +556,14 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
       const int A = (pr & 0xffff) * D, B = (pr >> 16) * D;
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
+        const int md = mode_of(j);
+        if (md == 3) { x[j] = 0.0; continue; }
         const double xab = fma(us[cB[j] + B], vs[cA[j] + A], us[cA[j] + A] * vs[cB[j] + B]);
-        if (mode[j] == 3) x[j] = 0.0;
-        else if (A == B) x[j] = mode[j] == 0 ? 0.5 * xab : xab;   // diagonal row: X_ba = 0 (a < b)
-        else if (mode[j] == 0) x[j] = xab;
+        if (md == 0) x[j] = A == B ? 0.5 * xab : xab;
+        else if (A == B) x[j] = xab;   // diagonal row: X_ba = 0 (a < b)
         else {
           const double xba = fma(us[cA[j] + B], vs[cB[j] + A], us[cB[j] + A] * vs[cA[j] + B]);
-          x[j] = mode[j] == 1 ? xab + xba : xab - xba;
+          x[j] = md == 1 ? xab + xba : xab - xba;
         }
       }
     } else {
