@@ -114,10 +114,10 @@ __device__ __forceinline__ double bernstein1(int q, int k, double x) {
 // ---- Eq. 38 (Ā_ij[a,b] = Ā_ji[b,a]) reduced contraction ("sym" layout) ----
 // Part 1 pairs / outputs: the d(d+1)/2 index pairs (a,b), a <= b, diagonal first then
 // (0,1), (0,2), (1,2); part 2: the d(d-1)/2 pairs a < b in the same order.
-__host__ __device__ __forceinline__ int sym_index(int D, int a, int b) {   // a <= b
+__host__ __device__ __forceinline__ constexpr int sym_index(int D, int a, int b) {   // a <= b
   return a == b ? a : (D == 2 ? 2 : (a == 0 ? 2 + b : 5));
 }
-__host__ __device__ __forceinline__ int anti_index(int D, int a, int b) {  // a < b
+__host__ __device__ __forceinline__ constexpr int anti_index(int D, int a, int b) {  // a < b
   return D == 2 ? 0 : (a == 0 ? b - 1 : 2);
 }
 __host__ __device__ __forceinline__ void sym_pair(int D, int o, int &a, int &b) {

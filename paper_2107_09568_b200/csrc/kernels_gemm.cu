@@ -518,11 +518,13 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const int64_t nb = blockIdx.y, t0 = nb * TPC;
   const int kc0 = pinfo[3 * p], kc1 = pinfo[3 * (p + 1)], off = pinfo[3 * p + 1], nc = pinfo[3 * p + 2];
-  double *us = smem, *vs = smem + TPC * nc * D;
+  // per-tile stride nc·D + 1 (odd): the 8 tiles a warp reads at once fall in distinct banks
+  const int ts = nc * D + 1;
+  double *us = smem, *vs = smem + TPC * ts;
   for (int i = tid; i < TPC * nc; i += 128) {
     const int tl = i / nc, A = i % nc;
     const int64_t t = t0 + tl;
-    double *uo = us + i * D, *vo = vs + i * D;
+    double *uo = us + tl * ts + A * D, *vo = vs + tl * ts + A * D;
     if (t < n_tiles) {
       const int64_t I = node_map[t * nl + off + A];
 #pragma unroll
@@ -533,42 +535,48 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
     }
   }
   const int k = 4 * (tid >> 5) + (lane & 3);
-  // column tile j holds output o = j (3D) or j/2 (2D): its mode is a compile-time constant
-  auto o_of = [](int j) { return D == 3 ? j : j >> 1; };
-  auto mode_of = [&](int j) { const int o = o_of(j); return o < D ? 0 : (o < NP1 ? 1 : (o < NP1 + NP2 ? 2 : 3)); };
-  int cA[NI], cB[NI];   // mode 0: X_aa, 1: X_ab + X_ba, 2: X_ab − X_ba, 3: unused column
+  // column tile j holds output o = j (3D) or j/2 (2D), (a, b) and the mode are compile-time
+  // constants; the thread's tile(s) tl are fixed: 3D one tile (lane/4), 2D two (lane/4, +8)
+  constexpr int NTL = D == 3 ? 1 : 2;
+  int toff[NTL];
 #pragma unroll
-  for (int j = 0; j < NI; ++j) {
-    const int o = o_of(j), tl = D == 3 ? (lane >> 2) : (j & 1) * 8 + (lane >> 2);
-    int a = 0, b = 0;
-    if (o < NP1) sym_pair(D, o, a, b);
-    else if (o < NP1 + NP2) anti_pair(D, o - NP1, a, b);
-    cA[j] = (mode_of(j) == 3 ? 0 : tl) * nc * D + a;
-    cB[j] = (mode_of(j) == 3 ? 0 : tl) * nc * D + b;
-  }
+  for (int it = 0; it < NTL; ++it) toff[it] = (it * 8 + (lane >> 2)) * ts;
   __syncthreads();
   int32_t pr = k5_pair[(int64_t)kc0 * BK + k];
   for (int kc = kc0; kc < kc1; ++kc) {
     const int32_t pr_next = kc + 1 < kc1 ? k5_pair[(int64_t)(kc + 1) * BK + k] : -1;
     double *dst = X + (nb * nkc + kc) * (int64_t)K5_X_CHUNK_ + tid;
     double x[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) x[j] = 0.0;
     if (pr >= 0) {
       const int A = (pr & 0xffff) * D, B = (pr >> 16) * D;
+      double uA[NTL][D], vA[NTL][D], uB[NTL][D], vB[NTL][D];
+#pragma unroll
+      for (int it = 0; it < NTL; ++it)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          uA[it][c] = us[toff[it] + A + c];
+          vA[it][c] = vs[toff[it] + A + c];
+          uB[it][c] = us[toff[it] + B + c];
+          vB[it][c] = vs[toff[it] + B + c];
+        }
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
-        const int md = mode_of(j);
-        if (md == 3) { x[j] = 0.0; continue; }
-        const double xab = fma(us[cB[j] + B], vs[cA[j] + A], us[cA[j] + A] * vs[cB[j] + B]);
-        if (md == 0) x[j] = A == B ? 0.5 * xab : xab;
-        else if (A == B) x[j] = xab;   // diagonal row: X_ba = 0 (a < b)
+        const int o = D == 3 ? j : j >> 1, it = D == 3 ? 0 : (j & 1);
+        if (o >= NP1 + NP2) continue;                               // unused column (2D)
+        int a = 0, b = 0;
+        if (o < NP1) sym_pair(D, o, a, b);
+        else anti_pair(D, o - NP1, a, b);
+        // X_ab = u_{I,a} v_{J,b} + u_{J,b} v_{I,a} (K5x's original arithmetic)
+        const double xab = fma(uB[it][b], vA[it][a], uA[it][a] * vB[it][b]);
+        if (o < D) x[j] = A == B ? 0.5 * xab : xab;                 // X_aa
+        else if (A == B) x[j] = xab;                                 // diagonal row: X_ba = 0 (a < b)
         else {
-          const double xba = fma(us[cA[j] + B], vs[cB[j] + A], us[cB[j] + A] * vs[cA[j] + B]);
-          x[j] = md == 1 ? xab + xba : xab - xba;
+          const double xba = fma(uB[it][a], vA[it][b], uA[it][b] * vB[it][a]);
+          x[j] = o < NP1 ? xab + xba : xab - xba;
         }
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < NI; ++j) x[j] = 0.0;
     }
 #pragma unroll
     for (int j = 0; j < NI; ++j) dst[128 * j] = x[j];
@@ -669,7 +677,7 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
 }
 
 size_t k5x_smem_bytes(int d, int max_patch_ctrl) {
-  return sizeof(double) * (size_t)2 * (d == 3 ? 8 : 16) * max_patch_ctrl * d;
+  return sizeof(double) * (size_t)2 * (d == 3 ? 8 : 16) * (max_patch_ctrl * d + 1);
 }
 
 template <int D>
