@@ -264,30 +264,33 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     if (sum == 1.2345) out[0] = sum;
     return;
 #endif
+    // stage the tile-major L_t[a][b] (column tl·DD + a·D + b) straight from the registers:
+    // a thread holds, for its rows, the symmetric (column tile o) and antisymmetric (column
+    // tile NP1 + o') outputs of the same tiles tl, so L_ab = L⁺ + L⁻, L_ba = L⁺ − L⁻ here
+    constexpr int NP1 = D * (D + 1) / 2, NH = TPC / 8;   // column tiles per output: 1 (3D), 2 (2D)
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi)
+    for (int mi = 0; mi < MI; ++mi) {
+      const int rr = warp * 16 + mi * 8 + fr;   // K3_WARPS × 16 rows
 #pragma unroll
-      for (int ni = 0; ni < NI; ++ni) {
-        const int rr = warp * 16 + mi * 8 + fr, c = ni * 8 + 2 * fc;   // K3_WARPS × 16 rows
-        sC[rr * K3_CROW + c] = acc[mi][ni][0];
-        sC[rr * K3_CROW + c + 1] = acc[mi][ni][1];
-      }
+      for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int tl = hh * 8 + 2 * fc + e;
+#pragma unroll
+          for (int ab = 0; ab < DD; ++ab) {
+            const int a = ab / D, b = ab % D, lo = a < b ? a : b, hi = a < b ? b : a;
+            const double sp = acc[mi][sym_index(D, lo, hi) * NH + hh][e];
+            double v = sp;
+            if (a != b) {
+              const double am = acc[mi][(NP1 + anti_index(D, lo, hi)) * NH + hh][e];
+              v = a < b ? sp + am : sp - am;
+            }
+            sC[rr * K3_CROW + tl * DD + ab] = v;
+          }
+        }
+    }
   }
   __syncthreads();
-  {   // sym layout (column o·TPC + tl) -> tile-major L_t[a][b] (column tl·DD + a·D + b), in
-      // place: each thread holds its row's TPT tiles in registers across the barrier
-    double v[TPT * DD];
-#pragma unroll
-    for (int k = 0; k < TPT; ++k)
-#pragma unroll
-      for (int ab = 0; ab < DD; ++ab) v[k * DD + ab] = lval<D>(sC + er * K3_CROW, et0 + k, ab / D, ab % D);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < TPT; ++k)
-#pragma unroll
-      for (int ab = 0; ab < DD; ++ab) sC[er * K3_CROW + (et0 + k) * DD + ab] = v[k * DD + ab];
-    __syncthreads();
-  }
   if (EPI == 0) {   // nzdata (Eq. 58): local[row][t*DD + a*D + b]
     const int64_t N = n_tiles * DD;
     for (int i = tid; i < K3_BM * TPC * DD; i += K3_THREADS) {
@@ -423,12 +426,16 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const bool w1 = live && ev >= 0 && riA[k] >= 0;   // riA < 0: row of another shard
     const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff), str1 = D * (riA[k] & 0xffffff);
 #pragma unroll
+#ifndef IGA_EXPERIMENT_NO_PASS1
     for (int a = 0; a < D; ++a) coop(w1 ? off1 + a * str1 : -1, er, A == B, tl, a, false);
+#endif
     const int32_t evt = emt[k];
     const bool w2 = live_t && evt >= 0 && At != Bt && riB[k] >= 0;
     const int64_t off2 = DD * (riB[k] >> 24) + D * (evt >> 16), str2 = D * (riB[k] & 0xffffff);
 #pragma unroll
+#ifndef IGA_EXPERIMENT_NO_PASS2
     for (int b = 0; b < D; ++b) coop(w2 ? off2 + b * str2 : -1, et, false, tl, b, true);
+#endif
   }
 }
 
