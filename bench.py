@@ -196,6 +196,30 @@ def cpu_baseline_oracle(n_el=(8, 4, 4), sens=True, repeats=1):
     return prob.n_tiles, best, cores, pt.nnz
 
 
+def oracle_t_cost(n_std_tiles=2):
+    """On-box T_cost (Eq. 64) of the oracle: time per tile of the standard full-Gauss
+    element matrices K^• (same n_g as the tables) over the lookup K^π (interpolation,
+    table product and scatter), both the plain NumPy oracle on the host cores, on the cfg5
+    tile.  K^• is timed on n_std_tiles tiles and the lookup on the 8-tile sample (per-tile
+    cost is uniform); quoted beside the paper's 11-107x (serial laptop CPU)."""
+    from oracle import assemble as As
+    from oracle.dofmap import DofMap, Pattern
+    from synth import make_config
+    prob = make_config(5, n_el=(2, 2, 2))
+    tabs = As.Tables(prob)
+    pt = Pattern(prob, DofMap(prob), tabs.pairs)
+    t0 = time.perf_counter()
+    As.assemble_lookup(prob, tabs, pt)
+    t_pi = (time.perf_counter() - t0) / prob.n_tiles
+    pts = As._tile_points(prob, prob.n_gauss)
+    t0 = time.perf_counter()
+    for t in range(n_std_tiles):
+        As.local_standard(prob, t, tabs.pairs, pts=pts)
+    t_std = (time.perf_counter() - t0) / n_std_tiles
+    return {"t_cost": t_std / t_pi, "s_per_tile_standard": t_std, "s_per_tile_lookup": t_pi,
+            "note": "oracle K^bullet / oracle K^pi per tile on the host cores (Eq. 64); paper: 11-107x serial"}
+
+
 # ---------------------------------------------------------------------------
 def run_reference(args, rank, world):
     if rank != 0:
@@ -381,7 +405,8 @@ def run_ours(args, rank, world):
         n_t, dt, cores, nnz = cpu_baseline_oracle(sens=sens)
         line["cpu_baseline"] = {"value": n_t / dt, "unit": "tiles/s", "cores": cores, "kind": "oracle",
                                 "sample": f"cfg5 generator at macro grid (8,4,4) = {n_t} tiles (nnz {nnz}), "
-                                          f"oracle K^pi + full gradient, {dt:.1f} s; tables/pattern untimed"}
+                                          f"oracle K^pi + full gradient, {dt:.1f} s; tables/pattern untimed",
+                                "oracle_t_cost": oracle_t_cost()}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
