@@ -3,13 +3,17 @@
 //
 // K3 (Eq. 58; "Step 3 is largely the most demanding step"):
 //   nzdata[M][N] = mat𝔎[M][K] · mat⟨Ā⟩[K][N],  M = Σ_p n_nz,p, K = d² n_π, N = d² n_tiles,
-//   with the scatter of step 4 (reading R9) fused into the epilogue: each
-//   (row, tile) d×d block goes straight to its two CSR positions (I,J) and (J,I) when
-//   it is the block's only contribution, else to a side slot that K4 sums.  The 12 GB
-//   nzdata intermediate of cfg5 is never written.
-// K5a (Eq. 73, "the product of the lookup table ... and the displacement DOF"):
-//   W[n][κ] = Σ_row mat𝔎[row][κ] X[row][n],  X generated in shared memory from u, v
-//   (staged per tile patch) — never materialised.
+//   evaluated in the Eq. 38-reduced form of DESIGN.md §6 (symmetric part: [𝔎_ii | 𝔎_ij + 𝔎_ji]
+//   against the symmetric coefficient halves; antisymmetric part: 𝔎_ij − 𝔎_ji against the
+//   antisymmetric halves; 45/81 of the multiply-adds in 3D), with the scatter of step 4
+//   (reading R9) fused into the epilogue: each (row, tile) d×d block goes
+//   straight to its two CSR positions (I,J) and (J,I) when it is the block's only
+//   contribution, else to a side slot that K4 sums.  The 12 GB nzdata intermediate of cfg5
+//   is never written.
+// K5x / K5a (Eq. 73, "the product of the lookup table ... and the displacement DOF"):
+//   X̃ (the coefficient of every local entry in uᵀK^πv, symmetric / antisymmetric combinations)
+//   is written by the memory-bound K5x; K5a contracts it with the reduced table:
+//   Y[n][κ] = Σ_row tab[row][κ] X̃[row][n].
 //
 // Operands live in HBM in the fragment-major layout of device_common.cuh (fm_index):
 // every k-chunk of a CTA tile is one contiguous block moved by ONE cp.async.bulk
@@ -17,17 +21,11 @@
 // fragment is one conflict-free 256-B LDS.64 per warp.
 //
 // DMMA issue: ptxas gives every DMMA a fixed 15-cycle stall plus a NOP, so one warp
-// issues at most one DMMA per 16 cycles = the per-SM-sub-partition pipe rate.  Both
-// GEMMs are therefore warp-specialised: 8 MMA warps (2 per sub-partition) that only
-// wait on mbarriers, load fragments and issue DMMA, beside helper warps.
-// K3: persistent (one CTA per SM), CTA tile 128 rows × 72 columns (8 tiles in 3D),
-//   8 MMA warps of 16×72 (2×9 DMMA tiles), 4 epilogue warps that scatter the previous
-//   tile while the MMA warps compute the next; MMA warp 0 refills the 4-stage ring with
-//   bulk copies once all MMA warps released a stage (an mbarrier wait: measured faster
-//   here than letting the last releasing warp refill, which K5a uses).  Work order M-blocks fastest: the
-//   resident CTAs share one coefficient block and the table stays L2-resident.
-// K5a: CTA 128 κ-rows × 72 columns, 8 MMA warps of 16×72, 4 warps generating X into a
-//   4-stage ring (one of their lanes streams the table); long reduction over all rows.
+// issues at most one DMMA per 16 cycles; an SM needs ~16 MMA warps to keep its FP64 tensor
+// pipe busy.  K3: 64×72 CTA tiles, 4 MMA warps, 4 CTAs per SM, the same warps run the
+// scatter after the main loop (co-resident CTAs keep the pipe busy meanwhile).  K5a: one
+// CTA per 72-column N-block over all κ rows, 16 MMA warps.  Both: the last warp to release
+// a stage refills it.
 #include "device_common.cuh"
 
 namespace iga {
@@ -44,38 +42,9 @@ constexpr int K5_X_CHUNK_ = BN * BK;                                        // d
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
-// KS k-steps (≤ 4) of a k-chunk of a warp's 16×72 tile; sA/sB are FM chunks, g0 = first
-// 8-row group of the warp in sA.  KS is a template parameter so that the loop is fully
-// unrolled and the fragment loads of step kk+1 are scheduled under the DMMAs of step kk.
-// MIC <= MI: only the first MIC 8-row groups (the rest of the warp's rows are padding)
-template <int KS, int MIC = MI>
-__device__ __forceinline__ void mma_chunk_fm(const double *__restrict__ sA, const double *__restrict__ sB, int g0,
-                                             int lane, double (&acc)[MI][NI][2]) {
-#pragma unroll
-  for (int kk = 0; kk < KS; ++kk) {
-    double a[MI], b[NI];
-#pragma unroll
-    for (int mi = 0; mi < MIC; ++mi) a[mi] = sA[((g0 + mi) * 4 + kk) * 32 + lane];
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni) b[ni] = sB[(ni * 4 + kk) * 32 + lane];
-#pragma unroll
-    for (int mi = 0; mi < MIC; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-  }
-}
-
-template <int MIC = MI>
-__device__ __forceinline__ void mma_chunk_tail(const double *__restrict__ sA, const double *__restrict__ sB, int g0,
-                                               int lane, int ks, double (&acc)[MI][NI][2]) {
-  switch (ks) {
-    case 1: mma_chunk_fm<1, MIC>(sA, sB, g0, lane, acc); break;
-    case 2: mma_chunk_fm<2, MIC>(sA, sB, g0, lane, acc); break;
-    case 3: mma_chunk_fm<3, MIC>(sA, sB, g0, lane, acc); break;
-    default: mma_chunk_fm<4, MIC>(sA, sB, g0, lane, acc); break;
-  }
-}
-
+// Fragment loads: sA/sB are FM chunks, g0 = first 8-row group of the warp in sA; the k-step
+// loops are template-unrolled so that the fragment loads of step kk+1 are scheduled under the
+// DMMAs of step kk.
 // Eq. 38-reduced contraction: the GEMM columns are part 1 (P1 pairs × n_π,
 // against the symmetric outputs = DMMA column tiles [0, 6)) then part 2 (P2 pairs × n_π,
 // against the antisymmetric outputs = column tiles [6, NE), NE = 9 in 3D, 8 in 2D).
@@ -122,17 +91,6 @@ __device__ __forceinline__ void k3_chunk(const double *__restrict__ sA, const do
     mma_steps_n<0, MIC, 0, 6>(sA, sB, g0, lane, 0, j < ns ? j : ns, acc);
     if (j < ns) mma_steps_n<0, MIC, 6, NE>(sA, sB, g0, lane, j, ns - j, acc);
   }
-}
-
-// L_t[a][b] of tile tl from a staged row of the sym-layout output (column o*TPC + tl):
-// L⁺'_ab + L⁻'_ab (a < b), L⁺'_ba − L⁻'_ba (a > b), L⁺'_aa (a = b)
-template <int D>
-__device__ __forceinline__ double lval(const double *row, int tl, int a, int b) {
-  constexpr int TPC = D == 3 ? 8 : 16, NP1 = D * (D + 1) / 2;
-  if (a == b) return row[a * TPC + tl];
-  const int lo = a < b ? a : b, hi = a < b ? b : a;
-  const double sp = row[sym_index(D, lo, hi) * TPC + tl], am = row[(NP1 + anti_index(D, lo, hi)) * TPC + tl];
-  return a < b ? sp + am : sp - am;
 }
 
 // one d-double row segment of a CSR block row: the 16-B aligned pair goes out as one

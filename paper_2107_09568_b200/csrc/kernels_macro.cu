@@ -164,37 +164,6 @@ __device__ void macro_J(const InterpConst &c_ip, const MacroTile<D> &mt, int m, 
   }
 }
 
-// J at sample node m for a B-spline (non-rational) macro tile: nested loops over the
-// (p+1)^d active functions with the 1D values hoisted per direction (no div/mod per
-// control point); ∂_β N_r = Π_k (k == β ? D1 : B1)[k][m_k][r_k] (K2's hot loop)
-template <int D>
-__device__ __forceinline__ void macro_J_bspline(const InterpConst &c_ip, const MacroTile<D> &mt, int m, double J[D][D]) {
-  const int mm[3] = {m % c_ip.mv[0], (m / c_ip.mv[0]) % c_ip.mv[1], m / (c_ip.mv[0] * c_ip.mv[1])};
-  const int n0 = c_ip.pm[0] + 1, n1 = c_ip.pm[1] + 1, n2 = D == 3 ? c_ip.pm[2] + 1 : 1;
-  const double *B0 = mt.B1[0][mm[0]], *D0 = mt.D1[0][mm[0]];
-  const double *B1 = mt.B1[1][mm[1]], *D1 = mt.D1[1][mm[1]];
-  const double *B2 = mt.B1[D - 1][mm[D - 1]], *D2 = mt.D1[D - 1][mm[D - 1]];
-  for (int a = 0; a < D; ++a)
-    for (int b = 0; b < D; ++b) J[a][b] = 0.0;
-  const double *P = mt.P;
-  for (int r2 = 0; r2 < n2; ++r2) {
-    const double b2 = D == 3 ? B2[r2] : 1.0, d2 = D == 3 ? D2[r2] : 0.0;
-    for (int r1 = 0; r1 < n1; ++r1) {
-      const double b12 = B1[r1] * b2, d12 = D1[r1] * b2, b1d2 = B1[r1] * d2;
-      for (int r0 = 0; r0 < n0; ++r0, P += D) {
-        const double b0 = B0[r0], g0 = D0[r0] * b12, g1 = b0 * d12, g2 = b0 * b1d2;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const double x = P[a];
-          J[a][0] = fma(x, g0, J[a][0]);
-          J[a][1] = fma(x, g1, J[a][1]);
-          if (D == 3) J[a][D - 1] = fma(x, g2, J[a][D - 1]);
-        }
-      }
-    }
-  }
-}
-
 // column β of J at sample node m for a B-spline macro tile: col[a] = Σ_r P_r[a] ∂_β N_r
 template <int D>
 __device__ __forceinline__ void macro_Jcol_bspline(const InterpConst &c_ip, const MacroTile<D> &mt, int m, int be,
