@@ -351,19 +351,26 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     emt[k] = live_t ? emap[t * M + rt] : 0;
     riB[k] = live_t ? rowinfo[t * nl + Bt] : 0;
   }
-  // lanes hold (o = CSR offset of their row segment or -1, smem row, diagonal?); word w of
-  // the warp comes from lane w/D, column w%D; value L[ra][cb] of that lane's block
-  auto coop = [&](int64_t o, int srow, bool dg, int tl, int idx, bool transposed) {
+  // lanes hold (o = CSR offset of their block's first row segment or -1, row stride,
+  // smem row | diagonal << 8); word w of the warp's row segments comes from lane w/D,
+  // column w%D, and the D row segments of a block are o, o + stride, ...: one set of
+  // shuffles per block serves its D rows; value L[ra][cb] of that lane's block
+  auto coop = [&](int64_t o, int str, int pk, int tl, bool transposed) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const int w = 32 * j + lane, src = w / D, c = w - src * D;
       const int64_t ob = __shfl_sync(0xffffffffu, o, src);
-      const int sb = __shfl_sync(0xffffffffu, srow, src);
-      const bool db = __shfl_sync(0xffffffffu, (int)dg, src) != 0;
+      const int sstr = __shfl_sync(0xffffffffu, str, src);
+      const int p = __shfl_sync(0xffffffffu, pk, src);
       if (ob >= 0) {
-        int ra = transposed ? c : idx, cb = transposed ? idx : c;
-        if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
-        out[ob + c] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+        const int sb = p & 0xff;
+        const bool db = (p >> 8) & 1;
+#pragma unroll
+        for (int idx = 0; idx < D; ++idx) {
+          int ra = transposed ? c : idx, cb = transposed ? idx : c;
+          if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+          out[ob + (int64_t)idx * sstr + c] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+        }
       }
     }
   };
@@ -382,17 +389,17 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
       for (int q = 0; q < DD; ++q) o[q] = L[tl * DD + q];
     }
     const bool w1 = live && ev >= 0 && riA[k] >= 0;   // riA < 0: row of another shard
-    const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff), str1 = D * (riA[k] & 0xffffff);
-#pragma unroll
+    const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff);
+    const int str1 = D * (int)(riA[k] & 0xffffff);
 #ifndef IGA_EXPERIMENT_NO_PASS1
-    for (int a = 0; a < D; ++a) coop(w1 ? off1 + a * str1 : -1, er, A == B, tl, a, false);
+    coop(w1 ? off1 : -1, str1, er | (A == B ? 256 : 0), tl, false);
 #endif
     const int32_t evt = emt[k];
     const bool w2 = live_t && evt >= 0 && At != Bt && riB[k] >= 0;
-    const int64_t off2 = DD * (riB[k] >> 24) + D * (evt >> 16), str2 = D * (riB[k] & 0xffffff);
-#pragma unroll
+    const int64_t off2 = DD * (riB[k] >> 24) + D * (evt >> 16);
+    const int str2 = D * (int)(riB[k] & 0xffffff);
 #ifndef IGA_EXPERIMENT_NO_PASS2
-    for (int b = 0; b < D; ++b) coop(w2 ? off2 + b * str2 : -1, et, false, tl, b, true);
+    coop(w2 ? off2 : -1, str2, et, tl, true);
 #endif
   }
 }
