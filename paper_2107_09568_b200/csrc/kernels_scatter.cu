@@ -72,26 +72,31 @@ k4_multi(const double *__restrict__ side, const MultiBlock *__restrict__ mblk, c
   }
   __syncwarp();
   const int wbase = tid & ~31;
-  auto coop = [&](int64_t o, bool dg, int pass, int idx) {
+  // lanes hold (o = CSR offset of their block's first row segment or -1, row stride,
+  // diagonal?); word w of the warp's row segments comes from lane w/D, column w%D, and the
+  // D row segments of a block are o, o + stride, ...: one set of shuffles per block
+  auto coop = [&](int64_t o, int str, bool dg, int pass) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const int w = 32 * j + lane, src = w / D, c = w - src * D;
       const int64_t ob = __shfl_sync(0xffffffffu, o, src);
+      const int sstr = __shfl_sync(0xffffffffu, str, src);
       const bool db = __shfl_sync(0xffffffffu, (int)dg, src) != 0;
       if (ob >= 0) {
-        int ra = pass ? c : idx, cb = pass ? idx : c;
-        if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
-        vals[ob + c] = sacc[pass][(wbase + src) * DD + ra * D + cb];
+#pragma unroll
+        for (int idx = 0; idx < D; ++idx) {
+          int ra = pass ? c : idx, cb = pass ? idx : c;
+          if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+          vals[ob + (int64_t)idx * sstr + c] = sacc[pass][(wbase + src) * DD + ra * D + cb];
+        }
       }
     }
   };
   const bool dg1 = b1.off_ij == b1.off_ji;
-#pragma unroll
-  for (int a = 0; a < D; ++a) coop(live ? b1.off_ij + a * b1.stride_i : -1, dg1, 0, a);
+  coop(live ? b1.off_ij : -1, b1.stride_i, dg1, 0);
   // diagonal blocks are complete after pass 1; off_ji < 0: row J belongs to another shard
   const bool w2 = live && b2.off_ji >= 0 && b2.off_ij != b2.off_ji;
-#pragma unroll
-  for (int b = 0; b < D; ++b) coop(w2 ? b2.off_ji + b * b2.stride_j : -1, false, 1, b);
+  coop(w2 ? b2.off_ji : -1, b2.stride_j, false, 1);
 }
 
 // row_ptr / col_idx of the scalar CSR from the block CSR (interleaved DOFs, R9).
