@@ -556,7 +556,10 @@ k5x_gen(const int32_t *__restrict__ k5_pair, const int32_t *__restrict__ pinfo, 
   }
 }
 
-constexpr int K5_STAGES = 4;
+#ifndef IGA_K5_STAGES
+#define IGA_K5_STAGES 4
+#endif
+constexpr int K5_STAGES = IGA_K5_STAGES;
 constexpr int K5_A_CHUNK = BM * BK, K5_B_CHUNK = BN * BK;   // doubles
 constexpr int K5_WP = BM + 1;                                // W staging pitch
 constexpr int K5_THREADS = 32 * N_MMA_WARPS;
