@@ -697,7 +697,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       sload[bb * 4 + ss] += w;
       bload[bb] += w;
     }
-    h.k5_gphys.assign(G1 + G2, 0);
+    h.k5_gphys.assign(h.k5_rows / 8, 0);   // unused tail groups: 0 (never read)
     h.k5_mode.assign(nbk * W, 0);
     auto part = [&](int g) { return g < 0 ? 0 : (g < G1 ? 1 : 2); };
     for (int b = 0; b < nbk; ++b)
