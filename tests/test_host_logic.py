@@ -210,3 +210,62 @@ def test_shard_gradient_allreduce_gloo():
     full = res[0][2]
     for r in range(2):
         assert np.abs(res[r][1] - full).max() < 1e-13 * np.abs(full).max()
+
+
+# ---------------------------------------------------------------------------
+# The Eq. 38-reduced contraction the GPU evaluates, checked on the host
+# against the oracle's plain Eq. 58 product: L = L⁺ ± L⁻ with L⁺ from [𝔎_ii | 𝔎_ij + 𝔎_ji]
+# and the symmetric coefficient halves, L⁻ from 𝔎_ij − 𝔎_ji and the antisymmetric halves;
+# and uᵀK^πv = Σ (X̃⁺ L⁺ + X̃⁻ L⁻).  (Design identity, numpy; no CUDA.)
+
+def _sym_pairs(d):
+    p1 = [(a, a) for a in range(d)] + [(a, b) for a in range(d) for b in range(a + 1, d)]
+    p2 = [(a, b) for a in range(d) for b in range(a + 1, d)]
+    return p1, p2
+
+
+@pytest.mark.parametrize("c,kw", [(1, {}), (2, dict(n_el=(2, 1, 1))), (2, dict(n_el=(2, 1, 1), q=(1, 2, 3)))])
+def test_eq38_reduced_contraction_identity(c, kw):
+    from oracle import assemble as As, macro as M, sensitivity as S
+    from oracle.dofmap import DofMap, Pattern
+    from synth import make_config, draw_uv_seeded
+    prob = make_config(c, **kw)
+    d = prob.d
+    tabs = As.Tables(prob)
+    dm = DofMap(prob)
+    pt = Pattern(prob, dm, tabs.pairs)
+    npi = tabs.T.shape[1] // (d * d)
+    T = tabs.T.reshape(-1, d, d, npi)                       # [r][i][j][C]
+    p1, p2 = _sym_pairs(d)
+    A1 = np.concatenate([T[:, i, i] if i == j else T[:, i, j] + T[:, j, i] for i, j in p1], axis=1)
+    A2 = np.concatenate([T[:, i, j] - T[:, j, i] for i, j in p2], axis=1)
+    # multiply-adds per row and tile: n_π(n_p1² + n_p2²) (45 n_π in 3D, 10 n_π in 2D) < d⁴ n_π
+    assert A1.shape[1] * len(p1) + A2.shape[1] * len(p2) == (len(p1) ** 2 + len(p2) ** 2) * npi < d ** 4 * npi
+    u, v = draw_uv_seeded(c + 70, dm.n_dof)
+    utkv = 0.0
+    for t in range(prob.n_tiles):
+        coef = M.tile_coefficients(prob, prob.macro.ctrl, t)   # [C][i][j][a][b]
+        B1 = np.stack([np.concatenate([0.5 * (coef[:, i, j, a, b] + coef[:, i, j, b, a]) for i, j in p1])
+                       for a, b in p1], axis=1)
+        B2 = np.stack([np.concatenate([0.5 * (coef[:, i, j, a, b] - coef[:, i, j, b, a]) for i, j in p2])
+                       for a, b in p2], axis=1)
+        Lp, Lm = A1 @ B1, A2 @ B2                           # L⁺/2 and L⁻/2 per output pair
+        L = np.zeros((T.shape[0], d, d))
+        for o, (a, b) in enumerate(p1):
+            L[:, a, b] += Lp[:, o]
+            if a != b:
+                L[:, b, a] += Lp[:, o]
+        for o, (a, b) in enumerate(p2):
+            L[:, a, b] += Lm[:, o]
+            L[:, b, a] -= Lm[:, o]
+        ref = As.local_lookup(prob, tabs, prob.macro.ctrl, [t])[0]
+        assert np.linalg.norm(L - ref) <= 1e-13 * np.linalg.norm(ref)
+        X = S.adjoint_X(prob, pt, u, v, t)                  # [r][a][b]
+        Xp = np.stack([X[:, a, b] if a == b else X[:, a, b] + X[:, b, a] for a, b in p1], axis=1)
+        Xm = np.stack([X[:, a, b] - X[:, b, a] for a, b in p2], axis=1)
+        utkv += np.sum(Xp * Lp) + np.sum(Xm * Lm)
+    K = As.assemble_lookup(prob, tabs, pt)[0]
+    import scipy.sparse as sp
+    Kc = sp.csr_matrix((K, pt.col_idx(), pt.row_ptr), shape=(dm.n_dof, dm.n_dof))
+    ref = u @ (Kc @ v)
+    assert abs(utkv - ref) <= 1e-12 * abs(ref)
