@@ -13,7 +13,7 @@ Handle::~Handle() {
   void *bufs[] = {d_table, d_tabA, d_tabAT, d_coef, d_side, d_W, d_X, d_gpart, d_node_map, d_pairA, d_pairB,
                   d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_mperm, d_slot_tr,
                   d_k5_pair, d_k5_col, d_tperm, d_g1len, d_g2len, d_g1slot, d_g2slot, d_sA_ptr, d_sA_slot,
-                  d_inv_ptr, d_inv_ent, d_part, d_k5_gphys, d_k5_mode, d_F, d_th, d_det, d_Vt, d_mweights, d_patch_info, d_mknots, d_mspan, d_flag};
+                  d_inv_ptr, d_inv_ent, d_part, d_k5_gphys, d_k5_mode, d_Wpart, d_F, d_th, d_det, d_Vt, d_mweights, d_patch_info, d_mknots, d_mspan, d_flag};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (int i = 0; i < N_STAGE; ++i)
@@ -217,6 +217,19 @@ iga_status iga_build_tables_q(const iga_spline *tile_patches, int32_t n_patches,
   CUB(cudaMalloc((void **)&h.d_coef, sizeof(double) * h.Npad * h.ks3));
   CUB(cudaMemsetAsync(h.d_coef, 0, sizeof(double) * h.Npad * h.ks3, s));
   CUB(cudaMalloc((void **)&h.d_W, sizeof(double) * h.Npad * h.k5_rows));
+  {   // K5a split-K: the segment count minimising waves-per-unit-of-work on this GPU's SMs
+    int dev = 0, nsm = 148;
+    CUB(cudaGetDevice(&dev));
+    CUB(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc, nkb = h.k5_rows / IGA_K5_BM;
+    const double w1 = (double)((nblk * nkb + nsm - 1) / nsm);
+    double best = w1;
+    for (int S = 2; S <= 16 && S <= (int)(h.Kp / IGA_KCHUNK); ++S) {
+      const double waves = (double)((nblk * nkb * S + nsm - 1) / nsm) / S;
+      if (waves < best - 1e-9 && waves < 0.9 * w1) { best = waves; h.k5_nseg = S; }   // worth the partials
+    }
+    if (h.k5_nseg > 1) CUB(cudaMalloc((void **)&h.d_Wpart, sizeof(double) * h.k5_nseg * h.Npad * h.k5_rows));
+  }
   CUB(cudaMalloc((void **)&h.d_F, sizeof(double) * h.n_local_ctrl * h.npi));
   CUB(cudaMalloc((void **)&h.d_th, sizeof(double) * h.npi));
   CUB(cudaMalloc((void **)&h.d_det, sizeof(double) * h.n_tiles * h.npi));

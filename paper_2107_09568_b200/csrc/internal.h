@@ -111,6 +111,8 @@ struct Handle {
   // K5a balance: logical 8-row κ group g -> physical group (block·16 + warp·2 + mi), chosen so
   // that every CTA and sub-partition carries a similar DMMA load (part-1 groups cost 6 column
   // tiles, part-2 groups 3); per (κ-block, warp) the parts of its two groups (mode p0·3 + p1)
+  int k5_nseg = 1;                   // K5a split-K segments (small problems: fill the SMs)
+  double *d_Wpart = nullptr;         // [k5_nseg][blocks·72][k5_rows] partial Y (k5_nseg > 1)
   std::vector<int32_t> k5_gphys;
   std::vector<uint8_t> k5_mode;
   int32_t *d_k5_gphys = nullptr;

@@ -582,7 +582,13 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   int *released = reinterpret_cast<int *>(full + K5_STAGES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t kb = blockIdx.x, nb = blockIdx.y;
-  const double *gA = tabAT + kb * (int64_t)nkc * K5_A_CHUNK, *gB = X + nb * (int64_t)nkc * K5_B_CHUNK;
+  // split-K for small problems (too few N-blocks to fill the SMs): segment z of the reduction
+  // writes its own partial Y, summed in segment order by k5a_reduce
+  const int kc_lo = (int)((int64_t)blockIdx.z * nkc / gridDim.z), kc_hi = (int)((int64_t)(blockIdx.z + 1) * nkc / gridDim.z);
+  const double *gA = tabAT + (kb * (int64_t)nkc + kc_lo) * K5_A_CHUNK;
+  const double *gB = X + (nb * (int64_t)nkc + kc_lo) * K5_B_CHUNK;
+  nkc = kc_hi - kc_lo;
+  Wout += (int64_t)blockIdx.z * N * ldw;
   // part (1, 2; 0 = padding) of each of the warp's two 8-row groups: part(mi0)·3 + part(mi1)
   // (host-balanced placement of the κ groups, Handle::k5_gphys)
   const int mode = k5_mode[kb * N_MMA_WARPS + warp];
@@ -672,15 +678,31 @@ cudaError_t launch_sens_X(const Handle &h, const double *u, const double *v, cud
   return h.d == 2 ? launch_k5x<2>(h, u, v, s) : launch_k5x<3>(h, u, v, s);
 }
 
+// Y = Σ_z partial_z in segment order (deterministic)
+__global__ void k5a_reduce(const double *__restrict__ part, int nseg, int64_t n, double *__restrict__ Y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = part[i];
+  for (int z = 1; z < nseg; ++z) acc += part[(int64_t)z * n + i];
+  Y[i] = acc;
+}
+
 template <int D>
 static cudaError_t launch_k5a(const Handle &h, double *W, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k5a_wgemm<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM);
   if (e) return e;
   const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc;   // N-blocks of the owned tiles
-  dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)nblk);
+  const int nseg = h.k5_nseg;
+  dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)nblk, (unsigned)nseg);
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k5a_wgemm<D><<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), nblk * BN, W, (int)h.k5_rows,
+  double *out = nseg > 1 ? h.d_Wpart : W;
+  k5a_wgemm<D><<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), nblk * BN, out, (int)h.k5_rows,
                                                  h.d_k5_mode);
+  if ((e = cudaGetLastError())) return e;
+  if (nseg > 1) {
+    const int64_t n = nblk * BN * h.k5_rows;
+    k5a_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.d_Wpart, nseg, n, W);
+  }
   return cudaGetLastError();
 }
 
