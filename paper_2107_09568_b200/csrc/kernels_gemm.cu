@@ -571,7 +571,7 @@ static_assert(sizeof(double) * BN * K5_WP <= K5_OFF_BAR, "W staging must fit in 
 // 16×72; the last MMA warp to release a stage refills it.  Eq. 38-reduced:
 // κ rows of part 1 (< k5s) meet the symmetric columns (tiles [0, 6)), part 2 rows
 // (< k5k) the antisymmetric ones ([6, NE)); no DMMA for the other pairings or padding.
-template <int D>
+template <int D, bool SPLIT>
 __global__ void __launch_bounds__(K5_THREADS, 1)
 k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nkc, int64_t N,
           double *__restrict__ Wout, int ldw, const uint8_t *__restrict__ k5_mode) {
@@ -584,11 +584,15 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   const int64_t kb = blockIdx.x, nb = blockIdx.y;
   // split-K for small problems (too few N-blocks to fill the SMs): segment z of the reduction
   // writes its own partial Y, summed in segment order by k5a_reduce
-  const int kc_lo = (int)((int64_t)blockIdx.z * nkc / gridDim.z), kc_hi = (int)((int64_t)(blockIdx.z + 1) * nkc / gridDim.z);
-  const double *gA = tabAT + (kb * (int64_t)nkc + kc_lo) * K5_A_CHUNK;
-  const double *gB = X + (nb * (int64_t)nkc + kc_lo) * K5_B_CHUNK;
-  nkc = kc_hi - kc_lo;
-  Wout += (int64_t)blockIdx.z * N * ldw;
+  const double *gA = tabAT + kb * (int64_t)nkc * K5_A_CHUNK, *gB = X + nb * (int64_t)nkc * K5_B_CHUNK;
+  if (SPLIT) {
+    const int kc_lo = (int)((int64_t)blockIdx.z * nkc / gridDim.z);
+    const int kc_hi = (int)((int64_t)(blockIdx.z + 1) * nkc / gridDim.z);
+    gA += (int64_t)kc_lo * K5_A_CHUNK;
+    gB += (int64_t)kc_lo * K5_B_CHUNK;
+    nkc = kc_hi - kc_lo;
+    Wout += (int64_t)blockIdx.z * N * ldw;
+  }
   // part (1, 2; 0 = padding) of each of the warp's two 8-row groups: part(mi0)·3 + part(mi1)
   // (host-balanced placement of the κ groups, Handle::k5_gphys)
   const int mode = k5_mode[kb * N_MMA_WARPS + warp];
@@ -689,15 +693,21 @@ __global__ void k5a_reduce(const double *__restrict__ part, int nseg, int64_t n,
 
 template <int D>
 static cudaError_t launch_k5a(const Handle &h, double *W, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k5a_wgemm<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM);
+  const bool split = h.k5_nseg > 1;
+  cudaError_t e = cudaFuncSetAttribute(split ? k5a_wgemm<D, true> : k5a_wgemm<D, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM);
   if (e) return e;
   const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc;   // N-blocks of the owned tiles
   const int nseg = h.k5_nseg;
   dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)nblk, (unsigned)nseg);
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   double *out = nseg > 1 ? h.d_Wpart : W;
-  k5a_wgemm<D><<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), nblk * BN, out, (int)h.k5_rows,
-                                                 h.d_k5_mode);
+  if (split)
+    k5a_wgemm<D, true><<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), nblk * BN, out,
+                                                         (int)h.k5_rows, h.d_k5_mode);
+  else
+    k5a_wgemm<D, false><<<grid, K5_THREADS, K5_SMEM, s>>>(h.d_tabAT, h.d_X, (int)(h.Kp / BK), nblk * BN, out,
+                                                          (int)h.k5_rows, h.d_k5_mode);
   if ((e = cudaGetLastError())) return e;
   if (nseg > 1) {
     const int64_t n = nblk * BN * h.k5_rows;
