@@ -538,8 +538,11 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
 
 // K5b: one CTA per tile: Ŵ = Πᵀ W at the m^d sample nodes, reverse mode of
 // S = ⟨Ŵ, Ā(J)⟩ per node, chain to the active macro control points.
+#ifndef IGA_K5B_THREADS
+#define IGA_K5B_THREADS 128   // per tile; several tiles' CTAs per SM overlap the per-node phase
+#endif
 template <int D, int Q>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(IGA_K5B_THREADS)
 k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
             const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
             const double *__restrict__ W, int ldw, int tpc, int k5s, const int32_t *__restrict__ gphys,
@@ -986,7 +989,7 @@ static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double 
   const size_t sm = macro_smem_bytes(D, h.ns, true);
   cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
-  k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
+  k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, IGA_K5B_THREADS, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
                                                         ypt, nu, W, (int)h.k5_rows, h.tpc, h.k5_split,
                                                         h.d_k5_gphys, gpart, h.d_flag);
   return cudaGetLastError();
