@@ -8,11 +8,12 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--apply", action="store_true")
+    ap.add_argument("--q", type=int, default=None, help="projection degree override (e.g. the Eq. 65 choice)")
     args = ap.parse_args()
     import torch
     from paper_2107_09568_b200 import Assembler
     from synth import make_config, draw_uv_seeded
-    prob = make_config(args.config)
+    prob = make_config(args.config, q=args.q)
     A = Assembler(prob)
     s = A.sizes
     dev = torch.device("cuda")
