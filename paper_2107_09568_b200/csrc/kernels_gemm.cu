@@ -172,8 +172,10 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     }
     mbar_fence_init();
   }
+#ifndef IGA_EXPERIMENT_NO_PREFETCH
   if (EPI == 1 && r < M)   // warm L2 with the epilogue's maps while the main loop runs
     for (int tl = et0; tl < et0 + TPT && t0 + tl < n_tiles; ++tl) prefetch_l2(emap + (t0 + tl) * M + r);
+#endif
   __syncthreads();
   auto produce = [&](int kc) {
     const int st = kc % K3_STAGES;
