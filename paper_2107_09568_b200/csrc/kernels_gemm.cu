@@ -132,7 +132,17 @@ constexpr size_t K3_STAGE_BYTES = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHU
 constexpr size_t K3_EPI_BYTES = sizeof(double) * (size_t)K3_BM * (K3_CROW + 4 * 3);   // staging + apply runs
 constexpr size_t K3_OFF_BAR = K3_STAGE_BYTES > K3_EPI_BYTES ? K3_STAGE_BYTES : K3_EPI_BYTES;
 constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int));
-static_assert(K3_THREADS == 2 * K3_BM, "epilogue: two threads (tile halves) per row");
+#ifndef IGA_K3_MI
+#define IGA_K3_MI 2   // 8-row DMMA groups per K3 MMA warp for EPI 0/1 (the apply epilogue keeps 2)
+#endif
+// per-epilogue K3 shape: MMA warps of 8·MI rows, threads = 32·warps, CTAs per SM hint
+template <int EPI>
+struct K3Cfg {
+  static constexpr int KMI = EPI == 2 ? 2 : IGA_K3_MI;
+  static constexpr int WARPS = K3_BM / (8 * KMI), THREADS = 32 * WARPS;
+  static constexpr int MINB = KMI == 2 ? 256 / K3_BM : 3;
+  static_assert(THREADS % K3_BM == 0, "epilogue: whole threads per row");
+};
 
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
@@ -148,13 +158,14 @@ struct ApplyArgs {
 // EPI = 0: local[M][N] (nzdata, Eq. 58) ; EPI = 1: fused CSR scatter (+ side slots);
 // EPI = 2: matrix-free apply y = K^π u (Eq. 74): block products summed into partial slots
 template <int D, int EPI>
-__global__ void __launch_bounds__(K3_THREADS, 256 / K3_BM)
+__global__ void __launch_bounds__(K3Cfg<EPI>::THREADS, K3Cfg<EPI>::MINB)
 k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int ksplit, int64_t M,
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
             int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm, const ApplyArgs ap) {
   // tiles per CTA (sym layout: 8 in 3D, 16 in 2D), per epilogue thread; part-2 column tiles end
-  constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, TPT = TPC / 2, NE = D == 3 ? 9 : 8;
+  constexpr int KMI = K3Cfg<EPI>::KMI, KW = K3Cfg<EPI>::WARPS, KT = K3Cfg<EPI>::THREADS;
+  constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, TPT = TPC / (KT / K3_BM), NE = D == 3 ? 9 : 8;
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K3_STAGES * K3_A_CHUNK;
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K3_OFF_BAR);
@@ -192,19 +203,20 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
   // 8-row groups of this warp that hold table rows < M (the rest is the zero padding of
   // the last row block: no DMMA is issued for it)
-  const int nmi = m0 + warp * 16 >= M ? 0 : (m0 + warp * 16 + 8 >= M ? 1 : 2);
+  const int64_t wr0 = m0 + warp * 8 * KMI;
+  const int nmi = wr0 >= M ? 0 : (KMI == 2 && wr0 + 8 < M ? 2 : 1);
   for (int kc = 0; kc < nkc; ++kc) {
     const int st = kc % K3_STAGES;
     mbar_wait(&full[st], (kc / K3_STAGES) & 1);
     const double *a_st = sA + st * K3_A_CHUNK, *b_st = sB + st * K3_B_CHUNK;
     // k-steps of this chunk and the first one of part 2 (Eq. 38-reduced contraction)
     const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), j = max(0, min(ksplit - s0, ns));
-    if (nmi == 2) k3_chunk<2, NE>(a_st, b_st, warp * MI, lane, ns, j, acc);
-    else if (nmi == 1) k3_chunk<1, NE>(a_st, b_st, warp * MI, lane, ns, j, acc);
+    if (nmi == 2) k3_chunk<2, NE>(a_st, b_st, warp * KMI, lane, ns, j, acc);
+    else if (nmi == 1) k3_chunk<1, NE>(a_st, b_st, warp * KMI, lane, ns, j, acc);
     __syncwarp();
     if (lane == 0) {   // the last warp to release a stage refills it
       __threadfence_block();
-      if (atomicAdd(&released[st], 1) == K3_WARPS - 1) {
+      if (atomicAdd(&released[st], 1) == KW - 1) {
         released[st] = 0;
         __threadfence_block();
         if (kc + K3_STAGES < nkc) produce(kc + K3_STAGES);
@@ -229,8 +241,8 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     // tile NP1 + o') outputs of the same tiles tl, so L_ab = L⁺ + L⁻, L_ba = L⁺ − L⁻ here
     constexpr int NP1 = D * (D + 1) / 2, NH = TPC / 8;   // column tiles per output: 1 (3D), 2 (2D)
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) {
-      const int rr = warp * 16 + mi * 8 + fr;   // K3_WARPS × 16 rows
+    for (int mi = 0; mi < KMI; ++mi) {
+      const int rr = warp * 8 * KMI + mi * 8 + fr;   // KW warps × 8·KMI rows
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh)
 #pragma unroll
@@ -253,7 +265,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   __syncthreads();
   if (EPI == 0) {   // nzdata (Eq. 58): local[row][t*DD + a*D + b]
     const int64_t N = n_tiles * DD;
-    for (int i = tid; i < K3_BM * TPC * DD; i += K3_THREADS) {
+    for (int i = tid; i < K3_BM * TPC * DD; i += KT) {
       const int rr = i / (TPC * DD), c = i % (TPC * DD), tl = c / DD, ab = c % DD;
       const int64_t gr = m0 + rr, t = t0 + tl;
       if (gr < M && t < n_tiles) out[gr * N + t * DD + ab] = sC[rr * K3_CROW + c];
@@ -412,7 +424,7 @@ static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, Apply
   if (e) return e;
   dim3 grid((unsigned)(h.Mpad / K3_BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  k3_contract<D, EPI><<<grid, K3_THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
+  k3_contract<D, EPI><<<grid, K3Cfg<EPI>::THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
                                                         h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,
                                                         h.n_local_ctrl, h.d_side, h.d_tperm, ap);
   return cudaGetLastError();
