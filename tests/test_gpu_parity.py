@@ -602,3 +602,29 @@ def test_edge_case_parity(d, p, q, n_el, tile_el, pm):
     import scipy.sparse as sp
     Kref = sp.csr_matrix((ref_vals, pt.col_idx(), pt.row_ptr), shape=(s.n_dof, s.n_dof))
     assert rel(y.cpu().numpy(), Kref @ u) < max(TOL_K, kappa)
+
+
+@pytest.mark.parametrize("c,kw", [(2, {}), (3, dict(n_el=(4, 2, 2)))])
+def test_sensitivity_bitwise_deterministic(c, kw):
+    """g is bitwise reproducible run to run (no atomics anywhere; the split-K partials of
+    small problems are summed in segment order), and the one-call step gives the same bits."""
+    from paper_2107_09568_b200 import Assembler
+    from synth import make_config, draw_uv_seeded
+    prob = make_config(c, **kw)
+    A = Assembler(prob)
+    s = A.sizes
+    d = prob.d
+    dev = torch.device("cuda")
+    ctrl = torch.tensor(prob.macro.ctrl, device=dev)
+    young = torch.tensor(prob.young, device=dev)
+    u, v = (torch.tensor(x, device=dev) for x in draw_uv_seeded(c + 90, s.n_dof))
+    gs = []
+    for _ in range(3):
+        g = torch.empty(s.n_macro_cp * d, dtype=torch.float64, device=dev)
+        A.sensitivity(ctrl, young, prob.nu, u, v, g)
+        gs.append(g)
+    vals = torch.empty(s.nnz, dtype=torch.float64, device=dev)
+    g2 = torch.empty_like(gs[0])
+    A.assemble_sensitivity(ctrl, young, prob.nu, u, v, vals, g2)
+    torch.cuda.synchronize()
+    assert torch.equal(gs[0], gs[1]) and torch.equal(gs[0], gs[2]) and torch.equal(gs[0], g2)
