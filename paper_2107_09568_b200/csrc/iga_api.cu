@@ -131,6 +131,27 @@ struct Prof {
   }
 };
 
+// X̃ and W: the fused K5g (X̃ built in shared memory, profiling slot 3) when its staging fits,
+// else K5x (slot 7) + K5a (slot 3)
+static cudaError_t sens_xw(Handle &h, Prof &pf, const double *du, const double *dv, cudaStream_t s) {
+#ifndef IGA_EXPERIMENT_NO_K5G
+  if (sens_xw_fits(h)) {
+    const int id = pf.begin(3);
+    const cudaError_t e = launch_sens_XW(h, du, dv, h.d_W, s);
+    pf.end(id);
+    return e;
+  }
+#endif
+  int id = pf.begin(7);
+  cudaError_t e = launch_sens_X(h, du, dv, s);
+  pf.end(id);
+  if (e) return e;
+  id = pf.begin(3);
+  e = launch_sens_W(h, h.d_W, s);
+  pf.end(id);
+  return e;
+}
+
 static iga_status check_flag(Handle &h, cudaStream_t s) {
   int f[3];
   CU(cudaMemcpyAsync(f, h.d_flag, sizeof(f), cudaMemcpyDeviceToHost, s));
@@ -558,12 +579,8 @@ iga_status iga_sensitivity(const iga_handle *Hc, const double *macro_ctrl, const
     return IGA_ENOMEM;
   }
   pf.end(idst);
-  int id = pf.begin(7);
-  CU(launch_sens_X(h, du, dv, s));
-  pf.end(id);
-  id = pf.begin(3);
-  CU(launch_sens_W(h, h.d_W, s));
-  pf.end(id);
+  int id = 0;
+  CU(sens_xw(h, pf, du, dv, s));
   id = pf.begin(4);
   CU(launch_sens_reverse(h, dctrl, dyoung, young_per_tile, nu, h.d_W, h.d_gpart, s));
   pf.end(id);
@@ -620,12 +637,7 @@ iga_status iga_assemble_sensitivity(const iga_handle *Hc, const double *macro_ct
   CU(launch_scatter_multi(h, dvals, s));
   pf.end(id);
   CU(cudaStreamWaitEvent(s, h.ev_join, 0));
-  id = pf.begin(7);
-  CU(launch_sens_X(h, du, dv, s));
-  pf.end(id);
-  id = pf.begin(3);
-  CU(launch_sens_W(h, h.d_W, s));
-  pf.end(id);
+  CU(sens_xw(h, pf, du, dv, s));
   id = pf.begin(4);
   CU(launch_sens_reverse(h, dctrl, dyoung, young_per_tile, nu, h.d_W, h.d_gpart, s));
   pf.end(id);

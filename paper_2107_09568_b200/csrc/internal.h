@@ -219,6 +219,9 @@ cudaError_t launch_apply(const Handle &h, const double *u, double *y, cudaStream
 cudaError_t launch_expand_pattern(const Handle &h, cudaStream_t s);
 cudaError_t launch_sens_X(const Handle &h, const double *u, const double *v, cudaStream_t s);
 cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s);
+// K5x fused into K5a (cudaErrorNotSupported: staging does not fit, run K5x + K5a)
+cudaError_t launch_sens_XW(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s);
+bool sens_xw_fits(const Handle &h);
 size_t k5x_smem_bytes(int d, int max_patch_ctrl);
 cudaError_t launch_sens_reverse(const Handle &h, const double *ctrl, const double *young, int young_per_tile,
                                 double nu, const double *W, double *gpart, cudaStream_t s);

@@ -127,7 +127,6 @@ __device__ __forceinline__ void store_row(double *p, double x0, double x1, doubl
 constexpr int K3_STAGES = IGA_K3_STAGES;
 constexpr int K3_A_CHUNK = K3_BM * BK, K3_B_CHUNK = BN * BK;          // doubles
 constexpr int K3_CROW = BN + 1;                                        // epilogue pitch (odd)
-constexpr int K3_THREADS = 32 * K3_WARPS;
 constexpr size_t K3_STAGE_BYTES = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
 constexpr size_t K3_EPI_BYTES = sizeof(double) * (size_t)K3_BM * (K3_CROW + 4 * 3);   // staging + apply runs
 constexpr size_t K3_OFF_BAR = K3_STAGE_BYTES > K3_EPI_BYTES ? K3_STAGE_BYTES : K3_EPI_BYTES;
@@ -675,6 +674,247 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
   }
 }
 
+// ---------------------------------------------------------------------------------
+// K5g: K5x fused into K5a.  Besides the 16 MMA warps, 4 generator warps build every B
+// chunk (X̃, K5x's arithmetic and thread mapping) in shared memory from u, v staged per tile
+// patch, so X̃ never goes to HBM.  Per stage: fullA (the TMA'd table chunk), fullB (the 128
+// generator threads), emptyB (the last MMA warp to release a stage lets the generators
+// refill it).  Every MMA warp keeps only the accumulators of its κ-group parts (registers:
+// the 640-thread CTA must fit 65,536).
+constexpr int K5G_GEN_WARPS = 4;
+constexpr int K5G_THREADS = 32 * (N_MMA_WARPS + K5G_GEN_WARPS);
+
+struct K5gArgs {
+  const double *tabAT;
+  const int32_t *k5_pair, *pinfo, *node_map;
+  int nl, n_patches;
+  const double *u, *v;
+  int64_t n_tiles;
+  int nkc;          // chunks of the whole reduction (Kp / 16)
+  int64_t N;        // Y rows (N-blocks × 72)
+  double *Wout;
+  int ldw;
+  const uint8_t *k5_mode;
+  int ts;           // per-tile stride of the u/v staging (max_patch_ctrl·D + 1)
+};
+
+template <int S>
+struct K5gSmem {
+  static constexpr size_t STAGES = sizeof(double) * (size_t)S * (K5_A_CHUNK + K5_B_CHUNK);
+  static size_t bytes(int d, int ts) {
+    return STAGES + sizeof(double) * 2 * (size_t)(d == 3 ? 8 : 16) * ts + S * (3 * sizeof(uint64_t) + sizeof(int));
+  }
+};
+
+template <int LO0, int HI0, int LO1, int HI1>
+struct K5gAcc {
+  static constexpr int N0 = HI0 - LO0, N1 = HI1 - LO1;
+  double a0[N0 > 0 ? N0 : 1][2], a1[N1 > 0 ? N1 : 1][2];
+};
+
+template <int D, int S, int LO0, int HI0, int LO1, int HI1>
+__device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int kc_lo, int nkc, int warp, int lane,
+                                             const double *gA) {
+  constexpr int N0 = HI0 - LO0, N1 = HI1 - LO1;
+  double *sA = smem, *sB = smem + S * K5_A_CHUNK;
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5gSmem<S>::STAGES +
+                                                 sizeof(double) * 2 * (D == 3 ? 8 : 16) * g.ts);
+  uint64_t *fullB = fullA + S, *emptyB = fullB + S;
+  int *released = reinterpret_cast<int *>(emptyB + S);
+  K5gAcc<LO0, HI0, LO1, HI1> acc;
+#pragma unroll
+  for (int i = 0; i < (N0 > 0 ? N0 : 1); ++i) acc.a0[i][0] = acc.a0[i][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < (N1 > 0 ? N1 : 1); ++i) acc.a1[i][0] = acc.a1[i][1] = 0.0;
+  const int g0 = warp * 2;
+  for (int kc = 0; kc < nkc; ++kc) {
+    const int st = kc % S;
+    const uint32_t par = (kc / S) & 1;
+    mbar_wait(&fullA[st], par);
+    mbar_wait(&fullB[st], par);
+    const double *a_st = sA + st * K5_A_CHUNK, *b_st = sB + st * K5_B_CHUNK;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      double a0 = 0.0, a1 = 0.0, b[NI];
+      if (N0 > 0) a0 = a_st[(g0 * 4 + kk) * 32 + lane];
+      if (N1 > 0) a1 = a_st[((g0 + 1) * 4 + kk) * 32 + lane];
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni)
+        if ((ni >= LO0 && ni < HI0) || (ni >= LO1 && ni < HI1)) b[ni] = b_st[(ni * 4 + kk) * 32 + lane];
+#pragma unroll
+      for (int ni = LO0; ni < HI0; ++ni) dmma884(acc.a0[ni - LO0][0], acc.a0[ni - LO0][1], a0, b[ni]);
+#pragma unroll
+      for (int ni = LO1; ni < HI1; ++ni) dmma884(acc.a1[ni - LO1][0], acc.a1[ni - LO1][1], a1, b[ni]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&released[st], 1) == N_MMA_WARPS - 1) {
+        released[st] = 0;
+        __threadfence_block();
+        if (kc + S < nkc) {   // refill: the table chunk by TMA, the X̃ chunk by the generators
+          mbar_expect_tx(&fullA[st], K5_A_CHUNK * 8);
+          bulk_g2s(sA + st * K5_A_CHUNK, gA + (int64_t)(kc + S) * K5_A_CHUNK, K5_A_CHUNK * 8, &fullA[st]);
+          mbar_arrive(&emptyB[st]);
+        }
+      }
+    }
+  }
+  named_bar(1, K5G_THREADS);   // all stages consumed (generators included): stage Y in smem
+  double *sW = smem;
+  const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int ni = LO0; ni < HI0; ++ni) {
+    const int kap = warp * 16 + fr, n = ni * 8 + 2 * fc;
+    sW[n * K5_WP + kap] = acc.a0[ni - LO0][0];
+    sW[(n + 1) * K5_WP + kap] = acc.a0[ni - LO0][1];
+  }
+#pragma unroll
+  for (int ni = LO1; ni < HI1; ++ni) {
+    const int kap = warp * 16 + 8 + fr, n = ni * 8 + 2 * fc;
+    sW[n * K5_WP + kap] = acc.a1[ni - LO1][0];
+    sW[(n + 1) * K5_WP + kap] = acc.a1[ni - LO1][1];
+  }
+}
+
+template <int D, int S>
+__device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int kc_lo, int nkc, int64_t nb, int gtid) {
+  constexpr int TPC = D == 3 ? 8 : 16, NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2, NTL = D == 3 ? 1 : 2;
+  double *sB = smem + S * K5_A_CHUNK;
+  double *us = smem + K5gSmem<S>::STAGES / sizeof(double), *vs = us + TPC * g.ts;
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(vs + TPC * g.ts);
+  uint64_t *fullB = fullA + S, *emptyB = fullB + S;
+  const int lane = gtid & 31, k = 4 * (gtid >> 5) + (lane & 3);
+  const int64_t t0 = nb * TPC;
+  int toff[NTL];
+#pragma unroll
+  for (int it = 0; it < NTL; ++it) toff[it] = (it * 8 + (lane >> 2)) * g.ts;
+  int p = -1, kc_next_patch = 0;
+  // the pair index of chunk kc + 2 is loaded two chunks ahead (its latency stays off the
+  // generator's critical path)
+  int32_t pr0 = nkc > 0 ? g.k5_pair[(int64_t)kc_lo * BK + k] : -1;
+  int32_t pr1 = nkc > 1 ? g.k5_pair[(int64_t)(kc_lo + 1) * BK + k] : -1;
+  for (int kc = 0; kc < nkc; ++kc) {
+    const int gkc = kc_lo + kc;
+    const int32_t pr = pr0;
+    pr0 = pr1;
+    pr1 = kc + 2 < nkc ? g.k5_pair[(int64_t)(gkc + 2) * BK + k] : -1;
+    if (gkc >= kc_next_patch) {   // entering the next tile patch: restage u, v of its control points
+      while (p + 1 < g.n_patches && g.pinfo[3 * (p + 1)] <= gkc) ++p;
+      kc_next_patch = g.pinfo[3 * (p + 1)];
+      const int off = g.pinfo[3 * p + 1], nc = g.pinfo[3 * p + 2];
+      named_bar(2, 32 * K5G_GEN_WARPS);   // nobody still reads the previous patch's u, v
+      for (int i = gtid; i < TPC * nc; i += 32 * K5G_GEN_WARPS) {
+        const int tl = i / nc, A = i % nc;
+        const int64_t t = t0 + tl;
+        double *uo = us + tl * g.ts + A * D, *vo = vs + tl * g.ts + A * D;
+        if (t < g.n_tiles) {
+          const int64_t I = g.node_map[t * g.nl + off + A];
+#pragma unroll
+          for (int a = 0; a < D; ++a) { uo[a] = g.u[I * D + a]; vo[a] = g.v[I * D + a]; }
+        } else {
+#pragma unroll
+          for (int a = 0; a < D; ++a) { uo[a] = 0.0; vo[a] = 0.0; }
+        }
+      }
+      named_bar(2, 32 * K5G_GEN_WARPS);
+    }
+    const int st = kc % S;
+    if (kc >= S) mbar_wait(&emptyB[st], ((kc / S) - 1) & 1);
+    double x[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) x[j] = 0.0;
+    if (pr >= 0) {
+      const int A = (pr & 0xffff) * D, B = (pr >> 16) * D;
+      double uA[NTL][D], vA[NTL][D], uB[NTL][D], vB[NTL][D];
+#pragma unroll
+      for (int it = 0; it < NTL; ++it)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          uA[it][c] = us[toff[it] + A + c];
+          vA[it][c] = vs[toff[it] + A + c];
+          uB[it][c] = us[toff[it] + B + c];
+          vB[it][c] = vs[toff[it] + B + c];
+        }
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int o = D == 3 ? j : j >> 1, it = D == 3 ? 0 : (j & 1);
+        if (o >= NP1 + NP2) continue;
+        int a = 0, b = 0;
+        if (o < NP1) sym_pair(D, o, a, b);
+        else anti_pair(D, o - NP1, a, b);
+        const double xab = fma(uB[it][b], vA[it][a], uA[it][a] * vB[it][b]);
+        if (o < D) x[j] = A == B ? 0.5 * xab : xab;
+        else if (A == B) x[j] = xab;
+        else {
+          const double xba = fma(uB[it][a], vA[it][b], uA[it][b] * vB[it][a]);
+          x[j] = o < NP1 ? xab + xba : xab - xba;
+        }
+      }
+    }
+    double *dst = sB + st * K5_B_CHUNK + gtid;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) dst[128 * j] = x[j];
+    mbar_arrive(&fullB[st]);
+  }
+  named_bar(1, K5G_THREADS);
+}
+
+template <int D, int S, bool SPLIT>
+__global__ void __launch_bounds__(K5G_THREADS, 1)
+k5g_wgemm(const __grid_constant__ K5gArgs g) {
+  constexpr int NE = D == 3 ? 9 : 8;
+  extern __shared__ __align__(128) double smem[];
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5gSmem<S>::STAGES +
+                                                 sizeof(double) * 2 * (D == 3 ? 8 : 16) * g.ts);
+  uint64_t *fullB = fullA + S, *emptyB = fullB + S;
+  int *released = reinterpret_cast<int *>(emptyB + S);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t kb = blockIdx.x, nb = blockIdx.y;
+  int nkc = g.nkc, kc_lo = 0;
+  double *Wout = g.Wout;
+  if (SPLIT) {
+    kc_lo = (int)((int64_t)blockIdx.z * g.nkc / gridDim.z);
+    nkc = (int)((int64_t)(blockIdx.z + 1) * g.nkc / gridDim.z) - kc_lo;
+    Wout += (int64_t)blockIdx.z * g.N * g.ldw;
+  }
+  const double *gA = g.tabAT + (kb * (int64_t)g.nkc + kc_lo) * K5_A_CHUNK;
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&fullA[st], 1);
+      mbar_init(&fullB[st], 32 * K5G_GEN_WARPS);
+      mbar_init(&emptyB[st], 1);
+      released[st] = 0;
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int st = 0; st < S && st < nkc; ++st) {
+      mbar_expect_tx(&fullA[st], K5_A_CHUNK * 8);
+      bulk_g2s(smem + st * K5_A_CHUNK, gA + (int64_t)st * K5_A_CHUNK, K5_A_CHUNK * 8, &fullA[st]);
+    }
+  if (warp >= N_MMA_WARPS) {
+    k5g_gen_role<D, S>(g, smem, kc_lo, nkc, nb, tid - 32 * N_MMA_WARPS);
+  } else {
+    switch (g.k5_mode[kb * N_MMA_WARPS + warp]) {   // parts of the warp's two κ groups
+      case 4: k5g_mma_role<D, S, 0, 6, 0, 6>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 8: k5g_mma_role<D, S, 6, NE, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 5: k5g_mma_role<D, S, 0, 6, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 3: k5g_mma_role<D, S, 0, 6, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 6: k5g_mma_role<D, S, 6, NE, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      default: k5g_mma_role<D, S, 0, 0, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+    }
+  }
+  __syncthreads();
+  const double *sW = smem;
+  for (int i = tid; i < BN * BM; i += K5G_THREADS) {
+    const int n = i / BM, kap = i % BM;
+    const int64_t gn = nb * BN + n, gk = kb * BM + kap;
+    if (gn < g.N && gk < g.ldw) Wout[gn * g.ldw + gk] = sW[n * K5_WP + kap];
+  }
+}
+
 size_t k5x_smem_bytes(int d, int max_patch_ctrl) {
   return sizeof(double) * (size_t)2 * (d == 3 ? 8 : 16) * (max_patch_ctrl * d + 1);
 }
@@ -728,6 +968,52 @@ static cudaError_t launch_k5a(const Handle &h, double *W, cudaStream_t s) {
     k5a_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.d_Wpart, nseg, n, W);
   }
   return cudaGetLastError();
+}
+
+template <int D, int S>
+static cudaError_t launch_k5g_s(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s) {
+  const int ts = h.max_patch_ctrl * D + 1;
+  const size_t smem = K5gSmem<S>::bytes(D, ts);
+  const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc;
+  const int nseg = h.k5_nseg;
+  K5gArgs g{h.d_tabAT, h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, h.n_patches, u, v, h.n_tiles_own,
+            (int)(h.Kp / BK), nblk * BN, nseg > 1 ? h.d_Wpart : W, (int)h.k5_rows, h.d_k5_mode, ts};
+  dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)nblk, (unsigned)nseg);
+  if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+  cudaError_t e;
+  if (nseg > 1) {
+    if ((e = cudaFuncSetAttribute(k5g_wgemm<D, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    k5g_wgemm<D, S, true><<<grid, K5G_THREADS, smem, s>>>(g);
+  } else {
+    if ((e = cudaFuncSetAttribute(k5g_wgemm<D, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    k5g_wgemm<D, S, false><<<grid, K5G_THREADS, smem, s>>>(g);
+  }
+  if ((e = cudaGetLastError())) return e;
+  if (nseg > 1) {
+    const int64_t n = nblk * BN * h.k5_rows;
+    k5a_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.d_Wpart, nseg, n, W);
+  }
+  return cudaGetLastError();
+}
+
+// K5x fused into K5a (X̃ generated in shared memory); cudaErrorNotSupported when the
+// per-patch u, v staging does not fit beside a 3-stage ring (the caller then runs K5x + K5a)
+bool sens_xw_fits(const Handle &h) {
+  const int ts = h.max_patch_ctrl * h.d + 1;
+  return (h.d == 3 ? K5gSmem<3>::bytes(3, ts) : K5gSmem<3>::bytes(2, ts)) <= 227 * 1024;
+}
+
+cudaError_t launch_sens_XW(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s) {
+  const int ts = h.max_patch_ctrl * h.d + 1;
+  const size_t lim = 227 * 1024;
+  if (h.d == 3) {
+    if (K5gSmem<4>::bytes(3, ts) <= lim) return launch_k5g_s<3, 4>(h, u, v, W, s);
+    if (K5gSmem<3>::bytes(3, ts) <= lim) return launch_k5g_s<3, 3>(h, u, v, W, s);
+  } else {
+    if (K5gSmem<4>::bytes(2, ts) <= lim) return launch_k5g_s<2, 4>(h, u, v, W, s);
+    if (K5gSmem<3>::bytes(2, ts) <= lim) return launch_k5g_s<2, 3>(h, u, v, W, s);
+  }
+  return cudaErrorNotSupported;
 }
 
 cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s) {
