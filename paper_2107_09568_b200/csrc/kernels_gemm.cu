@@ -855,7 +855,8 @@ __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int
     double *dst = sB + st * K5_B_CHUNK + gtid;
 #pragma unroll
     for (int j = 0; j < NI; ++j) dst[128 * j] = x[j];
-    mbar_arrive(&fullB[st]);
+    __syncwarp();   // the warp's stores happen before its elected arrival (release)
+    if (lane == 0) mbar_arrive(&fullB[st]);
   }
   named_bar(1, K5G_THREADS);
 }
@@ -882,7 +883,7 @@ k5g_wgemm(const __grid_constant__ K5gArgs g) {
   if (tid == 0) {
     for (int st = 0; st < S; ++st) {
       mbar_init(&fullA[st], 1);
-      mbar_init(&fullB[st], 32 * K5G_GEN_WARPS);
+      mbar_init(&fullB[st], K5G_GEN_WARPS);
       mbar_init(&emptyB[st], 1);
       released[st] = 0;
     }
