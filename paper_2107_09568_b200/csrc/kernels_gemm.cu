@@ -799,7 +799,11 @@ __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int
     const int32_t pr = pr0;
     pr0 = pr1;
     pr1 = kc + 2 < nkc ? g.k5_pair[(int64_t)(gkc + 2) * BK + k] : -1;
+#ifdef IGA_EXPERIMENT_K5G_STAGE_ONCE
+    if (gkc >= kc_next_patch && p < 0) {   // timing experiment only: stage the first patch once
+#else
     if (gkc >= kc_next_patch) {   // entering the next tile patch: restage u, v of its control points
+#endif
       while (p + 1 < g.n_patches && g.pinfo[3 * (p + 1)] <= gkc) ++p;
       kc_next_patch = g.pinfo[3 * (p + 1)];
       const int off = g.pinfo[3 * p + 1], nc = g.pinfo[3 * p + 2];
