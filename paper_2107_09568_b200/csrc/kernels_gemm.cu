@@ -681,7 +681,11 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
 // generator threads), emptyB (the last MMA warp to release a stage lets the generators
 // refill it).  Every MMA warp keeps only the accumulators of its κ-group parts (registers:
 // the 640-thread CTA must fit 65,536).
-constexpr int K5G_GEN_WARPS = 4;
+#ifndef IGA_K5G_GEN_WARPS
+#define IGA_K5G_GEN_WARPS 8   // two groups of 4 warps, alternate chunks
+#endif
+constexpr int K5G_GEN_WARPS = IGA_K5G_GEN_WARPS;
+static_assert(K5G_GEN_WARPS % 4 == 0, "generator groups of 4 warps (128 threads per chunk)");
 constexpr int K5G_THREADS = 32 * (N_MMA_WARPS + K5G_GEN_WARPS);
 
 struct K5gArgs {
@@ -780,35 +784,33 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
 template <int D, int S>
 __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int kc_lo, int nkc, int64_t nb, int gtid) {
   constexpr int TPC = D == 3 ? 8 : 16, NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2, NTL = D == 3 ? 1 : 2;
+  constexpr int NG = K5G_GEN_WARPS / 4;          // groups of 4 warps: one chunk per group at a time
+  constexpr int NGT = 32 * K5G_GEN_WARPS;
   double *sB = smem + S * K5_A_CHUNK;
   double *us = smem + K5gSmem<S>::STAGES / sizeof(double), *vs = us + TPC * g.ts;
   uint64_t *fullA = reinterpret_cast<uint64_t *>(vs + TPC * g.ts);
   uint64_t *fullB = fullA + S, *emptyB = fullB + S;
-  const int lane = gtid & 31, k = 4 * (gtid >> 5) + (lane & 3);
+  const int grp = gtid >> 7, gt = gtid & 127;
+  const int lane = gt & 31, k = 4 * (gt >> 5) + (lane & 3);
   const int64_t t0 = nb * TPC;
+  const int kc_hi = kc_lo + nkc;
   int toff[NTL];
 #pragma unroll
   for (int it = 0; it < NTL; ++it) toff[it] = (it * 8 + (lane >> 2)) * g.ts;
-  int p = -1, kc_next_patch = 0;
-  // the pair index of chunk kc + 2 is loaded two chunks ahead (its latency stays off the
-  // generator's critical path)
-  int32_t pr0 = nkc > 0 ? g.k5_pair[(int64_t)kc_lo * BK + k] : -1;
-  int32_t pr1 = nkc > 1 ? g.k5_pair[(int64_t)(kc_lo + 1) * BK + k] : -1;
-  for (int kc = 0; kc < nkc; ++kc) {
-    const int gkc = kc_lo + kc;
-    const int32_t pr = pr0;
-    pr0 = pr1;
-    pr1 = kc + 2 < nkc ? g.k5_pair[(int64_t)(gkc + 2) * BK + k] : -1;
+  // the tile patches overlapping this CTA's chunk range, in order; all groups walk the same
+  // sequence (so the per-patch barriers match), group grp takes chunks c0 + grp, c0 + grp + NG, ...
+  int p = 0;
+  while (p + 1 < g.n_patches && g.pinfo[3 * (p + 1)] <= kc_lo) ++p;
+  for (; p < g.n_patches && g.pinfo[3 * p] < kc_hi; ++p) {
+    const int c0 = max(g.pinfo[3 * p], kc_lo), c1 = min(g.pinfo[3 * (p + 1)], kc_hi);
+    const int off = g.pinfo[3 * p + 1], nc = g.pinfo[3 * p + 2];
 #ifdef IGA_EXPERIMENT_K5G_STAGE_ONCE
-    if (gkc >= kc_next_patch && p < 0) {   // timing experiment only: stage the first patch once
+    if (c0 == kc_lo) {   // timing experiment only: stage the first patch once
 #else
-    if (gkc >= kc_next_patch) {   // entering the next tile patch: restage u, v of its control points
+    {   // restage u, v of the patch's control points for the CTA's tiles
 #endif
-      while (p + 1 < g.n_patches && g.pinfo[3 * (p + 1)] <= gkc) ++p;
-      kc_next_patch = g.pinfo[3 * (p + 1)];
-      const int off = g.pinfo[3 * p + 1], nc = g.pinfo[3 * p + 2];
-      named_bar(2, 32 * K5G_GEN_WARPS);   // nobody still reads the previous patch's u, v
-      for (int i = gtid; i < TPC * nc; i += 32 * K5G_GEN_WARPS) {
+      named_bar(2, NGT);   // every group is done with the previous patch's u, v
+      for (int i = gtid; i < TPC * nc; i += NGT) {
         const int tl = i / nc, A = i % nc;
         const int64_t t = t0 + tl;
         double *uo = us + tl * g.ts + A * D, *vo = vs + tl * g.ts + A * D;
@@ -821,46 +823,52 @@ __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int
           for (int a = 0; a < D; ++a) { uo[a] = 0.0; vo[a] = 0.0; }
         }
       }
-      named_bar(2, 32 * K5G_GEN_WARPS);
+      named_bar(2, NGT);
     }
-    const int st = kc % S;
-    if (kc >= S) mbar_wait(&emptyB[st], ((kc / S) - 1) & 1);
-    double x[NI];
+    // the pair index of the group's next chunk is loaded one chunk ahead
+    int32_t prn = c0 + grp < c1 ? g.k5_pair[(int64_t)(c0 + grp) * BK + k] : -1;
+    for (int gkc = c0 + grp; gkc < c1; gkc += NG) {
+      const int32_t pr = prn;
+      prn = gkc + NG < c1 ? g.k5_pair[(int64_t)(gkc + NG) * BK + k] : -1;
+      const int kc = gkc - kc_lo, st = kc % S;
+      if (kc >= S) mbar_wait(&emptyB[st], ((kc / S) - 1) & 1);
+      double x[NI];
 #pragma unroll
-    for (int j = 0; j < NI; ++j) x[j] = 0.0;
-    if (pr >= 0) {
-      const int A = (pr & 0xffff) * D, B = (pr >> 16) * D;
-      double uA[NTL][D], vA[NTL][D], uB[NTL][D], vB[NTL][D];
+      for (int j = 0; j < NI; ++j) x[j] = 0.0;
+      if (pr >= 0) {
+        const int A = (pr & 0xffff) * D, B = (pr >> 16) * D;
+        double uA[NTL][D], vA[NTL][D], uB[NTL][D], vB[NTL][D];
 #pragma unroll
-      for (int it = 0; it < NTL; ++it)
+        for (int it = 0; it < NTL; ++it)
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-          uA[it][c] = us[toff[it] + A + c];
-          vA[it][c] = vs[toff[it] + A + c];
-          uB[it][c] = us[toff[it] + B + c];
-          vB[it][c] = vs[toff[it] + B + c];
-        }
+          for (int c = 0; c < D; ++c) {
+            uA[it][c] = us[toff[it] + A + c];
+            vA[it][c] = vs[toff[it] + A + c];
+            uB[it][c] = us[toff[it] + B + c];
+            vB[it][c] = vs[toff[it] + B + c];
+          }
 #pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        const int o = D == 3 ? j : j >> 1, it = D == 3 ? 0 : (j & 1);
-        if (o >= NP1 + NP2) continue;
-        int a = 0, b = 0;
-        if (o < NP1) sym_pair(D, o, a, b);
-        else anti_pair(D, o - NP1, a, b);
-        const double xab = fma(uB[it][b], vA[it][a], uA[it][a] * vB[it][b]);
-        if (o < D) x[j] = A == B ? 0.5 * xab : xab;
-        else if (A == B) x[j] = xab;
-        else {
-          const double xba = fma(uB[it][a], vA[it][b], uA[it][b] * vB[it][a]);
-          x[j] = o < NP1 ? xab + xba : xab - xba;
+        for (int j = 0; j < NI; ++j) {
+          const int o = D == 3 ? j : j >> 1, it = D == 3 ? 0 : (j & 1);
+          if (o >= NP1 + NP2) continue;
+          int a = 0, b = 0;
+          if (o < NP1) sym_pair(D, o, a, b);
+          else anti_pair(D, o - NP1, a, b);
+          const double xab = fma(uB[it][b], vA[it][a], uA[it][a] * vB[it][b]);
+          if (o < D) x[j] = A == B ? 0.5 * xab : xab;
+          else if (A == B) x[j] = xab;
+          else {
+            const double xba = fma(uB[it][a], vA[it][b], uA[it][b] * vB[it][a]);
+            x[j] = o < NP1 ? xab + xba : xab - xba;
+          }
         }
       }
-    }
-    double *dst = sB + st * K5_B_CHUNK + gtid;
+      double *dst = sB + st * K5_B_CHUNK + gt;
 #pragma unroll
-    for (int j = 0; j < NI; ++j) dst[128 * j] = x[j];
-    __syncwarp();   // the warp's stores happen before its elected arrival (release)
-    if (lane == 0) mbar_arrive(&fullB[st]);
+      for (int j = 0; j < NI; ++j) dst[128 * j] = x[j];
+      __syncwarp();   // the warp's stores happen before its elected arrival (release)
+      if (lane == 0) mbar_arrive(&fullB[st]);
+    }
   }
   named_bar(1, K5G_THREADS);
 }
@@ -887,7 +895,7 @@ k5g_wgemm(const __grid_constant__ K5gArgs g) {
   if (tid == 0) {
     for (int st = 0; st < S; ++st) {
       mbar_init(&fullA[st], 1);
-      mbar_init(&fullB[st], K5G_GEN_WARPS);
+      mbar_init(&fullB[st], 4);   // the 4 warps of the group generating the chunk
       mbar_init(&emptyB[st], 1);
       released[st] = 0;
     }
