@@ -13,7 +13,7 @@ Handle::~Handle() {
   void *bufs[] = {d_table, d_tabA, d_tabAT, d_coef, d_side, d_W, d_X, d_gpart, d_node_map, d_pairA, d_pairB,
                   d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_mperm, d_slot_tr,
                   d_k5_pair, d_k5_col, d_tperm, d_g1len, d_g2len, d_g1slot, d_g2slot, d_sA_ptr, d_sA_slot,
-                  d_inv_ptr, d_inv_ent, d_part, d_k5_gphys, d_k5_mode, d_Wpart, d_F, d_th, d_det, d_Vt, d_mweights, d_patch_info, d_mknots, d_mspan, d_flag};
+                  d_inv_ptr, d_inv_ent, d_part, d_ug, d_k5_gphys, d_k5_mode, d_Wpart, d_F, d_th, d_det, d_Vt, d_mweights, d_patch_info, d_mknots, d_mspan, d_flag};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (int i = 0; i < N_STAGE; ++i)
@@ -447,9 +447,10 @@ iga_status iga_apply(const iga_handle *Hc, const double *macro_ctrl, const doubl
   cudaStream_t s = (cudaStream_t)stream;
   if (!h.d_part) {   // partial slots: allocated on first use (assemble-only users never pay it)
     const size_t bytes = std::max<size_t>(8, sizeof(double) * (size_t)h.n_tiles * h.P * h.d);
-    if (cudaMalloc((void **)&h.d_part, bytes) != cudaSuccess) {
+    const size_t ubytes = std::max<size_t>(8, sizeof(double) * (size_t)h.n_tiles * h.n_local_ctrl * h.d);
+    if (cudaMalloc((void **)&h.d_part, bytes) != cudaSuccess || cudaMalloc((void **)&h.d_ug, ubytes) != cudaSuccess) {
       cudaGetLastError();
-      set_error("cudaMalloc of %zu bytes of apply partials failed", bytes);
+      set_error("cudaMalloc of %zu + %zu bytes of apply buffers failed", bytes, ubytes);
       return IGA_ENOMEM;
     }
   }

@@ -167,6 +167,7 @@ struct Handle {
   int32_t *d_g1slot = nullptr, *d_g2slot = nullptr, *d_sA_ptr = nullptr, *d_sA_slot = nullptr, *d_inv_ent = nullptr;
   int64_t *d_inv_ptr = nullptr;
   double *d_part = nullptr;      // [n_tiles][P][d] apply partials (allocated by the first iga_apply)
+  double *d_ug = nullptr;        // [n_tiles][n_local_ctrl][d] u gathered per tile (iga_apply)
   // volume / load (NEXT N3)
   double *d_F = nullptr;         // [n_local_ctrl][npi] load table 𝔉 (Eq. 53)
   double *d_th = nullptr;        // [npi] volume table t^h (Eq. 18)

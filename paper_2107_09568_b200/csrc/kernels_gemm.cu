@@ -128,7 +128,7 @@ constexpr int K3_STAGES = IGA_K3_STAGES;
 constexpr int K3_A_CHUNK = K3_BM * BK, K3_B_CHUNK = BN * BK;          // doubles
 constexpr int K3_CROW = BN + 1;                                        // epilogue pitch (odd)
 constexpr size_t K3_STAGE_BYTES = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
-constexpr size_t K3_EPI_BYTES = sizeof(double) * (size_t)K3_BM * (K3_CROW + 4 * 3);   // staging + apply runs
+constexpr size_t K3_EPI_BYTES = sizeof(double) * (size_t)K3_BM * (K3_CROW + 8 * 3);   // staging + apply runs (2 tiles)
 constexpr size_t K3_OFF_BAR = K3_STAGE_BYTES > K3_EPI_BYTES ? K3_STAGE_BYTES : K3_EPI_BYTES;
 constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int));
 #ifndef IGA_K3_MI
@@ -275,7 +275,9 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     // thread e: c1 = L u_J (diagonal: L_sym u_I) of row e into s1, and c2 = Lᵀ u_I of row
     // tperm[e] into s2 (position e of the (B, A) order); the first thread of each run of
     // equal A (s1) / equal B (s2) sums its run in order into the run's partial slot.
-    double *s1 = sC + K3_BM * K3_CROW, *s2 = s1 + 2 * K3_BM * D;
+    // two tiles per barrier round (KR): s1/s2 hold [round tile][half][row][D]
+    constexpr int KR = TPT % 2 == 0 ? 2 : 1;
+    double *s1 = sC + K3_BM * K3_CROW, *s2 = s1 + KR * 2 * K3_BM * D;
     const int half = tid / K3_BM;
     const int et = tperm[m0 + er];
     const int64_t rt = m0 + et;
@@ -284,40 +286,45 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
     const int len1 = ap.g1len[m0 + er], len2 = ap.g2len[m0 + er];
     const int64_t sl1 = ap.g1slot[m0 + er], sl2 = ap.g2slot[m0 + er];
-    double *my1 = s1 + (half * K3_BM + er) * D, *my2 = s2 + (half * K3_BM + er) * D;
-    for (int k = 0; k < TPT; ++k) {
-      const int tl = et0 + k;
-      const int64_t t = t0 + tl;
-      const bool tv = t < n_tiles;
-      double c1[D], c2[D];
+    for (int k0 = 0; k0 < TPT; k0 += KR) {
 #pragma unroll
-      for (int a = 0; a < D; ++a) c1[a] = c2[a] = 0.0;
-      if (tv && live) {
-        const double *L = sC + er * K3_CROW;
-        const int64_t I = ap.node_map[t * nl + A], J = ap.node_map[t * nl + B];
-        double uv[D];
+      for (int kk = 0; kk < KR; ++kk) {
+        const int tl = et0 + k0 + kk;
+        const int64_t t = t0 + tl;
+        const bool tv = t < n_tiles;
+        double c1[D], c2[D];
 #pragma unroll
-        for (int b = 0; b < D; ++b) uv[b] = ap.u[(A == B ? I : J) * D + b];
+        for (int a = 0; a < D; ++a) c1[a] = c2[a] = 0.0;
+        if (tv && live) {
+          const double *L = sC + er * K3_CROW;
+          double uv[D];   // u of node(t, B) (diagonal: node(t, A)) from the per-tile gathered copy
 #pragma unroll
-        for (int a = 0; a < D; ++a)
+          for (int b = 0; b < D; ++b) uv[b] = ap.u[(t * nl + B) * D + b];
 #pragma unroll
-          for (int b = 0; b < D; ++b) c1[a] += (A == B && a > b ? L[tl * DD + b * D + a] : L[tl * DD + a * D + b]) * uv[b];
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) c1[a] += (A == B && a > b ? L[tl * DD + b * D + a] : L[tl * DD + a * D + b]) * uv[b];
+        }
+        if (tv && live_t && At != Bt) {
+          const double *L = sC + et * K3_CROW;
+          double uv[D];   // u of node(t, A_t)
+#pragma unroll
+          for (int a = 0; a < D; ++a) uv[a] = ap.u[(t * nl + At) * D + a];
+#pragma unroll
+          for (int b = 0; b < D; ++b)
+#pragma unroll
+            for (int a = 0; a < D; ++a) c2[b] += L[tl * DD + a * D + b] * uv[a];
+        }
+        double *my1 = s1 + ((kk * 2 + half) * K3_BM + er) * D, *my2 = s2 + ((kk * 2 + half) * K3_BM + er) * D;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { my1[a] = c1[a]; my2[a] = c2[a]; }
       }
-      if (tv && live_t && At != Bt) {
-        const double *L = sC + et * K3_CROW;
-        const int64_t I = ap.node_map[t * nl + At];
-        double uv[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) uv[a] = ap.u[I * D + a];
-#pragma unroll
-        for (int b = 0; b < D; ++b)
-#pragma unroll
-          for (int a = 0; a < D; ++a) c2[b] += L[tl * DD + a * D + b] * uv[a];
-      }
-#pragma unroll
-      for (int a = 0; a < D; ++a) { my1[a] = c1[a]; my2[a] = c2[a]; }
       __syncthreads();
-      if (tv) {
+#pragma unroll
+      for (int kk = 0; kk < KR; ++kk) {
+        const int64_t t = t0 + et0 + k0 + kk;
+        if (t >= n_tiles) continue;
+        const double *my1 = s1 + ((kk * 2 + half) * K3_BM + er) * D, *my2 = s2 + ((kk * 2 + half) * K3_BM + er) * D;
         if (len1) {
           double acc[D];
 #pragma unroll
@@ -455,8 +462,24 @@ k4_apply_gather(const double *__restrict__ part, int64_t P, const int32_t *__res
   for (int a = 0; a < D; ++a) y[i * D + a] = acc[a];
 }
 
+// ug[t][A][a] = u[node(t, A)·d + a]: u gathered per tile once, so the apply epilogue reads it
+// without the node-map indirection
+template <int D>
+__global__ void k3_gather_u(const double *__restrict__ u, const int32_t *__restrict__ node_map, int64_t n,
+                            double *__restrict__ ug) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t I = node_map[i];
+#pragma unroll
+  for (int a = 0; a < D; ++a) ug[i * D + a] = u[I * D + a];
+}
+
 cudaError_t launch_apply(const Handle &h, const double *u, double *y, cudaStream_t s) {
-  ApplyArgs ap{u, h.d_part, h.P, h.d_g1len, h.d_g2len, h.d_g1slot, h.d_g2slot, h.d_node_map};
+  const int64_t n = h.n_tiles * h.n_local_ctrl;
+  double *ug = h.d_ug;
+  if (h.d == 2) k3_gather_u<2><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(u, h.d_node_map, n, ug);
+  else k3_gather_u<3><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(u, h.d_node_map, n, ug);
+  ApplyArgs ap{ug, h.d_part, h.P, h.d_g1len, h.d_g2len, h.d_g1slot, h.d_g2slot, h.d_node_map};
   cudaError_t e = h.d == 2 ? launch_k3<2, 2>(h, nullptr, s, ap) : launch_k3<3, 2>(h, nullptr, s, ap);
   if (e) return e;
   const unsigned blocks = (unsigned)((h.n_nodes + 255) / 256);
