@@ -4,7 +4,9 @@
 //   ∇F at the (q+1)^d tensor Gauss nodes of the element-local cube (Eq. 7 frame, R4),
 //   Ā_ij[a,b] = D (λ ǧ_i[a] ǧ_j[b] + μ ǧ_j[a] ǧ_i[b] + μ (ǧ_i·ǧ_j) δ_ab)   (Eq. 37, App. A)
 //   and the coefficients ⟨Ā⟩ = (V1⁻¹)^{⊗d} · samples (sum-factorised, one pass per direction).
-//   HBM-bound: the only large traffic is the coefficient write (n_pi d⁴ doubles per tile).
+//   For K3 it writes the 45 (3D) / 10 (2D) distinct symmetric / antisymmetric halves
+//   ½(⟨Ā_ij[a,b]⟩ ± ⟨Ā_ij[b,a]⟩) of the Eq. 38-reduced contraction; for
+//   iga_interpolate all d⁴ components.  The only large traffic is the coefficient write.
 //
 // K5b (sensitivity, Eqs. 70-72): Ŵ_t = Πᵀ W_t, then at each node the analytic
 //   reverse mode of S = ⟨Ŵ, Ā(J)⟩:
@@ -295,11 +297,12 @@ __device__ __forceinline__ void node_geometry(const InterpConst &c_ip, const Mac
   }
 }
 
-// K2: thread = (tile, Ā component (i,j,a,b)); TPB tiles per CTA.  Phases: macro data
-// per tile -> node geometry (one thread per node) -> each thread evaluates its component
-// of Ā (Eq. 37, closed form) at the (q+1)^d nodes into registers, applies (V1⁻¹)^{⊗d}
-// by D 1D passes in registers (all indices compile-time) and writes its (q+1)^d
-// interpolation coefficients.
+// K2: thread = (tile, component) — a distinct symmetric / antisymmetric half (SYM, the K3
+// operand) or an Ā component (i,j,a,b) (iga_interpolate); TPB tiles per CTA.  Phases: macro
+// data per tile -> ∇F columns (one thread per node and direction) -> det / J⁻¹ per node ->
+// each thread evaluates its component (Eq. 37, closed form) at the (q+1)^d nodes into
+// registers, applies (V1⁻¹)^{⊗d} by D in-place 1D passes (all indices compile-time) and
+// writes its (q+1)^d interpolation coefficients.
 template <int D, int Q, bool SYM = false>
 struct K2Shape {
   static constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, DD = D * D, NC = DD * DD;
