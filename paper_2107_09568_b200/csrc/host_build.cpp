@@ -771,7 +771,7 @@ iga_status set_projection_v(Handle &h, const int *mv) {
     ns *= mv[k];
     iso = iso && mv[k] == mv[0] && h.qv[k] == h.qv[0];
   }
-  if (macro_smem_bytes(h.d, ns, true) > 227 * 1024 || macro_smem_bytes(h.d, ns, false) > 227 * 1024) {
+  if (k5b_smem_bytes(h, ns) > 227 * 1024 || macro_smem_bytes(h.d, ns) > 227 * 1024) {
     set_error("projection with %d sample nodes per tile: per-tile staging exceeds shared memory", ns);
     return IGA_ELIMIT;
   }

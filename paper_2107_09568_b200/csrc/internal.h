@@ -240,7 +240,8 @@ void gauss_legendre01(int n, double *x, double *w);
 // host: Pi1, x per direction; m = 0: interpolation (m_k = q_k+1), else m_k = m for every k
 iga_status set_projection(Handle &h, int m);
 iga_status set_projection_v(Handle &h, const int *mv);
-size_t macro_smem_bytes(int d, int ns, bool reverse);
+size_t macro_smem_bytes(int d, int ns);
+size_t k5b_smem_bytes(const Handle &h, int ns);
 // a-priori projection error (Eq. 59) per tile of the macro map in h (device work)
 cudaError_t launch_projection_error(const Handle &h, const double *ctrl, double nu, int n_s, double *e_tile,
                                     cudaStream_t s);

@@ -461,12 +461,26 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   }
 }
 
-// shared memory of the one-CTA-per-tile macro kernels (K2 projection path, K5b):
-// two ns×d⁴ buffers (+ ∂S/∂J ns×d² for K5b) and the ns node geometries, ns = Π m_k
-size_t macro_smem_bytes(int d, int ns_, bool reverse) {
+// shared memory of the one-CTA-per-tile K2 projection path: two ns×d⁴ buffers and the ns
+// node geometries, ns = Π m_k
+size_t macro_smem_bytes(int d, int ns_) {
   const size_t ns = (size_t)ns_, nc = (size_t)d * d * d * d;
   const size_t geo = d == 2 ? sizeof(NodeGeo<2>) : sizeof(NodeGeo<3>);
-  return sizeof(double) * (2 * ns * nc + (reverse ? ns * d * d : 0)) + ns * geo;
+  return sizeof(double) * 2 * ns * nc + ns * geo;
+}
+
+// K5b: each of its two buffers holds ns×d⁴ doubles (W', Ŵ) or the tile's staged Y
+__host__ __device__ inline size_t k5b_buf_doubles(int d, int ns, int k5s, int k5kap) {
+  const size_t nc = (size_t)d * d * d * d, np1 = d * (d + 1) / 2, np2 = d * (d - 1) / 2;
+  const size_t ny = np1 * k5s + np2 * (size_t)(k5kap - k5s), nw = (size_t)ns * nc;
+  return ny > nw ? ny : nw;
+}
+
+// K5b dynamic shared memory: two buffers, ∂S/∂J (ns×d²), the node geometries, the gphys groups
+size_t k5b_smem_bytes(const Handle &h, int ns) {
+  const size_t geo = h.d == 2 ? sizeof(NodeGeo<2>) : sizeof(NodeGeo<3>);
+  return sizeof(double) * (2 * k5b_buf_doubles(h.d, ns, h.k5_split, h.k5_kap) + (size_t)ns * h.d * h.d) + ns * geo +
+         sizeof(int) * (size_t)(h.k5_kap / 8);
 }
 
 // compile-time n_π for an isotropic degree Q; Q = -1: anisotropic (runtime c_ip.npi)
@@ -539,6 +553,98 @@ k2_interpolate_smem(const __grid_constant__ InterpConst c_ip, const double *__re
   }
 }
 
+// K5b tail (both variants): the reverse mode of S = ⟨Ŵ, Ā(J)⟩ at the ns nodes from Ŵ
+// (Wh_all[m·d⁴ + ij·d² + ab]) and the node geometries, ∂S/∂J, the chain to the active
+// control points.  Sp, Qm: ns·d² doubles of scratch each.
+template <int D>
+__device__ void k5b_tail(const InterpConst &c_ip, const MacroTile<D> &mt, const NodeGeo<D> *geo, const double *Wh_all,
+                         double *Sp, double *Qm, double *dSdJ, double lam, double mu, int64_t t,
+                         double *__restrict__ gpart) {
+  constexpr int DD = D * D, NC = DD * DD;
+  const int ns = c_ip.ns;
+  // reverse mode of S = ⟨Ŵ, Ā(J)⟩ per node, one thread per (node m, i, n):
+  // Sp = the (i, n) part of S / det, Q[i][n] = det (λ d1 + μ d2 + μ d3)
+  for (int it = threadIdx.x; it < ns * DD; it += blockDim.x) {
+    const int m = it / DD, mi = (it % DD) / D, n = it % D;
+    const double *Wh = Wh_all + m * NC;   // Ŵ[ij*DD + ab]
+    const NodeGeo<D> &g = geo[m];
+    double sp = 0.0, d1 = 0, d2 = 0, d3 = 0, sd = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      sd += Wh[(mi * D + n) * DD + a * D + a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        const double x = Wh[(mi * D + n) * DD + a * D + b];
+        sp = fma(x, lam * g.G[mi][a] * g.G[n][b] + mu * g.G[n][a] * g.G[mi][b], sp);
+      }
+    }
+    sp = fma(mu * sd, g.gg[mi][n], sp);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double wmj = 0.0, wjm = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        const double Gjb = g.G[j][b];
+        d1 = fma(Wh[(mi * D + j) * DD + n * D + b] + Wh[(j * D + mi) * DD + b * D + n], Gjb, d1);
+        d2 = fma(Wh[(j * D + mi) * DD + n * D + b] + Wh[(mi * D + j) * DD + b * D + n], Gjb, d2);
+        wmj += Wh[(mi * D + j) * DD + b * D + b];
+        wjm += Wh[(j * D + mi) * DD + b * D + b];
+      }
+      d3 = fma(wmj + wjm, g.G[j][n], d3);
+    }
+    Sp[it] = sp;
+    Qm[it] = g.det * (lam * d1 + mu * d2 + mu * d3);
+  }
+  __syncthreads();
+  // ∂S/∂J[a][β] = S G[β][a] - Σ_{i,n} G[i][a] Q[i][n] G[β][n], one thread per (m, a, β)
+  for (int it = threadIdx.x; it < ns * DD; it += blockDim.x) {
+    const int m = it / DD, a = (it % DD) / D, be = it % D;
+    const NodeGeo<D> &g = geo[m];
+    double S = 0.0;
+#pragma unroll
+    for (int x = 0; x < DD; ++x) S += Sp[m * DD + x];
+    double v = g.det * S * g.G[be][a];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int n = 0; n < D; ++n) v -= g.G[i][a] * Qm[m * DD + i * D + n] * g.G[be][n];
+    dSdJ[it] = v;
+  }
+  __syncthreads();
+  // chain to the active control points: g[r][a] = Σ_m Σ_β ∂S/∂J[a][β] ∂_β R_r(ξ_m)
+  // (node indices (m0, m1, m2) stepped, no divisions in the node loop)
+  for (int idx = threadIdx.x; idx < mt.nact * D; idx += blockDim.x) {
+    const int ra = idx / D, a = idx % D;
+    const int n0 = c_ip.pm[0] + 1, n1 = D > 1 ? c_ip.pm[1] + 1 : 1;
+    const int r[3] = {ra % n0, (ra / n0) % n1, ra / (n0 * n1)};
+    double acc = 0.0;
+    int mm[3] = {0, 0, 0};
+    for (int m = 0; m < ns; ++m) {
+      double g[D];
+      if (mt.rational) {
+        basis_grad<D>(c_ip, mt, m, ra, geo[m].W, geo[m].dW, g);
+      } else {
+        double bv[D], dv[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          bv[k] = mt.B1[k][mm[k]][r[k]];
+          dv[k] = mt.D1[k][mm[k]][r[k]];
+        }
+        g[0] = D == 2 ? dv[0] * bv[1] : dv[0] * bv[1] * bv[D - 1];
+        g[1] = D == 2 ? bv[0] * dv[1] : bv[0] * dv[1] * bv[D - 1];
+        if (D == 3) g[D - 1] = bv[0] * bv[1] * dv[D - 1];
+      }
+#pragma unroll
+      for (int be = 0; be < D; ++be) acc = fma(dSdJ[m * DD + a * D + be], g[be], acc);
+      if (++mm[0] == c_ip.mv[0]) {
+        mm[0] = 0;
+        if (++mm[1] == c_ip.mv[1]) { mm[1] = 0; ++mm[2]; }
+      }
+    }
+    gpart[((size_t)t * mt.nact + ra) * D + a] = acc;
+  }
+}
+
 // K5b: one CTA per tile: Ŵ = Πᵀ W at the m^d sample nodes, reverse mode of
 // S = ⟨Ŵ, Ā(J)⟩ per node, chain to the active macro control points.
 #ifndef IGA_K5B_THREADS
@@ -548,38 +654,52 @@ template <int D, int Q>
 __global__ void __launch_bounds__(IGA_K5B_THREADS)
 k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
             const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
-            const double *__restrict__ W, int ldw, int tpc, int k5s, const int32_t *__restrict__ gphys,
+            const double *__restrict__ W, int ldw, int tpc, int k5s, int k5kap, const int32_t *__restrict__ gphys,
             double *__restrict__ gpart, int *flag) {
-  constexpr int DD = D * D, NC = DD * DD;
-  const int NPI = npi_of<D, Q>(c_ip), NK = DD * NPI;
-  const int ns = c_ip.ns;
+  constexpr int DD = D * D, NC = DD * DD, NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2;
+  const int NPI = npi_of<D, Q>(c_ip);
+  const int ns = c_ip.ns, k2n = k5kap - k5s;
+  const size_t nbuf = k5b_buf_doubles(D, ns, k5s, k5kap);
   extern __shared__ double dyn[];
-  double *S0 = dyn, *S1 = dyn + (size_t)ns * NC, *dSdJ = dyn + 2 * (size_t)ns * NC;
+  double *S0 = dyn, *S1 = dyn + nbuf, *dSdJ = dyn + 2 * nbuf;
   NodeGeo<D> *geo = reinterpret_cast<NodeGeo<D> *>(dSdJ + (size_t)ns * DD);
+  int *sgp = reinterpret_cast<int *>(geo + ns);   // gphys of the k5kap/8 logical groups
   __shared__ MacroTile<D> mt;
   const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
   load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan);
-  // W' from K5a's Y (Eq. 38-reduced contraction): ⟨W', Ā⟩ = Σ Y⁺ Ā⁺' + Σ Y⁻ Ā⁻'
-  // with Ā^±'_ij[a,b] = ½(Ā_ij[a,b] ± Ā_ij[b,a]) for i <= j, so W'_ij[a,b] = ½Y⁺_ij[ab]
-  // (Y⁺_ij[aa] on the diagonal) ± ½Y⁻_ij[ab] (i < j, + for a < b), W'_ij = 0 for i > j
-  (void)NK;
-  constexpr int NP1 = D * (D + 1) / 2;
+  for (int g = threadIdx.x; g < k5kap / 8; g += blockDim.x) sgp[g] = gphys[g];
+  __syncthreads();
+  // stage this tile's Y (K5g/K5a output) compactly, coalesced: Y⁺[o][κ] (o < NP1, κ < k5s),
+  // then Y⁻[o][κ - k5s]; 8 consecutive threads read one 64-byte physical row group
   const int64_t nbk = t / tpc;
   const int tl = (int)(t - nbk * tpc);
+  const double *Wt = W + (size_t)(nbk * IGA_GEMM_BN + tl) * ldw;
+  const int n1 = NP1 * k5s;
+#pragma unroll
+  for (int o = 0; o < NP1 + NP2; ++o) {
+    const bool p2 = o >= NP1;
+    const int len = p2 ? k2n : k5s, k0 = p2 ? k5s : 0;
+    double *dst = S1 + (p2 ? n1 + (o - NP1) * k2n : o * k5s);
+    const double *src = Wt + (size_t)(o * tpc) * ldw;
+    for (int r = threadIdx.x; r < len; r += blockDim.x) {
+      const int kap = k0 + r;
+      dst[r] = src[sgp[kap >> 3] * 8 + (kap & 7)];
+    }
+  }
+  __syncthreads();
+  // W' from Y (Eq. 38-reduced contraction): ⟨W', Ā⟩ = Σ Y⁺ Ā⁺' + Σ Y⁻ Ā⁻'
+  // with Ā^±'_ij[a,b] = ½(Ā_ij[a,b] ± Ā_ij[b,a]) for i <= j, so W'_ij[a,b] = ½Y⁺_ij[ab]
+  // (Y⁺_ij[aa] on the diagonal) ± ½Y⁻_ij[ab] (i < j, + for a < b), W'_ij = 0 for i > j
   for (int idx = threadIdx.x; idx < NC * NPI; idx += blockDim.x) {
     const int C = idx / NC, comp = idx % NC, ij = comp / DD, ab = comp % DD;
     const int i = ij / D, j = ij % D, a = ab / D, b = ab % D;
     double w = 0.0;
     if (i <= j) {
       const int lo = min(a, b), hi = max(a, b);
-      const int o1 = sym_index(D, lo, hi), p1 = sym_index(D, i, j);
-      const int k1 = p1 * NPI + C;   // logical κ row -> its balanced physical row
-      const double y1 = W[(size_t)(nbk * IGA_GEMM_BN + o1 * tpc + tl) * ldw + gphys[k1 >> 3] * 8 + (k1 & 7)];
+      const double y1 = S1[sym_index(D, lo, hi) * k5s + sym_index(D, i, j) * NPI + C];
       w = a == b ? y1 : 0.5 * y1;
       if (i < j && a != b) {
-        const int o2 = anti_index(D, lo, hi), p2 = anti_index(D, i, j);
-        const int k2 = k5s + p2 * NPI + C;
-        const double y2 = W[(size_t)(nbk * IGA_GEMM_BN + (NP1 + o2) * tpc + tl) * ldw + gphys[k2 >> 3] * 8 + (k2 & 7)];
+        const double y2 = S1[n1 + anti_index(D, lo, hi) * k2n + anti_index(D, i, j) * NPI + C];
         w = fma(a < b ? 0.5 : -0.5, y2, w);
       }
     }
@@ -589,63 +709,130 @@ k5b_reverse(const __grid_constant__ InterpConst c_ip, const double *__restrict__
   node_geometry<D>(c_ip, mt, geo, tg, flag);
   // Ŵ = Πᵀ W (also syncs geo)
   const double *Wh_all = apply_projection<D, Q, true, NC>(c_ip, S0, S1);
+  double *Sp = Wh_all == S0 ? S1 : S0, *Qm = Sp + (size_t)ns * DD;   // the free buffer
   double lam, mu;
   lame(young[ypt ? tg : 0], nu, lam, mu);
-  for (int m = threadIdx.x; m < ns; m += blockDim.x) {
-    const double *Wh = Wh_all + m * NC;   // Ŵ[ij*DD + ab]
-    const NodeGeo<D> &g = geo[m];
-    const double det = g.det;
-    double T1 = 0, T2 = 0, T3 = 0, w[D][D];
-    for (int i = 0; i < D; ++i)
-      for (int j = 0; j < D; ++j) {
-        double sd = 0.0;
-        for (int a = 0; a < D; ++a) sd += Wh[(i * D + j) * DD + a * D + a];
-        w[i][j] = sd;
-        T3 += sd * g.gg[i][j];
+  k5b_tail<D>(c_ip, mt, geo, Wh_all, Sp, Qm, dSdJ, lam, mu, t, gpart);
+}
+
+// K5b register path (isotropic q, m = q+1, (q+1)^d <= 27; the bench shapes): one CTA per
+// tile in two roles.  Y role (warps 0-1): thread = one of the 45 (3D) / 10 (2D) distinct
+// components of Y, its n_π values loaded straight into registers (all loads in flight at
+// once), Ŷ = Πᵀ Y by d in-place register passes (Πᵀ is linear per component, so it
+// commutes with the W' expansion below), Ŷ to shared memory.  Geometry role (warps 2-3):
+// macro data, ∇F columns, det / J⁻¹ per node, overlapping the Y loads.  Then Ŵ' per node
+// from Ŷ and the common tail.
+#define IGA_K5B_YT 64   // threads of the Y role (>= 45)
+__device__ __forceinline__ void macro_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+template <int D, int Q>
+__global__ void __launch_bounds__(IGA_K5B_THREADS)
+k5b_reverse_reg(const __grid_constant__ InterpConst c_ip, const double *__restrict__ ctrl, const double *__restrict__ mknots,
+                const int *__restrict__ mspan, const double *__restrict__ young, int ypt, double nu,
+                const double *__restrict__ W, int ldw, int tpc, int k5s, const int32_t *__restrict__ gphys,
+                double *__restrict__ gpart, int *flag) {
+  constexpr int Q1 = Q + 1, NPI = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, DD = D * D, NC = DD * DD;
+  constexpr int NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2, NS = NP1 * NP1 + NP2 * NP2;
+  constexpr int GT = IGA_K5B_THREADS - IGA_K5B_YT;   // geometry-role threads
+  static_assert(NS <= IGA_K5B_YT && GT >= 32, "K5b role split");
+  __shared__ MacroTile<D> mt;
+  __shared__ NodeGeo<D> geo[NPI];
+  __shared__ double Yh[NPI][NS + 1];   // Ŷ[node][component]
+  __shared__ double Wh[NPI * NC];      // Ŵ'[node][ij·d² + ab]
+  __shared__ double SQ[2 * NPI * DD];  // Sp, Qm of the tail
+  __shared__ double dSdJ[NPI * DD];
+  const int tid = threadIdx.x;
+  const int64_t t = blockIdx.x, tg = t + c_ip.t_base;
+  if (tid < IGA_K5B_YT) {
+    if (tid < NS) {
+      bool part2;
+      int i, j, a, b, p, o;
+      sym_component<D>(tid, part2, i, j, a, b, p, o);
+      const int64_t nbk = t / tpc;
+      const int tl = (int)(t - nbk * tpc);
+      const double *src = W + (size_t)(nbk * IGA_GEMM_BN + (part2 ? NP1 + o : o) * tpc + tl) * ldw;
+      const int kb = part2 ? k5s + p * NPI : p * NPI;
+      double x[NPI];
+#pragma unroll
+      for (int C = 0; C < NPI; ++C) {
+        const int k = kb + C;
+        x[C] = src[__ldg(gphys + (k >> 3)) * 8 + (k & 7)];
+      }
+      // Πᵀ along directions 0, 1 (, 2), in place: out[m] = Σ_c Π1[dir][c][m] in[c]
+#pragma unroll
+      for (int dir = 0; dir < D; ++dir) {
+        constexpr int L = NPI / Q1;
+        const int stride = dir == 0 ? 1 : (dir == 1 ? Q1 : Q1 * Q1);
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const int base = dir == 0 ? l * Q1 : (dir == 1 ? (l % Q1) + (l / Q1) * Q1 * Q1 : l);
+          double v[Q1];
+#pragma unroll
+          for (int c = 0; c < Q1; ++c) v[c] = x[base + c * stride];
+#pragma unroll
+          for (int m = 0; m < Q1; ++m) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < Q1; ++c) acc = fma(c_ip.Pi1[dir][c * Q1 + m], v[c], acc);
+            x[base + m * stride] = acc;
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < NPI; ++m) Yh[m][tid] = x[m];
+    }
+  } else {
+    const int gt = tid - IGA_K5B_YT;
+    load_macro_tile<D>(c_ip, mt, tg, ctrl, mknots, mspan, gt, GT);
+    macro_bar(1, GT);
+    if (!mt.rational)
+      for (int w = gt; w < NPI * D; w += GT) {   // ∇F column β at node m
+        const int m = w / D, be = w % D;
+        double col[D];
+        macro_Jcol_bspline<D>(c_ip, mt, m, be, col);
+#pragma unroll
+        for (int a = 0; a < D; ++a) geo[m].G[a][be] = col[a];
+      }
+    macro_bar(1, GT);
+    for (int m = gt; m < NPI; m += GT) {
+      double J[D][D], G[D][D];
+      if (mt.rational) macro_J<D>(c_ip, mt, m, J);
+      else
         for (int a = 0; a < D; ++a)
-          for (int b = 0; b < D; ++b) {
-            const double x = Wh[(i * D + j) * DD + a * D + b];
-            T1 += x * g.G[i][a] * g.G[j][b];
-            T2 += x * g.G[j][a] * g.G[i][b];
-          }
-      }
-    const double S = det * (lam * T1 + mu * T2 + mu * T3);
-    double Q_[D][D];
-    for (int mi = 0; mi < D; ++mi)
-      for (int n = 0; n < D; ++n) {
-        double d1 = 0, d2 = 0, d3 = 0;
-        for (int j = 0; j < D; ++j)
-          for (int b = 0; b < D; ++b) {
-            d1 += Wh[(mi * D + j) * DD + n * D + b] * g.G[j][b];   // Σ_{j,b} Ŵ_{mj,nb} G_jb
-            d1 += Wh[(j * D + mi) * DD + b * D + n] * g.G[j][b];   // Σ_{i,a} Ŵ_{im,an} G_ia
-            d2 += Wh[(j * D + mi) * DD + n * D + b] * g.G[j][b];   // Σ_{i,b} Ŵ_{im,nb} G_ib
-            d2 += Wh[(mi * D + j) * DD + b * D + n] * g.G[j][b];   // Σ_{j,a} Ŵ_{mj,an} G_ja
-          }
-        for (int j = 0; j < D; ++j) d3 += (w[mi][j] + w[j][mi]) * g.G[j][n];
-        Q_[mi][n] = det * (lam * d1 + mu * d2 + mu * d3);
-      }
-    // ∂S/∂J[a][β] = S G[β][a] - Σ_{i,n} G[i][a] Q[i][n] G[β][n]
-    double *o = dSdJ + m * DD;
-    for (int a = 0; a < D; ++a)
-      for (int be = 0; be < D; ++be) {
-        double v = S * g.G[be][a];
-        for (int i = 0; i < D; ++i)
-          for (int n = 0; n < D; ++n) v -= g.G[i][a] * Q_[i][n] * g.G[be][n];
-        o[a * D + be] = v;
-      }
+          for (int be = 0; be < D; ++be) J[a][be] = geo[m].G[a][be];
+      const double det = det_inv<D>(J, G);
+      if (!(det > 0.0)) raise_flag(flag, 2, (int)tg, m);
+      NodeGeo<D> &o = geo[m];
+      for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+          o.G[i][j] = G[i][j];
+          double v = 0.0;
+          for (int c = 0; c < D; ++c) v += G[i][c] * G[j][c];
+          o.gg[i][j] = v;
+        }
+      o.det = det;
+      macro_W<D>(c_ip, mt, m, o.W, o.dW);
+    }
   }
   __syncthreads();
-  // chain to the active control points: g[r][a] = Σ_m Σ_β ∂S/∂J[a][β] ∂_β R_r(ξ_m)
-  for (int idx = threadIdx.x; idx < mt.nact * D; idx += blockDim.x) {
-    const int ra = idx / D, a = idx % D;
-    double acc = 0.0;
-    for (int m = 0; m < ns; ++m) {
-      double g[D];
-      basis_grad<D>(c_ip, mt, m, ra, geo[m].W, geo[m].dW, g);
-      for (int be = 0; be < D; ++be) acc += dSdJ[m * DD + a * D + be] * g[be];
+  // Ŵ' from Ŷ (the W' expansion of k5b_reverse, per node): W'_ij[a,b] = ½Y⁺_ij[ab]
+  // (Y⁺_ij[aa] on the diagonal) ± ½Y⁻_ij[ab] (i < j, + for a < b), 0 for i > j
+  for (int it = tid; it < NPI * NC; it += IGA_K5B_THREADS) {
+    const int m = it / NC, comp = it % NC, ij = comp / DD, ab = comp % DD;
+    const int i = ij / D, j = ij % D, a = ab / D, b = ab % D;
+    double w = 0.0;
+    if (i <= j) {
+      const int lo = min(a, b), hi = max(a, b);
+      const double y1 = Yh[m][sym_index(D, i, j) * NP1 + sym_index(D, lo, hi)];
+      w = a == b ? y1 : 0.5 * y1;
+      if (i < j && a != b) w = fma(a < b ? 0.5 : -0.5, Yh[m][NP1 * NP1 + anti_index(D, i, j) * NP2 + anti_index(D, lo, hi)], w);
     }
-    gpart[((size_t)t * mt.nact + ra) * D + a] = acc;
+    Wh[it] = w;
   }
+  __syncthreads();
+  double lam, mu;
+  lame(young[ypt ? tg : 0], nu, lam, mu);
+  k5b_tail<D>(c_ip, mt, geo, Wh, SQ, SQ + NPI * DD, dSdJ, lam, mu, t, gpart);
 }
 
 // ---------------------------------------------------------------------------------
@@ -975,7 +1162,7 @@ static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *
     }
   }
   {
-    const size_t sm = macro_smem_bytes(D, h.ns, false);
+    const size_t sm = macro_smem_bytes(D, h.ns);
     cudaError_t e = cudaFuncSetAttribute(k2_interpolate_smem<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     k2_interpolate_smem<D, Q><<<(unsigned)h.n_tiles, 256, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan,
@@ -989,11 +1176,19 @@ static cudaError_t launch_k2(const Handle &h, const double *ctrl, const double *
 template <int D, int Q>
 static cudaError_t launch_k5b(const Handle &h, const double *ctrl, const double *young, int ypt, double nu,
                               const double *W, double *gpart, cudaStream_t s) {
-  const size_t sm = macro_smem_bytes(D, h.ns, true);
+  if constexpr (Q >= 0 && K2Shape<D, (Q >= 0 ? Q : 0)>::REG) {
+    if (h.iso && h.mv[0] == Q + 1) {   // interpolation (m = q+1): register path
+      k5b_reverse_reg<D, Q><<<(unsigned)h.n_tiles_own, IGA_K5B_THREADS, 0, s>>>(
+          make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young, ypt, nu, W, (int)h.k5_rows, h.tpc, h.k5_split,
+          h.d_k5_gphys, gpart, h.d_flag);
+      return cudaGetLastError();
+    }
+  }
+  const size_t sm = k5b_smem_bytes(h, h.ns);
   cudaError_t e = cudaFuncSetAttribute(k5b_reverse<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k5b_reverse<D, Q><<<(unsigned)h.n_tiles_own, IGA_K5B_THREADS, sm, s>>>(make_interp_const(h), ctrl, h.d_mknots, h.d_mspan, young,
-                                                        ypt, nu, W, (int)h.k5_rows, h.tpc, h.k5_split,
+                                                        ypt, nu, W, (int)h.k5_rows, h.tpc, h.k5_split, h.k5_kap,
                                                         h.d_k5_gphys, gpart, h.d_flag);
   return cudaGetLastError();
 }
