@@ -817,17 +817,17 @@ k5b_reverse_reg(const __grid_constant__ InterpConst c_ip, const double *__restri
   __syncthreads();
   // Ŵ' from Ŷ (the W' expansion of k5b_reverse, per node): W'_ij[a,b] = ½Y⁺_ij[ab]
   // (Y⁺_ij[aa] on the diagonal) ± ½Y⁻_ij[ab] (i < j, + for a < b), 0 for i > j
-  for (int it = tid; it < NPI * NC; it += IGA_K5B_THREADS) {
-    const int m = it / NC, comp = it % NC, ij = comp / DD, ab = comp % DD;
-    const int i = ij / D, j = ij % D, a = ab / D, b = ab % D;
-    double w = 0.0;
-    if (i <= j) {
-      const int lo = min(a, b), hi = max(a, b);
-      const double y1 = Yh[m][sym_index(D, i, j) * NP1 + sym_index(D, lo, hi)];
-      w = a == b ? y1 : 0.5 * y1;
-      if (i < j && a != b) w = fma(a < b ? 0.5 : -0.5, Yh[m][NP1 * NP1 + anti_index(D, i, j) * NP2 + anti_index(D, lo, hi)], w);
-    }
-    Wh[it] = w;
+  // (thread = component: its two Ŷ sources and weights once, then the n_π nodes)
+  for (int comp = tid; comp < NC; comp += IGA_K5B_THREADS) {
+    const int ij = comp / DD, ab = comp % DD, i = ij / D, j = ij % D, a = ab / D, b = ab % D;
+    const int lo = min(a, b), hi = max(a, b);
+    const int c1 = sym_index(D, i <= j ? i : 0, i <= j ? j : 0) * NP1 + sym_index(D, lo, hi);
+    const double f1 = i > j ? 0.0 : (a == b ? 1.0 : 0.5);
+    const bool two = i < j && a != b;
+    const int c2 = two ? NP1 * NP1 + anti_index(D, i, j) * NP2 + anti_index(D, lo, hi) : c1;
+    const double f2 = two ? (a < b ? 0.5 : -0.5) : 0.0;
+#pragma unroll
+    for (int m = 0; m < NPI; ++m) Wh[m * NC + comp] = fma(f2, Yh[m][c2], f1 * Yh[m][c1]);
   }
   __syncthreads();
   double lam, mu;

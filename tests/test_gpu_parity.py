@@ -560,6 +560,7 @@ def _custom_problem(d, p, q, n_el, tile_el, pm=2, amp=0.05, tile_amp=0.08, seed=
     (3, 2, 2, (1, 1, 1), (2, 2, 2), 2),    # a single 3D tile
     (2, 2, 0, (3, 2), (3, 3), 2),          # q = 0: n_k = d² (one K3 chunk, tail only)
     (3, 2, 1, (3, 1, 2), (2, 2, 2), 2),    # q = 1
+    (3, 2, 0, (2, 2, 1), (2, 2, 2), 2),    # 3D q = 0 (one node per tile: K5b register path, n_π = 1)
     (2, 3, 4, (2, 2), (2, 3), 3),          # q = 4 (max), p = 3, (q+1)^d = 25
     (3, 1, 2, (5, 3, 1), (3, 2, 2), 1),    # p = 1 tiles and a degree-1 macro map; 15 tiles (ragged N-block)
     (2, 4, 3, (9, 2), (2, 2), 2),          # p = 4 (max), 18 tiles = one full 2D N-block
