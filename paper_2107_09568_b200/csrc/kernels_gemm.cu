@@ -130,7 +130,10 @@ constexpr int K3_CROW = BN + 1;                                        // epilog
 constexpr size_t K3_STAGE_BYTES = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
 constexpr size_t K3_EPI_BYTES = sizeof(double) * (size_t)K3_BM * (K3_CROW + 8 * 3);   // staging + apply runs (2 tiles)
 constexpr size_t K3_OFF_BAR = K3_STAGE_BYTES > K3_EPI_BYTES ? K3_STAGE_BYTES : K3_EPI_BYTES;
-constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int));
+#ifndef IGA_K3_SMEM_EXTRA
+#define IGA_K3_SMEM_EXTRA 0   // experiment knob: unused bytes that cap the CTAs per SM
+#endif
+constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int)) + IGA_K3_SMEM_EXTRA;
 #ifndef IGA_K3_MI
 #define IGA_K3_MI 2   // 8-row DMMA groups per K3 MMA warp for EPI 0/1 (the apply epilogue keeps 2)
 #endif
