@@ -289,6 +289,19 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
     const int len1 = ap.g1len[m0 + er], len2 = ap.g2len[m0 + er];
     const int64_t sl1 = ap.g1slot[m0 + er], sl2 = ap.g2slot[m0 + er];
+    // u of node(t, B) (diagonal: node(t, A)) and of node(t, A_t) for all TPT tiles, from the
+    // per-tile gathered copy, loaded at once (the accumulators are dead here): one L2 latency
+    double uBv[TPT][D], uAv[TPT][D];
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      const int64_t t = t0 + et0 + k < n_tiles ? t0 + et0 + k : n_tiles - 1;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        uBv[k][a] = live ? ap.u[(t * nl + B) * D + a] : 0.0;
+        uAv[k][a] = live_t ? ap.u[(t * nl + At) * D + a] : 0.0;
+      }
+    }
+#pragma unroll
     for (int k0 = 0; k0 < TPT; k0 += KR) {
 #pragma unroll
       for (int kk = 0; kk < KR; ++kk) {
@@ -300,9 +313,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
         for (int a = 0; a < D; ++a) c1[a] = c2[a] = 0.0;
         if (tv && live) {
           const double *L = sC + er * K3_CROW;
-          double uv[D];   // u of node(t, B) (diagonal: node(t, A)) from the per-tile gathered copy
-#pragma unroll
-          for (int b = 0; b < D; ++b) uv[b] = ap.u[(t * nl + B) * D + b];
+          const double *uv = uBv[k0 + kk];
 #pragma unroll
           for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -310,9 +321,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
         }
         if (tv && live_t && At != Bt) {
           const double *L = sC + et * K3_CROW;
-          double uv[D];   // u of node(t, A_t)
-#pragma unroll
-          for (int a = 0; a < D; ++a) uv[a] = ap.u[(t * nl + At) * D + a];
+          const double *uv = uAv[k0 + kk];
 #pragma unroll
           for (int b = 0; b < D; ++b)
 #pragma unroll
