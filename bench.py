@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-sensitivity", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--select-degree", type=float, default=None, metavar="TOL",
+                    help="choose the projection degree per direction a priori (Eq. 65, iga_select_degree) "
+                         "for E_proj <= TOL instead of the config's q (not the BASELINE configuration)")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: shard ONE problem over the ranks (slabs + halo, gradient all-reduce; "
                          "strong scaling) instead of one independent problem per rank (weak scaling)")
@@ -256,6 +259,11 @@ def run_ours(args, rank, world):
     dev = torch.device("cuda", local_rank)
     sens = not args.no_sensitivity
     prob = make_config(args.config)
+    q_sel = None
+    if args.select_degree is not None:   # Eq. 65 a-priori degree (device E_proj, untimed like the tables)
+        from paper_2107_09568_b200 import select_degree
+        q_sel, e_sel = select_degree(prob.macro, prob.nu, args.select_degree)
+        prob = make_config(args.config, q=q_sel if len(set(q_sel)) > 1 else q_sel[0])
     shard = args.shard and world > 1
     t0 = time.perf_counter()
     A = Assembler(prob, shard=(world, rank) if shard else None)
@@ -383,11 +391,20 @@ def run_ours(args, rank, world):
             else:
                 r["frac_vs_8tbs"] = r["achieved"] / 8000.0
     dom = rooflines["K3_contraction_scatter"]
-    roofline = {"bound": "tensor", "kernel": "K3 contraction (FP64 DMMA) + fused CSR scatter", "achieved": dom["achieved"],
-                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": dom["frac"],
-                "traffic": traffic.get("K3_dram_bytes_per_launch"),
-                "peak_source": "measured DMMA ceiling, profiles/r01_fp64_ceiling.md (MEASURED_PEAKS.json has no FP64 entry)",
-                "algorithmic_flops_per_launch": alg["k3_flops"],
+    # K3's bound: the roof whose time is larger (tensor at the BASELINE q = 2; at q = 1, the
+    # Eq. 65 choice for cfg5, its 23 GB CSR epilogue takes longer than its flops)
+    k3_hbm_bound = alg["k3_bytes"] / (hbm * 1e9) > alg["k3_flops"] / (FP64_PEAK_TFLOPS * 1e12)
+    if k3_hbm_bound:
+        dom = dict(dom, bound="hbm", achieved=alg["k3_bytes"] / (k3_ms * 1e-3) / 1e9, peak=hbm, unit="GB/s")
+        dom["frac"] = dom["achieved"] / hbm
+        rooflines["K3_contraction_scatter"]["bound_note"] = "HBM-bound at this q: the CSR epilogue bytes take longer than the flops"
+    roofline = {"bound": dom["bound"], "kernel": "K3 contraction (FP64 DMMA) + fused CSR scatter", "achieved": dom["achieved"],
+                "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"],
+                # the committed ncu capture is of the default (BASELINE) configuration only
+                "traffic": traffic.get("K3_dram_bytes_per_launch") if q_sel is None and args.config == 5 else None,
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (else the profiling guide's fallback)" if k3_hbm_bound else
+                                "measured DMMA ceiling, profiles/r01_fp64_ceiling.md (MEASURED_PEAKS.json has no FP64 entry)"),
+                "algorithmic_flops_per_launch": alg["k3_flops"], "algorithmic_bytes_per_launch": alg["k3_bytes"],
                 "flops_note": "Eq. 38-reduced contraction (45 n_pi MACs per table row and tile in 3D); "
                               "the unreduced Eq. 58 product would be %.4g flop, i.e. %.2f TFLOP/s equivalent"
                               % (alg["eq58_flops"], alg["eq58_flops"] / (k3_ms * 1e-3) / 1e12)}
@@ -396,7 +413,9 @@ def run_ours(args, rank, world):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg{args.config}" + ("" if sens else " (K only)"),
+            "config": {"workload": f"cfg{args.config}" + ("" if sens else " (K only)")
+                       + (f" with the Eq. 65 degree q={list(q_sel)} (tol {args.select_degree:g}, E_proj {e_sel:.2e})"
+                          if q_sel is not None else ""),
                        "parallelism": (f"slab{world} (one problem: slabs + halo, gradient all-reduce)" if shard
                                        else f"replica{world} (one independent problem per GPU)"),
                        "n_tiles_per_gpu": int(s.n_tiles_owned if shard else s.n_tiles), "nnz": int(nnz_total),
