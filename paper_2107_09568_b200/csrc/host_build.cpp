@@ -62,7 +62,8 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_inv_ent, h.inv_ent.data(), h.inv_ent.size() * 4) ||
       !up((void **)&h.d_patch_info, pinfo.data(), pinfo.size() * 4) ||
       !up((void **)&h.d_k5_gphys, h.k5_gphys.data(), h.k5_gphys.size() * 4) ||
-      !up((void **)&h.d_k5_mode, h.k5_mode.data(), h.k5_mode.size()))
+      !up((void **)&h.d_k5_mode, h.k5_mode.data(), h.k5_mode.size()) ||
+      !up((void **)&h.d_k5_extra, h.k5_extra.data(), h.k5_extra.size() * 4))
     return IGA_ENOMEM;
   if (cudaMalloc((void **)&h.d_side, std::max<size_t>(8, (size_t)h.n_slots * h.d * h.d * 8)) != cudaSuccess) {
     set_error("cudaMalloc of the multi-contribution slots failed");
@@ -717,6 +718,41 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
           if (g1 >= 0) h.k5_gphys[g1] = (b * W + warp) * 2 + 1;
         }
       }
+    // K5g column split (3D; part-1 group = 6 column tiles, part-2 = 3): LPT leaves loads
+    // (m+3, m, m, m) DMMAs per k-step when the unit count is 1 mod 4 (cfg5: 42/39/39/39).
+    // The heavy sub-partition keeps columns 0-3 of one of its part-1 groups (mode 9/10) and
+    // hands columns 4 and 5 to one warp on each of two light sub-partitions (mode 11/12,
+    // an extra single-column piece): 40/40/40/39.  K5g only (K5a has no modes 9-12).
+    h.k5_extra.assign(nbk * W, -1);
+#ifndef IGA_EXPERIMENT_NO_K5G
+    if (d == 3 && sens_xw_fits(h))
+      for (int b = 0; b < nbk; ++b) {
+        int L[4], hq = 0;
+        for (int q = 0; q < 4; ++q) L[q] = 3 * sload[b * 4 + q];
+        for (int q = 1; q < 4; ++q) if (L[q] > L[hq]) hq = q;
+        int nlow = 0;
+        for (int q = 0; q < 4; ++q) nlow += q != hq && L[q] == L[hq] - 3;
+        if (nlow != 3) continue;
+        int wh = -1;   // heavy warp with a part-1 first group: prefer (1,2)
+        for (int hh = 0; hh < W / 4 && wh < 0; ++hh) if (h.k5_mode[b * W + hq + 4 * hh] == 5) wh = hq + 4 * hh;
+        for (int hh = 0; hh < W / 4 && wh < 0; ++hh) if (h.k5_mode[b * W + hq + 4 * hh] == 4) wh = hq + 4 * hh;
+        if (wh < 0) continue;
+        int wl[2], nl_ = 0;   // one light warp of mode (2,2) or (1,2) on two light sub-partitions
+        for (int q = 0; q < 4 && nl_ < 2; ++q) {
+          if (q == hq) continue;
+          int w = -1;
+          for (int hh = 0; hh < W / 4 && w < 0; ++hh) if (h.k5_mode[b * W + q + 4 * hh] == 8) w = q + 4 * hh;
+          for (int hh = 0; hh < W / 4 && w < 0; ++hh) if (h.k5_mode[b * W + q + 4 * hh] == 5 && q + 4 * hh != wh) w = q + 4 * hh;
+          if (w >= 0) wl[nl_++] = w;
+        }
+        if (nl_ < 2) continue;
+        h.k5_mode[b * W + wh] = h.k5_mode[b * W + wh] == 5 ? 10 : 9;
+        for (int i = 0; i < 2; ++i) {
+          h.k5_mode[b * W + wl[i]] = h.k5_mode[b * W + wl[i]] == 8 ? 11 : 12;
+          h.k5_extra[b * W + wl[i]] = (wh * 2) | ((4 + i) << 16);
+        }
+      }
+#endif
   }
 
   if (k5x_smem_bytes(d, h.max_patch_ctrl) > 227 * 1024) { set_error("tile patch too large for the K5 shared-memory staging (%d control points)", h.max_patch_ctrl); return IGA_ELIMIT; }

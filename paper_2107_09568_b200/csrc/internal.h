@@ -115,8 +115,12 @@ struct Handle {
   double *d_Wpart = nullptr;         // [k5_nseg][blocks·72][k5_rows] partial Y (k5_nseg > 1)
   std::vector<int32_t> k5_gphys;
   std::vector<uint8_t> k5_mode;
+  // K5g column split (3D): per (κ-block, warp) an extra single-column piece (local 8-row
+  // group | column tile << 16, or -1) that evens the sub-partition DMMA loads (modes 9-12)
+  std::vector<int32_t> k5_extra;
   int32_t *d_k5_gphys = nullptr;
   uint8_t *d_k5_mode = nullptr;
+  int32_t *d_k5_extra = nullptr;
   int64_t Kp = 0;                    // K5a reduction length: table rows, each patch padded to 16
   int max_patch_ctrl = 0;
   std::vector<int32_t> pcol;         // [n_patches+1] first padded column of each patch

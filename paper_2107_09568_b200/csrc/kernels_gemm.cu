@@ -735,6 +735,7 @@ struct K5gArgs {
   int ldw;
   const uint8_t *k5_mode;
   int ts;           // per-tile stride of the u/v staging (max_patch_ctrl·D + 1)
+  const int32_t *k5_extra;   // modes 11/12: the extra single-column piece (local group | column << 16)
 };
 
 template <int S>
@@ -751,9 +752,9 @@ struct K5gAcc {
   double a0[N0 > 0 ? N0 : 1][2], a1[N1 > 0 ? N1 : 1][2];
 };
 
-template <int D, int S, int LO0, int HI0, int LO1, int HI1>
+template <int D, int S, int LO0, int HI0, int LO1, int HI1, bool HX = false>
 __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int kc_lo, int nkc, int warp, int lane,
-                                             const double *gA) {
+                                             const double *gA, int xg = 0, int xn = 0) {
   constexpr int N0 = HI0 - LO0, N1 = HI1 - LO1;
   double *sA = smem, *sB = smem + S * K5_A_CHUNK;
   uint64_t *fullA = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5gSmem<S>::STAGES +
@@ -761,6 +762,7 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
   uint64_t *fullB = fullA + S, *emptyB = fullB + S;
   int *released = reinterpret_cast<int *>(emptyB + S);
   K5gAcc<LO0, HI0, LO1, HI1> acc;
+  double accx0 = 0.0, accx1 = 0.0;   // HX: the extra piece (group xg, column tile xn)
 #pragma unroll
   for (int i = 0; i < (N0 > 0 ? N0 : 1); ++i) acc.a0[i][0] = acc.a0[i][1] = 0.0;
 #pragma unroll
@@ -784,6 +786,7 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
       for (int ni = LO0; ni < HI0; ++ni) dmma884(acc.a0[ni - LO0][0], acc.a0[ni - LO0][1], a0, b[ni]);
 #pragma unroll
       for (int ni = LO1; ni < HI1; ++ni) dmma884(acc.a1[ni - LO1][0], acc.a1[ni - LO1][1], a1, b[ni]);
+      if (HX) dmma884(accx0, accx1, a_st[(xg * 4 + kk) * 32 + lane], b_st[(xn * 4 + kk) * 32 + lane]);
     }
     __syncwarp();
     if (lane == 0) {
@@ -813,6 +816,11 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
     const int kap = warp * 16 + 8 + fr, n = ni * 8 + 2 * fc;
     sW[n * K5_WP + kap] = acc.a1[ni - LO1][0];
     sW[(n + 1) * K5_WP + kap] = acc.a1[ni - LO1][1];
+  }
+  if (HX) {
+    const int kap = xg * 8 + fr, n = xn * 8 + 2 * fc;
+    sW[n * K5_WP + kap] = accx0;
+    sW[(n + 1) * K5_WP + kap] = accx1;
   }
 }
 
@@ -951,6 +959,19 @@ k5g_wgemm(const __grid_constant__ K5gArgs g) {
       case 5: k5g_mma_role<D, S, 0, 6, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
       case 3: k5g_mma_role<D, S, 0, 6, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
       case 6: k5g_mma_role<D, S, 6, NE, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      // column split (host_build.cpp, 3D): part-1 group cut to columns 0-3; extra column pieces
+      case 9: k5g_mma_role<D, S, 0, 4, 0, 6>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 10: k5g_mma_role<D, S, 0, 4, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 11: {
+        const int x = g.k5_extra[kb * N_MMA_WARPS + warp];
+        k5g_mma_role<D, S, 6, NE, 6, NE, true>(g, smem, kc_lo, nkc, warp, lane, gA, x & 0xffff, x >> 16);
+        break;
+      }
+      case 12: {
+        const int x = g.k5_extra[kb * N_MMA_WARPS + warp];
+        k5g_mma_role<D, S, 0, 6, 6, NE, true>(g, smem, kc_lo, nkc, warp, lane, gA, x & 0xffff, x >> 16);
+        break;
+      }
       default: k5g_mma_role<D, S, 0, 0, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
     }
   }
@@ -1025,7 +1046,7 @@ static cudaError_t launch_k5g_s(const Handle &h, const double *u, const double *
   const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc;
   const int nseg = h.k5_nseg;
   K5gArgs g{h.d_tabAT, h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, h.n_patches, u, v, h.n_tiles_own,
-            (int)(h.Kp / BK), nblk * BN, nseg > 1 ? h.d_Wpart : W, (int)h.k5_rows, h.d_k5_mode, ts};
+            (int)(h.Kp / BK), nblk * BN, nseg > 1 ? h.d_Wpart : W, (int)h.k5_rows, h.d_k5_mode, ts, h.d_k5_extra};
   dim3 grid((unsigned)(h.k5_rows / BM), (unsigned)nblk, (unsigned)nseg);
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   cudaError_t e;
