@@ -1016,6 +1016,8 @@ __global__ void k5a_reduce(const double *__restrict__ part, int nseg, int64_t n,
 
 template <int D>
 static cudaError_t launch_k5a(const Handle &h, double *W, cudaStream_t s) {
+  for (int32_t x : h.k5_extra)   // the K5g column split (modes 9-12) has no K5a instance
+    if (x >= 0) return cudaErrorNotSupported;
   const bool split = h.k5_nseg > 1;
   cudaError_t e = cudaFuncSetAttribute(split ? k5a_wgemm<D, true> : k5a_wgemm<D, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM);
