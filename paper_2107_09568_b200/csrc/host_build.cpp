@@ -685,7 +685,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     std::vector<int> sload(nbk * 4, 0), bload(nbk, 0);
     std::vector<std::vector<int>> slot(nbk * 4);
     for (int g = 0; g < G1 + G2; ++g) {
-      const int w = g < G1 ? 2 : 1;
+      const int w = g < G1 ? (d == 3 ? 2 : 3) : 1;   // DMMAs per k-step: 6 : 3 (3D), 6 : 2 (2D)
       int bb = -1, ss = -1;
       for (int b = 0; b < nbk; ++b) {
         bool free_ = false;
