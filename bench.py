@@ -169,37 +169,58 @@ def load_traffic():
     return {}
 
 
-def cpu_baseline_oracle(n_el=(8, 4, 4), sens=True, repeats=1):
-    """The oracle (NumPy FP64, as it stands) on a bounded sample of the cfg5 workload:
-    the cfg5 generator (same tile, p=q=2) at a reduced macro grid.  Tables, DofMap and
-    pattern are built untimed (offline, as for the GPU).  Timed: K^π (interpolation,
-    table·coefficient product, CSR scatter) + g = uᵀ(∂K^π/∂P)v for every coordinate."""
-    from oracle import assemble as As, sensitivity as S
+def _oracle_sample(n_el):
+    from oracle import assemble as As
     from oracle.dofmap import DofMap, Pattern
     from synth import make_config, draw_uv_seeded
-    try:
-        import threadpoolctl
-        info = threadpoolctl.threadpool_info()
-        cores = max([i.get("num_threads", 1) for i in info] + [1])
-    except Exception:
-        cores = os.cpu_count()
     prob = make_config(5, n_el=n_el)
     dm = DofMap(prob)
     tabs = As.Tables(prob)
     pt = Pattern(prob, dm, tabs.pairs)
     u, v = draw_uv_seeded(5, dm.n_dof)
-    best = None
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        As.assemble_lookup(prob, tabs, pt)
-        if sens:
-            S.sensitivity(prob, tabs, pt, u, v)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return prob.n_tiles, best, cores, pt.nnz
+    return prob, tabs, pt, u, v
 
 
-def oracle_t_cost(n_std_tiles=2):
+def cpu_baseline_oracle(n_el=(8, 4, 4), sens=True, parallel=False):
+    """The oracle (NumPy FP64, as it stands) on a bounded sample of the cfg5 workload:
+    the cfg5 generator (same tile, p=q=2) at a reduced macro grid.  Tables, DofMap and
+    pattern are built untimed (offline, as for the GPU).  Timed: K^π (interpolation,
+    table·coefficient product, CSR scatter) + g = uᵀ(∂K^π/∂P)v for every coordinate.
+    parallel=False: one host thread (BLAS limited to 1 thread; the paper's serial setting,
+    P:459).  parallel=True: the same oracle calls over tiles (element matrices, gradient
+    terms) and node ranges (scatter) in a fork pool of one single-threaded process per
+    host core (tests/parity_tools.py).  Returns (tiles, seconds, cores, nnz)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import assemble as As, sensitivity as S
+    prob, tabs, pt, u, v = _oracle_sample(n_el)
+    if not parallel:
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            As.assemble_lookup(prob, tabs, pt)
+            if sens:
+                S.sensitivity(prob, tabs, pt, u, v)
+            dt = time.perf_counter() - t0
+        return prob.n_tiles, dt, 1, pt.nnz
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import parity_tools as PT
+    d = prob.d
+    t0 = time.perf_counter()
+    local = PT.shared_array((prob.n_tiles, pt.n_rows_tile, d, d), np.float64)
+    PT.run(PT.w_local, PT.tile_chunks(prob.n_tiles, 2), prob=prob, tabs=tabs, local=local)
+    bm = PT.shared_array((prob.n_tiles * pt.n_rows_tile, 2), np.int64)     # (offline on the GPU side)
+    PT.run(PT.w_block_map, PT.tile_chunks(prob.n_tiles, 8), pattern=pt, bm=bm)
+    t_bm = time.perf_counter()
+    vals = PT.shared_array((pt.nnz,), np.float64)
+    PT.run(PT.w_scatter, PT.node_ranges(pt, d, PT.n_workers()), prob=prob, pattern=pt, local=local, bm=bm, vals=vals)
+    t1 = time.perf_counter()
+    if sens:
+        np.sum(PT.run(PT.w_sensitivity, PT.tile_chunks(prob.n_tiles, 2), prob=prob, tabs=tabs, pattern=pt, u=u, v=v),
+               axis=0)
+    dt = time.perf_counter() - t1 + (t_bm - t0)
+    return prob.n_tiles, dt, PT.n_workers(), pt.nnz
+
+
+def oracle_t_cost(n_std_tiles=4):
     """On-box T_cost (Eq. 64) of the oracle: time per tile of the standard full-Gauss
     element matrices K^• (same n_g as the tables) over the lookup K^π (interpolation,
     table product and scatter), both the plain NumPy oracle on the host cores, on the cfg5
@@ -220,25 +241,28 @@ def oracle_t_cost(n_std_tiles=2):
         As.local_standard(prob, t, tabs.pairs, pts=pts)
     t_std = (time.perf_counter() - t0) / n_std_tiles
     return {"t_cost": t_std / t_pi, "s_per_tile_standard": t_std, "s_per_tile_lookup": t_pi,
-            "note": "oracle K^bullet / oracle K^pi per tile on the host cores (Eq. 64); paper: 11-107x serial"}
+            "tiles_timed": {"standard": n_std_tiles, "lookup": prob.n_tiles},
+            "note": "oracle K^bullet / oracle K^pi per tile on the host (Eq. 64), K^bullet timed on a subset of "
+                    "tiles (per-tile cost is uniform); paper: 11-107x serial"}
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    n_el = (4, 2, 2)
+    n_el = (8, 4, 4)
     times = []
     n_tiles = nnz = cores = None
     for i in range(args.warmup + args.steps):
-        n_tiles, dt, cores, nnz = cpu_baseline_oracle(n_el=n_el, sens=not args.no_sensitivity)
+        n_tiles, dt, cores, nnz = cpu_baseline_oracle(n_el=n_el, sens=not args.no_sensitivity, parallel=True)
         if i >= args.warmup:
             times.append(dt)
     t = float(np.mean(times))
     value = n_tiles / t
     sample = (f"cfg5 generator at macro grid {n_el} ({n_tiles} tiles, nnz {nnz}): oracle K^pi "
               f"(interpolation + table product + CSR scatter)" + ("" if args.no_sensitivity else " + full gradient")
-              + "; tables/DofMap/pattern untimed (offline)")
+              + f"; tables/DofMap/pattern untimed (offline); tiles and node ranges over a pool of {cores} "
+              "single-threaded host processes")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -289,22 +313,35 @@ def run_ours(args, rank, world):
         else:
             A.assemble(ctrl, young, prob.nu, vals, stream=stream)
 
+    def timed_loop(fn, steps):
+        """steps calls of fn on `stream`, an event before each and one after the last:
+        (total ms / steps, per-step ms list), barrier + synchronize on both sides."""
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        barrier(world)
+        torch.cuda.synchronize()
+        for i in range(steps):
+            evs[i].record(stream)
+            fn()
+        evs[steps].record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+        return evs[0].elapsed_time(evs[steps]) / steps, per
+
+    def window(per, mean, n_tiles_w, nnz_w):
+        med, best = float(np.median(per)), float(np.min(per))
+        med_g, best_g, mean_g = reduce_max(med, world), reduce_max(best, world), reduce_max(mean, world)
+        return {"ms_mean": mean_g, "ms_median": med_g, "ms_best": best_g,
+                "tiles_per_s_median": n_tiles_w / (med_g * 1e-3), "tiles_per_s_best": n_tiles_w / (best_g * 1e-3),
+                "nnz_per_s_median": nnz_w / (med_g * 1e-3) if nnz_w else None, "steps": len(per)}
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     A.set_profiling(True)
     clocks = ClockSampler(local_rank)
-    barrier(world)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier(world)
+    ms_local, per_main = timed_loop(step, args.steps)    # THE timed region: K steps of the whole hot path
     clk = clocks.stop()
-    ms_local = e0.elapsed_time(e1) / args.steps
     kms, kn = A.kernel_times()
     A.set_profiling(False)
     ms = reduce_max(ms_local, world)
@@ -312,6 +349,31 @@ def run_ours(args, rank, world):
     nnz_total = reduce_sum(s.nnz, world) if shard else s.nnz * world
     value = tiles_total / (ms * 1e-3)
     nnz_per_s = nnz_total / (ms * 1e-3)
+
+    # ---- SURVEY §8(d) windows, each its own CUDA-event loop (median and best) --------
+    windows = {("K_plus_g" if sens else "K_formation"): window(per_main, ms_local, tiles_total, nnz_total)}
+    if sens:
+        for _ in range(2):
+            A.assemble(ctrl, young, prob.nu, vals, stream=stream)
+        m, per = timed_loop(lambda: A.assemble(ctrl, young, prob.nu, vals, stream=stream), args.steps)
+        windows["K_formation"] = window(per, m, tiles_total, nnz_total)
+    if not shard:
+        try:
+            local_buf = torch.empty(s.n_local_rows * s.n_tiles_local * d * d, dtype=torch.float64, device=dev)
+        except RuntimeError:
+            local_buf = None
+        if local_buf is not None:
+            nz = lambda: A.assemble(ctrl, young, prob.nu, None, local_buf, stream=stream)
+            for _ in range(2):
+                nz()
+            m, per = timed_loop(nz, args.steps)
+            windows["non_zeros"] = window(per, m, tiles_total, None)
+            windows["non_zeros"]["local_values"] = int(s.n_local_rows * s.n_tiles_local * d * d) * world
+            del local_buf
+            torch.cuda.empty_cache()
+    windows["note"] = ("non_zeros = K2 + K3 into the element matrices, no CSR (the paper's convention, P:457); "
+                       "K_formation = K2 + K3 + K4 into CSR (iga_assemble, the metric's name); K_plus_g = the "
+                       "bench step (iga_assemble_sensitivity, BASELINE cfg5: K and the gradient) whose mean is `value`")
 
     # ---- e2e: host (pinned) inputs through the C ABI, gradient read back ---------
     e2e = None
@@ -334,16 +396,10 @@ def run_ours(args, rank, world):
             else:
                 A.assemble(h_ctrl.numpy(), h_young.numpy(), prob.nu, vals, stream=stream)
         step_e2e()
-        torch.cuda.synchronize()
-        barrier(world)
-        e0.record(stream)
-        for _ in range(args.steps):
-            step_e2e()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier(world)
-        ms_e2e = reduce_max(e0.elapsed_time(e1) / args.steps, world)
-        h2d = 8 * (s.n_macro_cp * d * (2 if sens else 1) + s.n_tiles * (2 if sens else 1) + (2 * s.n_dof if sens else 0))
+        m, _ = timed_loop(step_e2e, args.steps)
+        ms_e2e = reduce_max(m, world)
+        # staged by the library once per call: P (n_cp·d), E (n_tiles), u and v (n_dof each)
+        h2d = 8 * (s.n_macro_cp * d + s.n_tiles + (2 * s.n_dof if sens else 0))
         e2e = {"value": tiles_total / (ms_e2e * 1e-3), "unit": "tiles/s", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * s.n_macro_cp * d if sens else 0),
                "note": "inputs P, E (and u, v) from pinned host memory via the C ABI [any]-pointer staging; "
@@ -422,7 +478,7 @@ def run_ours(args, rank, world):
                        "n_dof": int(s.n_dof), "p": prob.p,
                        "q": prob.q, "sensitivity": sens,
                        "l2": "working set >> 126 MB L2 (CSR values alone 8*nnz bytes); no explicit flush"},
-            "nnz_per_s": nnz_per_s, "roofline": roofline, "rooflines_all": rooflines,
+            "nnz_per_s": nnz_per_s, "windows": windows, "roofline": roofline, "rooflines_all": rooflines,
             "clocks": clk, "e2e": e2e,
             "gpu_launches": int(sum(kn[i] for i in (0, 1, 2, 3, 4, 5, 7))),   # libiga kernels in the timed region
             "kernel_ms_per_step": {"K2": k2_ms, "K3": k3_ms, "K4": k4_ms, "K5x (0: fused into K5g)": k5x_ms if sens else 0.0,
@@ -430,11 +486,20 @@ def run_ours(args, rank, world):
                                    "K5c": per(5) if sens else 0.0},
             "offline": {"build_s (host topology + K1 tables + pattern)": build_s}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_t, dt, cores, nnz = cpu_baseline_oracle(sens=sens)
-        line["cpu_baseline"] = {"value": n_t / dt, "unit": "tiles/s", "cores": cores, "kind": "oracle",
-                                "sample": f"cfg5 generator at macro grid (8,4,4) = {n_t} tiles (nnz {nnz}), "
-                                          f"oracle K^pi + full gradient, {dt:.1f} s; tables/pattern untimed",
-                                "oracle_t_cost": oracle_t_cost()}
+        n_t, dt1, _, nnz = cpu_baseline_oracle(sens=sens)
+        n_t, dtp, cores, _ = cpu_baseline_oracle(sens=sens, parallel=True)
+        what = "oracle K^pi" + (" + full gradient" if sens else "")
+        line["cpu_baseline"] = {
+            "value": n_t / dtp, "unit": "tiles/s", "cores": cores, "kind": "oracle",
+            "sample": f"cfg5 generator at macro grid (8,4,4) = {n_t} tiles (nnz {nnz}), {what}: {dtp:.2f} s over a "
+                      f"fork pool of {cores} single-threaded processes (tiles / node ranges); tables/pattern untimed",
+            "single_thread": {"value": n_t / dt1, "unit": "tiles/s", "cores": 1, "seconds": dt1,
+                              "note": "same sample, one host thread (BLAS limited to 1), the paper's serial setting (P:459)"},
+            "extrapolated_cfg5_s": {"single_thread": 8192 * dt1 / n_t, "all_cores": 8192 * dtp / n_t,
+                                    "extrapolated": True,
+                                    "note": "linear extrapolation to the 8192 cfg5 tiles (per-tile cost is uniform); "
+                                            "the full cfg5 oracle is not run here"},
+            "oracle_t_cost": oracle_t_cost()}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

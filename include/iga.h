@@ -95,7 +95,8 @@ typedef struct {
   int32_t k_stride;       /* padded row stride (doubles) of the table / coefficient buffers */
   int32_t n_patches;
   int32_t n_gauss;        /* Gauss points per direction per tile knot span (R3) */
-  int32_t reserved;
+  int32_t sens_path;      /* sensitivity route chosen at build: bit 0 = fused K5g (else K5x + K5a),
+                             bits 8..15 = K5a split-K segments (1 = none); informational */
   int64_t n_tiles;        /* m_M = macro elements (Eq. 5), whole problem; per-tile E has this length */
   int64_t n_local_rows;   /* Σ_p n_nz,p = rows of the stacked mat𝔎 (Eqs. 56-57) */
   int64_t n_macro_cp;     /* macro control points (Eq. 4) */
@@ -168,7 +169,9 @@ iga_status iga_build_topology_q(const iga_spline *tile_patches, int32_t n_patche
  *  young        [any] E: one double (young_per_tile = 0) or n_tiles doubles (= 1).
  *  nu           Poisson ratio, -1 < ν < 0.5.
  *  csr_values   [any] nnz doubles, overwritten, ordered as the pattern of iga_get_pattern
- *               (the rows [row_begin, row_begin + n_rows) of K for a shard).
+ *               (the rows [row_begin, row_begin + n_rows) of K for a shard).  May be NULL
+ *               when local_values is given: then only the non-zero components are formed
+ *               (K2 + K3 into nzdata, no CSR — the paper's timing convention).
  *  local_values [any] optional (NULL = skip): n_local_rows*n_tiles_local*d² doubles receiving
  *               nzdata (Eq. 58) as local[row][t*d² + a*d + b], t = local tile index.
  * Kernels: K2 (per-tile ∇F at the (q+1)^d Gauss nodes -> Ā (Eq. 37) -> interpolation

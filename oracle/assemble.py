@@ -50,29 +50,39 @@ def local_lookup(prob, tabs: Tables, ctrl, tiles, coefs=None):
     return np.stack(out)
 
 
-def scatter(prob, pattern, local, tiles=None):
-    """CSR values of K from element matrices (reading R9)."""
+def scatter(prob, pattern, local, tiles=None, out=None, bmap=None, nodes=None):
+    """CSR values of K from element matrices (reading R9).  local (len(tiles), n_rows, d, d)
+    of the given tiles (default all); `out`: add into this CSR value array instead of a
+    new zero one (so that consecutive tile ranges accumulate in the order t, row);
+    `bmap`: the tiles' block map (pattern.block_map(tiles)) if already at hand;
+    `nodes` = (n0, n1): only the CSR rows of nodes n0 <= I < n1 (the same additions in
+    the same order, restricted to those rows — for filling disjoint row ranges apart)."""
     d = prob.d
     nt = local.shape[0]
     tiles = np.arange(nt) if tiles is None else np.asarray(tiles)
     I, J = pattern.I[tiles].ravel(), pattern.J[tiles].ravel()
     L = local.reshape(-1, d, d)
-    fwd = pattern.pos(I, J)
-    bwd = pattern.pos(J, I)
+    if bmap is None:
+        fwd = pattern.pos(I, J)
+        bwd = pattern.pos(J, I)
+    else:
+        fwd, bwd = bmap[:, 0], bmap[:, 1]
     rowlen = d * pattern.nnzb
-    vals = np.zeros(pattern.nnz, dtype=local.dtype)
+    vals = np.zeros(pattern.nnz, dtype=local.dtype) if out is None else out
     off = I != J
+    in1 = np.ones(len(I), dtype=bool) if nodes is None else (I >= nodes[0]) & (I < nodes[1])
+    in2 = off if nodes is None else off & (J >= nodes[0]) & (J < nodes[1])
     n = len(I)
     idx = np.full((n, d, d, 2), -1, dtype=np.int64)
     val = np.zeros((n, d, d, 2), dtype=local.dtype)
     for a in range(d):
         for b in range(d):
             # (I,a),(J,b) for every block; diagonal blocks use the upper entry
-            idx[:, a, b, 0] = fwd + a * rowlen[I] + b
-            val[:, a, b, 0] = np.where(off, L[:, a, b], L[:, min(a, b), max(a, b)])
+            idx[in1, a, b, 0] = fwd[in1] + a * rowlen[I[in1]] + b
+            val[in1, a, b, 0] = np.where(off[in1], L[in1, a, b], L[in1, min(a, b), max(a, b)])
             # mirrored (J,b),(I,a) for A < B
-            idx[off, a, b, 1] = bwd[off] + b * rowlen[J[off]] + a
-            val[off, a, b, 1] = L[off, a, b]
+            idx[in2, a, b, 1] = bwd[in2] + b * rowlen[J[in2]] + a
+            val[in2, a, b, 1] = L[in2, a, b]
     idx, val = idx.ravel(), val.ravel()          # C order: t, row, a, b, copy
     keep = idx >= 0
     np.add.at(vals, idx[keep], val[keep])

@@ -148,7 +148,8 @@ class Pattern:
         self.J = np.concatenate(J_all, axis=1)
         nn = dm.n_nodes
         keys = np.concatenate([(self.I * nn + self.J).ravel(), (self.J * nn + self.I).ravel()])
-        blocks = np.unique(keys)
+        keys.sort()                                              # unique by sort + adjacent compare
+        blocks = keys[np.concatenate([[True], keys[1:] != keys[:-1]])]
         bI, bJ = blocks // nn, blocks % nn
         self.nnzb = np.bincount(bI, minlength=nn).astype(np.int64)
         self.brow_ptr = np.concatenate([[0], np.cumsum(self.nnzb)])
@@ -174,43 +175,19 @@ class Pattern:
         """CSR position of scalar entry (I*d, J*d) for node-block arrays I, J."""
         d = self.prob.d
         nn = self.dm.n_nodes
-        b = np.searchsorted(self.blocks, I * nn + J)
-        assert np.all(self.blocks[b] == I * nn + J)
+        key = I * nn + J
+        order = np.argsort(key, kind="stable")                  # sorted queries: a faster binary search
+        b = np.empty(len(key), dtype=np.int64)
+        b[order] = np.searchsorted(self.blocks, key[order])
+        assert np.all(self.blocks[b] == key)
         jpos = b - self.brow_ptr[I]
         return self.row_ptr[I * d] + d * jpos
 
-    def block_map(self):
-        """(n_tiles * n_rows_tile, 2) int64: (pos(I*d, J*d), pos(J*d, I*d))."""
-        fwd = self.pos(self.I.ravel(), self.J.ravel())
-        bwd = self.pos(self.J.ravel(), self.I.ravel())
+    def block_map(self, tiles=None):
+        """(len(tiles) * n_rows_tile, 2) int64: (pos(I*d, J*d), pos(J*d, I*d)); all tiles
+        by default, else the given tiles in the given order."""
+        I = self.I if tiles is None else self.I[np.asarray(tiles)]
+        J = self.J if tiles is None else self.J[np.asarray(tiles)]
+        fwd = self.pos(I.ravel(), J.ravel())
+        bwd = self.pos(J.ravel(), I.ravel())
         return np.stack([fwd, bwd], axis=1)
-
-
-def node_locations(dm):
-    """node -> list of flat (t*n_local + loc) indices (CSR-like arrays)."""
-    flat = dm.node.ravel()
-    order = np.argsort(flat, kind="stable")
-    starts = np.searchsorted(flat[order], np.arange(dm.n_nodes + 1))
-    return order, starts
-
-
-def row_contributions(prob, dm, pairs, I, locs=None):
-    """For one node row I (no full pattern needed): the sorted block columns J and,
-    per J, the contributing (t, row, transposed) triples in (t, row) order (R9)."""
-    order, starts = locs if locs is not None else node_locations(dm)
-    nl = dm.n_local_ctrl
-    row_off = np.cumsum([0] + [len(p) for p in pairs])
-    contrib = {}
-    for f in order[starts[I]:starts[I + 1]]:
-        t, loc = divmod(int(f), nl)
-        p = int(np.searchsorted(dm.offsets, loc, side="right") - 1)
-        A = loc - dm.offsets[p]
-        pr = pairs[p]
-        for k in np.nonzero((pr[:, 0] == A) | (pr[:, 1] == A))[0]:
-            a, b = int(pr[k, 0]), int(pr[k, 1])
-            other = b if a == A else a
-            J = int(dm.node[t, dm.offsets[p] + other])
-            tr = int(a != A)                 # I is the B-side of the pair -> transposed block
-            contrib.setdefault(J, []).append((t, int(row_off[p] + k), tr))
-    cols = sorted(contrib)
-    return cols, [sorted(contrib[J]) for J in cols]

@@ -70,7 +70,9 @@ def macro_jacobian(macro, ctrl, t, xi):
     F(u) = Σ_i R_i^H(u) m_i (Eq. 4); u_k = U_k[s_k] + h_k ξ_k; ∂/∂ξ_k = h_k ∂/∂u_k.
     NURBS (macro.weights, NEXT N4): R_i = w_i N_i / W with W = Σ_j w_j N_j, so
     ∂_k R_i = w_i (∂_k N_i W - N_i ∂_k W) / W².
-    `ctrl` may be complex (complex-step sensitivity).  Returns (n_pts, d, d)."""
+    `ctrl` may be complex (complex-step sensitivity) and may carry leading batch axes
+    (..., n_cp, d) — one control net per batch entry, e.g. one complex-step
+    perturbation each.  Returns (..., n_pts, d, d)."""
     d = macro.dim
     spans = tile_element(macro, t)
     vals, ders = [], []
@@ -94,11 +96,12 @@ def macro_jacobian(macro, ctrl, t, xi):
     if w is not None:
         W = sum(w[A] * Nt[A] for A in act)
         dW = [sum(w[A] * dNt[A][k] for A in act) for k in range(d)]
-    J = np.zeros((xi.shape[0], d, d), dtype=np.result_type(ctrl, np.float64))
+    ctrl = np.asarray(ctrl)
+    J = np.zeros(ctrl.shape[:-2] + (xi.shape[0], d, d), dtype=np.result_type(ctrl, np.float64))
     for A in act:
         for k in range(d):
             g = dNt[A][k] if w is None else w[A] * (dNt[A][k] * W - Nt[A] * dW[k]) / W ** 2
-            J[:, :, k] += g[:, None] * ctrl[A][None, :]
+            J[..., :, :, k] += g[:, None] * ctrl[..., A, None, :]
     return J
 
 
@@ -265,6 +268,23 @@ def tile_coefficients(prob, ctrl, t, E=None, route=A_closed, m=None):
             raise ValueError(f"degenerate macro element: tile {t}")
         return route(J, lam, mu)
     return project_field(field, prob.q, d, m or getattr(prob, "n_proj", 0))
+
+
+def tile_coefficients_batch(prob, ctrls, t, E=None, route=A_closed, m=None):
+    """tile_coefficients for a batch of control nets ctrls (B, n_cp, d) of the same tile:
+    (B, n_pi, d, d, d, d).  The same arithmetic per batch entry (the batch rides along as
+    extra columns of the projection's right-hand side); used by the complex-step
+    sensitivity, one perturbed net per (k, α)."""
+    d = prob.d
+    E = prob.young[t] if E is None else E
+    lam, mu = lame(E, prob.nu)
+
+    def field(X):
+        J = macro_jacobian(prob.macro, ctrls, t, X)             # (B, n, d, d)
+        if np.any(np.real(np.linalg.det(J)) <= 0):
+            raise ValueError(f"degenerate macro element: tile {t}")
+        return np.moveaxis(route(J, lam, mu), 1, 0)              # (n, B, d, d, d, d)
+    return np.moveaxis(project_field(field, prob.q, d, m or getattr(prob, "n_proj", 0)), 0, 1)
 
 
 def projection_points(q, d, m=0):

@@ -68,17 +68,36 @@ def sensitivity(prob, tabs, pattern, u, v, ctrl=None, entries=None, tiles=None):
     want = None if entries is None else set((int(k), int(a)) for k, a in entries)
     for t in (range(prob.n_tiles) if tiles is None else tiles):
         act = macro_active(prob, t)
-        if want is not None and not any((k, a) in want for k in act for a in range(d)):
+        ent = [(k, a) for k in act for a in range(d) if want is None or (k, a) in want]
+        if not ent:
             continue
         W = tile_W(prob, tabs, pattern, u, v, t)
-        for k in act:
-            for a in range(d):
-                if want is not None and (k, a) not in want:
-                    continue
-                c = ctrl.astype(np.complex128)
-                c[k, a] += 1j * H
-                coef = M.tile_coefficients(prob, c, t)
-                g[k, a] += np.imag(np.sum(W * coef_matrix(coef))) / H
+        # one complex-step perturbed control net per entry (k, α), evaluated as a batch
+        c = np.broadcast_to(ctrl.astype(np.complex128), (len(ent),) + ctrl.shape).copy()
+        for n, (k, a) in enumerate(ent):
+            c[n, k, a] += 1j * H
+        coefs = M.tile_coefficients_batch(prob, c, t)
+        for n, (k, a) in enumerate(ent):
+            g[k, a] += np.imag(np.sum(W * coef_matrix(coefs[n]))) / H
+    return g
+
+
+def sensitivity_entrywise(prob, tabs, pattern, u, v, entries, ctrl=None):
+    """The same complex step, one tile_coefficients call per (tile, k, α): pins the
+    batched evaluation of `sensitivity`."""
+    ctrl = prob.macro.ctrl if ctrl is None else ctrl
+    g = np.zeros_like(ctrl, dtype=np.float64)
+    want = set((int(k), int(a)) for k, a in entries)
+    for t in range(prob.n_tiles):
+        act = macro_active(prob, t)
+        ent = [(k, a) for k in act for a in range(prob.d) if (k, a) in want]
+        if not ent:
+            continue
+        W = tile_W(prob, tabs, pattern, u, v, t)
+        for k, a in ent:
+            c = ctrl.astype(np.complex128)
+            c[k, a] += 1j * H
+            g[k, a] += np.imag(np.sum(W * coef_matrix(M.tile_coefficients(prob, c, t)))) / H
     return g
 
 

@@ -38,7 +38,7 @@ class iga_interface(C.Structure):
 
 class iga_sizes(C.Structure):
     _fields_ = [("dim", C.c_int32), ("q", C.c_int32), ("n_pi", C.c_int32), ("n_k", C.c_int32),
-                ("k_stride", C.c_int32), ("n_patches", C.c_int32), ("n_gauss", C.c_int32), ("reserved", C.c_int32),
+                ("k_stride", C.c_int32), ("n_patches", C.c_int32), ("n_gauss", C.c_int32), ("sens_path", C.c_int32),
                 ("n_tiles", C.c_int64), ("n_local_rows", C.c_int64), ("n_macro_cp", C.c_int64),
                 ("n_nodes", C.c_int64), ("n_dof", C.c_int64), ("nnz", C.c_int64), ("n_blocks", C.c_int64),
                 ("n_contrib", C.c_int64), ("n_multi_blocks", C.c_int64), ("n_side_slots", C.c_int64),
@@ -115,14 +115,36 @@ def _check(status):
         raise IgaError(status, load().iga_last_error().decode())
 
 
-def _ptr(x):
-    """Raw pointer of a torch tensor (any device) or a C-contiguous numpy array."""
+_NP_OF_TORCH = {"torch.float64": np.float64, "torch.int64": np.int64, "torch.int32": np.int32}
+
+
+def _ptr(x, n=None, dtype=np.float64, name="argument"):
+    """Raw pointer of a torch tensor (host or CUDA) or a numpy array, after checking what
+    the C ABI will read or write through it: C-contiguous, of `dtype`, with at least `n`
+    elements (None: no size check), on the current CUDA device if it is a CUDA tensor.
+    Raises ValueError (never an assert: the ABI trusts these n·sizeof bytes)."""
     if x is None:
         return None
     if isinstance(x, np.ndarray):
-        assert x.flags["C_CONTIGUOUS"]
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name}: numpy array must be C-contiguous")
+        if x.dtype != np.dtype(dtype):
+            raise ValueError(f"{name}: dtype {x.dtype}, expected {np.dtype(dtype)}")
+        if n is not None and x.size < n:
+            raise ValueError(f"{name}: {x.size} elements, needs {n}")
         return x.ctypes.data
-    assert x.is_contiguous(), "tensor must be contiguous"
+    if not hasattr(x, "data_ptr"):
+        raise ValueError(f"{name}: expected a numpy array or a torch tensor, got {type(x).__name__}")
+    if not x.is_contiguous():
+        raise ValueError(f"{name}: tensor must be contiguous")
+    if _NP_OF_TORCH.get(str(x.dtype)) is not np.dtype(dtype).type:
+        raise ValueError(f"{name}: dtype {x.dtype}, expected {np.dtype(dtype)}")
+    if n is not None and x.numel() < n:
+        raise ValueError(f"{name}: {x.numel()} elements, needs {n}")
+    if x.is_cuda:
+        import torch
+        if x.device.index != torch.cuda.current_device():
+            raise ValueError(f"{name}: on {x.device}, the handle works on cuda:{torch.cuda.current_device()}")
     return x.data_ptr()
 
 
@@ -173,7 +195,7 @@ def projection_error(macro, q, nu, n_samples=8, m_extra=0, e_tile=None, stream=N
     mac = _spline(macro, keep)
     e = C.c_double()
     _check(load().iga_projection_error(C.byref(mac), _qvec(q, macro.dim), int(m_extra), float(nu), int(n_samples),
-                                       C.byref(e), _ptr(e_tile), _stream_ptr(stream)))
+                                       C.byref(e), _ptr(e_tile, name="e_tile"), _stream_ptr(stream)))
     return e.value
 
 
@@ -220,42 +242,74 @@ class Assembler:
             self._h = None
 
     # --- hot path -----------------------------------------------------------
+    # required lengths of the [any] arguments (include/iga.h)
+    def _ctrl(self, ctrl):
+        return _ptr(ctrl, self.sizes.n_macro_cp * self.sizes.dim, name="macro_ctrl")
+
+    def _young(self, young):
+        n = _numel(young)
+        if n not in (1, self.sizes.n_tiles):
+            raise ValueError(f"young: {n} values, expected 1 or n_tiles = {self.sizes.n_tiles}")
+        return _ptr(young, n, name="young"), int(n > 1)
+
+    def _nloc(self):
+        s = self.sizes
+        return s.n_local_rows * s.n_tiles_local * s.dim * s.dim
+
     def assemble(self, ctrl, young, nu, values, local=None, stream=None):
-        _check(load().iga_assemble(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
-                                   _ptr(values), _ptr(local), _stream_ptr(stream)))
+        yp, per_tile = self._young(young)
+        _check(load().iga_assemble(self._h, self._ctrl(ctrl), yp, per_tile, float(nu),
+                                   _ptr(values, self.sizes.nnz, name="csr_values"),
+                                   _ptr(local, self._nloc(), name="local_values"), _stream_ptr(stream)))
 
     def sensitivity(self, ctrl, young, nu, u, v, grad, stream=None):
-        _check(load().iga_sensitivity(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
-                                      _ptr(u), _ptr(v), _ptr(grad), _stream_ptr(stream)))
+        s = self.sizes
+        yp, per_tile = self._young(young)
+        _check(load().iga_sensitivity(self._h, self._ctrl(ctrl), yp, per_tile, float(nu),
+                                      _ptr(u, s.n_dof, name="u"), _ptr(v, s.n_dof, name="v"),
+                                      _ptr(grad, s.n_macro_cp * s.dim, name="grad"), _stream_ptr(stream)))
 
     def assemble_sensitivity(self, ctrl, young, nu, u, v, values, grad, stream=None):
         """K (CSR values) and g = uᵀ(∂K/∂P)v in one call (iga_assemble_sensitivity)."""
-        _check(load().iga_assemble_sensitivity(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
-                                               _ptr(u), _ptr(v), _ptr(values), _ptr(grad), _stream_ptr(stream)))
+        s = self.sizes
+        yp, per_tile = self._young(young)
+        _check(load().iga_assemble_sensitivity(self._h, self._ctrl(ctrl), yp, per_tile, float(nu),
+                                               _ptr(u, s.n_dof, name="u"), _ptr(v, s.n_dof, name="v"),
+                                               _ptr(values, s.nnz, name="csr_values"),
+                                               _ptr(grad, s.n_macro_cp * s.dim, name="grad"), _stream_ptr(stream)))
 
     def volume(self, ctrl, grad=None, stream=None):
         """V^π (float) and optionally dV^π/dP into grad (iga_volume)."""
         out = np.zeros(1)
-        _check(load().iga_volume(self._h, _ptr(ctrl), out.ctypes.data, _ptr(grad), _stream_ptr(stream)))
+        _check(load().iga_volume(self._h, self._ctrl(ctrl), out.ctypes.data,
+                                 _ptr(grad, self.sizes.n_macro_cp * self.sizes.dim, name="grad"), _stream_ptr(stream)))
         return float(out[0])
 
     def load_vector(self, ctrl, body_force, f, stream=None):
         """Body-force load vector for a constant b (iga_load_vector)."""
         b = np.ascontiguousarray(body_force, dtype=np.float64)
-        _check(load().iga_load_vector(self._h, _ptr(ctrl), b.ctypes.data, _ptr(f), _stream_ptr(stream)))
+        if b.size != self.sizes.dim:
+            raise ValueError(f"body_force: {b.size} values, expected d = {self.sizes.dim}")
+        _check(load().iga_load_vector(self._h, self._ctrl(ctrl), b.ctypes.data, _ptr(f, self.sizes.n_rows, name="f"),
+                                      _stream_ptr(stream)))
 
     def apply(self, ctrl, young, nu, u, y, stream=None):
         """Matrix-free y = K^π u (iga_apply)."""
-        _check(load().iga_apply(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu), _ptr(u),
-                                _ptr(y), _stream_ptr(stream)))
+        yp, per_tile = self._young(young)
+        _check(load().iga_apply(self._h, self._ctrl(ctrl), yp, per_tile, float(nu), _ptr(u, self.sizes.n_dof, name="u"),
+                                _ptr(y, self.sizes.n_rows, name="y"), _stream_ptr(stream)))
 
     def interpolate(self, ctrl, young, nu, coef, stream=None):
-        _check(load().iga_interpolate(self._h, _ptr(ctrl), _ptr(young), int(_numel(young) > 1), float(nu),
-                                      _ptr(coef), _stream_ptr(stream)))
+        s = self.sizes
+        yp, per_tile = self._young(young)
+        _check(load().iga_interpolate(self._h, self._ctrl(ctrl), yp, per_tile, float(nu),
+                                      _ptr(coef, s.n_tiles_local * s.dim * s.dim * s.k_stride, name="coef"),
+                                      _stream_ptr(stream)))
 
     # --- accessors ----------------------------------------------------------
     def pattern(self, row_ptr=None, col_idx=None):
-        _check(load().iga_get_pattern(self._h, _ptr(row_ptr), _ptr(col_idx)))
+        _check(load().iga_get_pattern(self._h, _ptr(row_ptr, self.sizes.n_rows + 1, np.int64, "row_ptr"),
+                                      _ptr(col_idx, self.sizes.nnz, np.int32, "col_idx")))
 
     def block_map(self, t_begin=0, t_end=None):
         t_end = self.sizes.n_tiles_local if t_end is None else t_end

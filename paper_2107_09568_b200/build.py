@@ -22,17 +22,20 @@ def build(verbose=False, force=False, defines=(), lib=None):
         return LIBP
     objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(defines))
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in srcs:
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+    objs = [os.path.join(objdir, os.path.basename(src) + ".o") for src in srcs]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
         cmd = [NVCC] + FLAGS + ["-D" + x for x in defines] + ["-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed for {src}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return src, subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:   # nvcc processes in parallel
+        for src, r in ex.map(compile_one, zip(srcs, objs)):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed for {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIBP] + objs + ["-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -372,6 +372,11 @@ iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
   o->k_stride = h.kstride;
   o->n_patches = h.n_patches;
   o->n_gauss = h.n_g;
+#ifndef IGA_EXPERIMENT_NO_K5G
+  o->sens_path = (sens_xw_fits(h) ? 1 : 0) | (h.k5_nseg << 8);
+#else
+  o->sens_path = h.k5_nseg << 8;
+#endif
   o->n_tiles = h.n_tiles_glob;
   o->n_local_rows = h.M;
   o->n_macro_cp = h.n_cp;
@@ -392,7 +397,7 @@ iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
 
 iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const double *young, int32_t young_per_tile,
                         double nu, double *csr_values, double *local_values, void *stream) {
-  if (!Hc || !macro_ctrl || !csr_values) { set_error("NULL argument"); return IGA_EINVAL; }
+  if (!Hc || !macro_ctrl || (!csr_values && !local_values)) { set_error("NULL argument"); return IGA_EINVAL; }
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   iga_status st = check_material(h, young, nu);
@@ -418,12 +423,14 @@ iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const do
   int id = pf.begin(0);
   CU(launch_interpolate(h, dctrl, dyoung, young_per_tile, nu, h.d_coef, true, s));
   pf.end(id);
-  id = pf.begin(1);
-  CU(launch_contraction(h, dvals, nullptr, s));
-  pf.end(id);
-  id = pf.begin(2);
-  CU(launch_scatter_multi(h, dvals, s));
-  pf.end(id);
+  if (dvals) {   // csr_values NULL: the non-zero components only (K2 + K3 nzdata)
+    id = pf.begin(1);
+    CU(launch_contraction(h, dvals, nullptr, s));
+    pf.end(id);
+    id = pf.begin(2);
+    CU(launch_scatter_multi(h, dvals, s));
+    pf.end(id);
+  }
   if (dlocal_out) {   // optional nzdata output (parity of the element matrices, R17): K3 again
     id = pf.begin(8);
     CU(launch_contraction(h, nullptr, dlocal_out, s));

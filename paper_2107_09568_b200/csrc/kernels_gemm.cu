@@ -37,6 +37,7 @@ constexpr int MI = 2;              // 2 DMMA row tiles per warp (16 rows)
 constexpr int N_MMA_WARPS = IGA_K5_BM / 16;                                // K5a: 16
 constexpr int BM = 16 * N_MMA_WARPS;                                        // 256 (K5a κ rows)
 constexpr int K3_BM = IGA_K3_BM, K3_WARPS = K3_BM / 16;                     // K3: 64 rows, 4 MMA warps
+static_assert(K3_BM == 64 || K3_BM == 128, "K3 row blocks: 64 (product) or 128 rows; other shapes are not supported by every epilogue");
 static_assert(BM == IGA_K5_BM, "K5a CTA rows");
 constexpr int K5_X_CHUNK_ = BN * BK;                                        // doubles per X chunk
 
@@ -721,6 +722,7 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
 #endif
 constexpr int K5G_GEN_WARPS = IGA_K5G_GEN_WARPS;
 static_assert(K5G_GEN_WARPS % 4 == 0, "generator groups of 4 warps (128 threads per chunk)");
+static_assert(K5G_GEN_WARPS / 4 <= 3, "the generators' emptyB parity wait needs groups <= stages (S >= 3)");
 constexpr int K5G_THREADS = 32 * (N_MMA_WARPS + K5G_GEN_WARPS);
 
 struct K5gArgs {
@@ -1045,6 +1047,10 @@ template <int D, int S>
 static cudaError_t launch_k5g_s(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s) {
   const int ts = h.max_patch_ctrl * D + 1;
   const size_t smem = K5gSmem<S>::bytes(D, ts);
+  // the Y staging (after the main loop) overlays the stage ring and the u/v staging, not
+  // the mbarriers behind them
+  if (sizeof(double) * BN * K5_WP > K5gSmem<S>::STAGES + sizeof(double) * 2 * (D == 3 ? 8 : 16) * (size_t)ts)
+    return cudaErrorNotSupported;
   const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc;
   const int nseg = h.k5_nseg;
   K5gArgs g{h.d_tabAT, h.d_k5_pair, h.d_patch_info, h.d_node_map, h.n_local_ctrl, h.n_patches, u, v, h.n_tiles_own,
@@ -1071,7 +1077,10 @@ static cudaError_t launch_k5g_s(const Handle &h, const double *u, const double *
 // per-patch u, v staging does not fit beside a 3-stage ring (the caller then runs K5x + K5a)
 bool sens_xw_fits(const Handle &h) {
   const int ts = h.max_patch_ctrl * h.d + 1;
-  return (h.d == 3 ? K5gSmem<3>::bytes(3, ts) : K5gSmem<3>::bytes(2, ts)) <= 227 * 1024;
+  const size_t uv = sizeof(double) * 2 * (h.d == 3 ? 8 : 16) * (size_t)ts;
+  const size_t lim = 227 * 1024;
+  auto ok = [&](size_t stages, size_t bytes) { return bytes <= lim && sizeof(double) * BN * K5_WP <= stages + uv; };
+  return ok(K5gSmem<4>::STAGES, K5gSmem<4>::bytes(h.d, ts)) || ok(K5gSmem<3>::STAGES, K5gSmem<3>::bytes(h.d, ts));
 }
 
 cudaError_t launch_sens_XW(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s) {

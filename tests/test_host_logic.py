@@ -60,6 +60,36 @@ def test_host_topology_bit_exact_vs_oracle(c, oracle_problem):
     assert np.array_equal(A.pairs(), np.concatenate(ob["tabs"].pairs))
 
 
+def test_binding_validates_buffers():
+    """The binding checks dtype, length and contiguity of every [any] buffer before the C
+    ABI reads or writes through it (ValueError; no compute call is reached)."""
+    from paper_2107_09568_b200 import Assembler
+    from synth import make_config
+    prob = make_config(1)
+    A = Assembler(prob, topology_only=True)
+    s = A.sizes
+    ctrl = np.ascontiguousarray(prob.macro.ctrl)
+    young = np.ones(1)
+    good = np.empty(s.nnz)
+    with pytest.raises(ValueError, match="dtype"):
+        A.assemble(ctrl.astype(np.float32), young, 0.3, good)
+    with pytest.raises(ValueError, match="elements"):
+        A.assemble(ctrl[:-1], young, 0.3, good)
+    with pytest.raises(ValueError, match="elements"):
+        A.assemble(ctrl, young, 0.3, np.empty(s.nnz - 1))
+    with pytest.raises(ValueError, match="young"):
+        A.assemble(ctrl, np.ones(3), 0.3, good)
+    with pytest.raises(ValueError, match="contiguous"):
+        A.sensitivity(ctrl, young, 0.3, np.empty(2 * s.n_dof)[::2], np.empty(s.n_dof), np.empty(ctrl.size))
+    with pytest.raises(ValueError, match="grad"):
+        A.sensitivity(ctrl, young, 0.3, np.empty(s.n_dof), np.empty(s.n_dof), np.empty(ctrl.size - 2))
+    with pytest.raises(ValueError, match="col_idx"):
+        A.pattern(np.empty(s.n_dof + 1, dtype=np.int64), np.empty(s.nnz, dtype=np.int64))
+    torch = pytest.importorskip("torch")
+    with pytest.raises(ValueError, match="dtype"):
+        A.apply(ctrl, young, 0.3, torch.zeros(s.n_dof, dtype=torch.float32), np.empty(s.n_dof))
+
+
 def test_topology_errors():
     from paper_2107_09568_b200 import Assembler, IgaError
     from synth import make_config

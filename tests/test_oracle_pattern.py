@@ -127,3 +127,27 @@ def test_lattice_interfaces_and_no_hub_coupling():
             if np.allclose(prob4.tile[p].ctrl[A], 0.5)] for p in range(6)]
     hub_nodes = {dm4.node[0, dm4.offsets[p] + A] for p in range(6) for (_, A) in hub[p]}
     assert len(hub_nodes) == 3
+
+
+def test_block_map_and_scatter_by_tile_ranges(oracle_problem):
+    """block_map(tiles) is block_map()'s rows of those tiles; scatter over consecutive tile
+    ranges into one array (out=, bmap=) equals the single scatter bit for bit (the
+    accumulation order t, row is kept) — the chunked form the full-size tests use."""
+    from oracle import assemble as As
+    ob = oracle_problem(2)
+    prob, pt, tabs = ob["prob"], ob["pattern"], ob["tabs"]
+    nr = pt.n_rows_tile
+    bm = pt.block_map()
+    assert np.array_equal(pt.block_map(range(10, 17)), bm[10 * nr:17 * nr])
+    local = As.local_lookup(prob, tabs, prob.macro.ctrl, range(prob.n_tiles))
+    whole = As.scatter(prob, pt, local)
+    acc = np.zeros(pt.nnz)
+    for t0 in range(0, prob.n_tiles, 24):
+        ts = np.arange(t0, min(prob.n_tiles, t0 + 24))
+        As.scatter(prob, pt, local[ts], tiles=ts, out=acc, bmap=pt.block_map(ts))
+    assert np.array_equal(acc, whole)
+    # disjoint node ranges filled apart add up to the same array, bit for bit
+    parts = np.zeros(pt.nnz)
+    for n0, n1 in [(0, 1000), (1000, 3001), (3001, ob["dm"].n_nodes)]:
+        As.scatter(prob, pt, local, out=parts, nodes=(n0, n1))
+    assert np.array_equal(parts, whole)

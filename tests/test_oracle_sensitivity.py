@@ -63,3 +63,15 @@ def test_linearity_in_u(case):
     ob, u, v, g = case
     g2 = S.sensitivity(ob["prob"], ob["tabs"], ob["pattern"], 2.5 * u, v)
     assert np.allclose(g2, 2.5 * g, rtol=1e-12, atol=1e-12 * np.abs(g).max())
+
+
+def test_batched_complex_step_equals_entrywise(case):
+    """`sensitivity` evaluates the complex-step perturbations of one tile as a batch
+    (macro.tile_coefficients_batch); the entry-by-entry evaluation gives the same values."""
+    ob, u, v, g = case
+    prob = ob["prob"]
+    rng = np.random.default_rng(11)
+    ent = [(int(k), int(a)) for k, a in zip(rng.integers(0, len(g), 6), rng.integers(0, prob.d, 6))]
+    ref = S.sensitivity_entrywise(prob, ob["tabs"], ob["pattern"], u, v, ent)
+    for k, a in ent:
+        assert abs(g[k, a] - ref[k, a]) <= 1e-14 * np.abs(g).max(), (k, a)
