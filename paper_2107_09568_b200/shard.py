@@ -16,7 +16,12 @@ def allreduce_grad(grad, world: int):
     data-path collective of the sharded step (NCCL on GPUs, gloo on CPU tensors)."""
     if world > 1:
         import torch.distributed as dist
-        dist.all_reduce(grad, op=dist.ReduceOp.SUM)
+        if grad.is_cuda and dist.get_backend() == "gloo":   # gloo: through a host copy
+            h = grad.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM)
+            grad.copy_(h)
+        else:
+            dist.all_reduce(grad, op=dist.ReduceOp.SUM)
     return grad
 
 
