@@ -1,0 +1,3 @@
+timeout 60 python microbench/time_kernels.py --config 5 --reps 1 > gpurun_out/plain9.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k3p_contract -s 2 -c 1 -o gpurun_out/k3p_v3 python microbench/time_kernels.py --config 5 --reps 1 > gpurun_out/ncu9.log 2>&1
+echo done $?

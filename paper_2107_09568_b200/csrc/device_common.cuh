@@ -178,6 +178,28 @@ __device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t 
                : "memory");
 }
 
+// L2 cache policies (createpolicy) for bulk copies and stores
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *smem, const void *gmem, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_hint(double *p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // Fragment-major ("FM") operand layout of an R×K matrix for mma.m8n8k4:
 // chunks of BR rows × 16 columns are contiguous (BR*16 doubles, ordered [row block][k
 // chunk]); inside a chunk, 8-row group g and 4-column step kk hold the 32 values a warp

@@ -194,7 +194,11 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   auto produce = [&](int kc) {
     const int st = kc % K3_STAGES;
     mbar_expect_tx(&full[st], (K3_A_CHUNK + K3_B_CHUNK) * 8);
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS   // keep the re-read table in L2 against the CSR store stream
+    bulk_g2s_hint(sA + st * K3_A_CHUNK, gA + (int64_t)kc * K3_A_CHUNK, K3_A_CHUNK * 8, &full[st], l2_policy_evict_last());
+#else
     bulk_g2s(sA + st * K3_A_CHUNK, gA + (int64_t)kc * K3_A_CHUNK, K3_A_CHUNK * 8, &full[st]);
+#endif
     bulk_g2s(sB + st * K3_B_CHUNK, gB + (int64_t)kc * K3_B_CHUNK, K3_B_CHUNK * 8, &full[st]);
   };
   if (tid == 0)
@@ -402,7 +406,11 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
         for (int idx = 0; idx < D; ++idx) {
           int ra = transposed ? c : idx, cb = transposed ? idx : c;
           if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS   // CSR values are written once: evict them first
+          st_hint(out + ob + (int64_t)idx * sstr + c, sC[sb * K3_CROW + tl * DD + ra * D + cb], l2_policy_evict_first());
+#else
           out[ob + (int64_t)idx * sstr + c] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+#endif
         }
       }
     }
@@ -436,6 +444,332 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
 #endif
   }
 }
+
+#ifdef IGA_EXPERIMENT_K3P
+// ---------------------------------------------------------------------------------
+// K3p: the persistent, warp-specialised K3 with the fused CSR scatter (EPI 1, the hot path).
+// One CTA per SM walks the 64-row × 72-column output tiles L = blockIdx.x + i·gridDim.x
+// (row blocks fastest, as K3's grid).  Its 12 MMA warps form 3 groups of 4 (one warp of
+// each group per SM sub-partition); group g takes the tiles i ≡ g (mod 3) through its own
+// 3-stage bulk-copy ring (the last of its warps to release a stage refills it with the
+// group's next chunk, across tile boundaries) — three independent rings per SM, like three
+// co-resident K3 CTAs, so the groups drift apart in phase and the DMMA pipe does not wait
+// on one hand-off.  At the end of a tile a group stages it in shared memory (L_t[a][b], as
+// K3) into staging slot i % 2 and goes on with its next tile; 8 store warps scatter the
+// staged tiles in the order i (K3's cooperative CSR row-segment stores, side slots for
+// shared blocks), with the maps of the next tile loaded while they wait for it.  Register
+// split by setmaxnreg: MMA warpgroups 128 registers per thread, store warpgroups 64.
+// Hand-off per slot: mbarriers `slot_full` (the 128 threads of a group) and `slot_free`
+// (the 256 store threads); tiles are handed off in the order i.
+constexpr int K3P_GROUPS = 3, K3P_GW = 4;                            // MMA groups, warps per group
+constexpr int K3P_MMA_WARPS = K3P_GROUPS * K3P_GW, K3P_STORE_WARPS = 8;
+constexpr int K3P_THREADS = 32 * (K3P_MMA_WARPS + K3P_STORE_WARPS);
+constexpr int K3P_MMA_REGS = 120, K3P_STORE_REGS = 56;
+static_assert(K3P_MMA_WARPS % 4 == 0 && K3P_STORE_WARPS % 4 == 0, "setmaxnreg acts per warpgroup");
+// setmaxnreg only redistributes the CTA's launch allocation (65536 / threads, rounded down to 8)
+static_assert(K3P_MMA_WARPS * K3P_MMA_REGS + K3P_STORE_WARPS * K3P_STORE_REGS <=
+                  (K3P_MMA_WARPS + K3P_STORE_WARPS) * (65536 / K3P_THREADS / 8 * 8), "register file");
+constexpr int K3P_BM = 16 * K3P_GW;                                  // 64 rows = one FM row block
+constexpr int K3P_STAGES = 3, K3P_SLOTS = 2;
+constexpr int K3P_A_CHUNK = K3P_BM * BK, K3P_B_CHUNK = BN * BK;     // doubles
+constexpr int K3P_STAGE = K3P_A_CHUNK + K3P_B_CHUNK;
+constexpr size_t K3P_RING = sizeof(double) * (size_t)K3P_GROUPS * K3P_STAGES * K3P_STAGE;
+constexpr size_t K3P_STAGING = sizeof(double) * (size_t)K3P_SLOTS * K3P_BM * K3_CROW;
+constexpr size_t K3P_OFF_BAR = K3P_RING + K3P_STAGING;
+constexpr int K3P_BATCHES = 4;                                       // ring of fetched tile batches
+constexpr size_t K3P_SMEM = K3P_OFF_BAR + (K3P_GROUPS * K3P_STAGES + 2 * K3P_SLOTS) * sizeof(uint64_t) +
+                            (K3P_GROUPS * K3P_STAGES + 2 * K3P_BATCHES) * sizeof(int);
+static_assert(K3P_BM == IGA_K3_BM, "a K3p tile is one 64-row FM row block (tperm is per 64-row block)");
+static_assert(K3P_SMEM <= 227 * 1024, "K3p shared memory");
+
+// what a store warp needs of one (row half, tile) unit, loaded ahead of the staged tile
+template <int SPT>
+struct K3pUnits {
+  int A[2], B[2], At[2], Bt[2], et[2];
+  int32_t em[2][SPT], emt[2][SPT];
+  int64_t riA[2][SPT], riB[2][SPT];
+};
+
+// Dynamic tile scheduling: the CTA takes its tiles in batches of K3P_GROUPS consecutive tiles
+// from a global counter (items 3b, 3b+1, 3b+2 of the CTA = tiles L0, L0+1, L0+2), so that
+// all SMs work on neighbouring tiles at any time (as the hardware block scheduler would):
+// the CSR rows of a tile are then written within a short window and merge in L2, and the
+// table and coefficient chunks stay L2-resident.  Batch b lives in slot b % 4 of a smem
+// ring; whoever needs it first claims the slot (it held batch b-4, which nobody needs any
+// more: the store warps are at most ~7 items behind the groups) and fetches it.
+__device__ __forceinline__ int k3p_batch(int b, int *bseq, int *bL, int *ctr) {
+  volatile int *vs = bseq, *vl = bL;
+  const int slot = b % K3P_BATCHES;
+  for (;;) {
+    const int cur = vs[slot];
+    if (cur == b) {
+      __threadfence_block();
+      return vl[slot];
+    }
+    if (cur == b - K3P_BATCHES && atomicCAS(&bseq[slot], cur, -(1 << 30) - b) == cur) {   // claim and fetch
+      const int L0 = atomicAdd(ctr, K3P_GROUPS);
+      vl[slot] = L0;
+      __threadfence_block();
+      atomicExch(&bseq[slot], b);
+      return L0;
+    }
+    __nanosleep(32);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(K3P_THREADS, 1)
+k3p_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int ksplit,
+             int64_t M, int n_mb, int n_work, int64_t n_tiles, double *__restrict__ out,
+             const int32_t *__restrict__ pairA, const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap,
+             const int64_t *__restrict__ rowinfo, int nl, double *__restrict__ side,
+             const uint8_t *__restrict__ tperm, int *__restrict__ work_ctr) {
+  constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, NE = D == 3 ? 9 : 8;
+  constexpr int NP1 = D * (D + 1) / 2, NH = TPC / 8, SPT = TPC / K3P_STORE_WARPS;
+  extern __shared__ __align__(128) double smem[];
+  double *staging = smem + K3P_RING / sizeof(double);
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K3P_OFF_BAR);  // [group][stage]
+  uint64_t *slot_full = full + K3P_GROUPS * K3P_STAGES, *slot_free = slot_full + K3P_SLOTS;
+  int *released = reinterpret_cast<int *>(slot_free + K3P_SLOTS);                           // [group][stage]
+  int *bseq = released + K3P_GROUPS * K3P_STAGES, *bL = bseq + K3P_BATCHES;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // tile of the CTA's item i (-1: none left); one lane asks, the warp shares the answer
+  auto tile_of = [&](int i) -> int {
+    int L = 0;
+    if (lane == 0) {
+      L = k3p_batch(i / K3P_GROUPS, bseq, bL, work_ctr) + i % K3P_GROUPS;
+      if (L >= n_work) L = -1;
+    }
+    return __shfl_sync(0xffffffffu, L, 0);
+  };
+  if (tid == 0) {
+    for (int b = 0; b < K3P_BATCHES; ++b) bseq[b] = b - K3P_BATCHES;   // "holds batch b-4": free
+    for (int s = 0; s < K3P_GROUPS * K3P_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    for (int s = 0; s < K3P_SLOTS; ++s) {
+      mbar_init(&slot_full[s], 32 * K3P_GW);
+      mbar_init(&slot_free[s], 32 * K3P_STORE_WARPS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp < K3P_MMA_WARPS) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(K3P_MMA_REGS));
+    // ---------------- MMA group grp: rows [16·lw, 16·lw + 16) of its tiles i ≡ grp (mod 3) ----
+    const int grp = warp / K3P_GW, lw = warp % K3P_GW;
+    double *sA = smem + grp * K3P_STAGES * K3P_STAGE;
+    uint64_t *gfull = full + grp * K3P_STAGES;
+    int *grel = released + grp * K3P_STAGES;
+    // operand chunk 0 of a tile L
+    auto bases = [&](int L, const double *&ga, const double *&gb) {
+      const int mb = L % n_mb, nb = L / n_mb;
+      ga = tabA + (int64_t)mb * nkc * K3P_A_CHUNK;
+      gb = coef + (int64_t)nb * nkc * K3P_B_CHUNK;
+    };
+    auto produce = [&](const double *ga, const double *gb, int kc, int st) {
+      double *a = sA + st * K3P_STAGE;
+      mbar_expect_tx(&gfull[st], (uint32_t)(K3P_STAGE * 8));
+      bulk_g2s(a, ga + (int64_t)kc * K3P_A_CHUNK, K3P_A_CHUNK * 8, &gfull[st]);
+      bulk_g2s(a + K3P_A_CHUNK, gb + (int64_t)kc * K3P_B_CHUNK, K3P_B_CHUNK * 8, &gfull[st]);
+    };
+    // the group's k-th item is i = grp + 3k; the ring runs K3P_STAGES chunks ahead: (pk, pkc)
+    int pk = 0, pkc = 0;
+    const double *pga = nullptr, *pgb = nullptr;
+    int pL = tile_of(grp);
+    if (pL >= 0) bases(pL, pga, pgb);
+    for (int st = 0; st < K3P_STAGES && pL >= 0; ++st) {   // prologue: the first K3P_STAGES chunks
+      if (warp % K3P_GW == 0 && lane == 0) produce(pga, pgb, pkc, st);
+      if (++pkc == nkc) {
+        pkc = 0;
+        ++pk;
+        pL = tile_of(grp + K3P_GROUPS * pk);
+        if (pL >= 0) bases(pL, pga, pgb);
+      }
+    }
+    const int fr = lane >> 2, fc = lane & 3;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int k = 0;; ++k) {
+      const int i = grp + K3P_GROUPS * k;
+      const int L = tile_of(i);
+      if (L < 0) break;
+      const int mb = L % n_mb;
+      const int64_t wr0 = (int64_t)mb * K3P_BM + lw * 16;
+      const int nmi = wr0 >= M ? 0 : (wr0 + 8 < M ? 2 : 1);
+      double acc[MI][NI][2];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int kc = 0; kc < nkc; ++kc) {
+        mbar_wait(&gfull[st], ph);
+        const double *a_st = sA + st * K3P_STAGE, *b_st = a_st + K3P_A_CHUNK;
+        const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), jj = max(0, min(ksplit - s0, ns));
+        if (nmi == 2) k3_chunk<2, NE>(a_st, b_st, lw * 2, lane, ns, jj, acc);
+        else if (nmi == 1) k3_chunk<1, NE>(a_st, b_st, lw * 2, lane, ns, jj, acc);
+        __syncwarp();
+        if (lane == 0) {   // the last warp of the group to release a stage refills it
+          __threadfence_block();
+          if (atomicAdd(&grel[st], 1) == K3P_GW - 1) {
+            grel[st] = 0;
+            __threadfence_block();
+            if (pL >= 0) produce(pga, pgb, pkc, st);
+          }
+        }
+        if (++pkc == nkc) {
+          pkc = 0;
+          ++pk;
+          if (pL >= 0) {
+            pL = tile_of(grp + K3P_GROUPS * pk);
+            if (pL >= 0) bases(pL, pga, pgb);
+          }
+        }
+        if (++st == K3P_STAGES) { st = 0; ph ^= 1u; }
+      }
+      // hand the tile to the store warps through staging slot i % 2, in the order i: first
+      // item i-1 must have been handed off (its slot_full phase; a parity wait is exact here
+      // because this group itself handed off i-3 on that slot), then the store warps must be
+      // done with item i-2 (slot_free; they finished i-4 before i-2 could be handed off)
+      const int slot = i % K3P_SLOTS;
+      if (i >= 1) mbar_wait(&slot_full[(i - 1) % K3P_SLOTS], (uint32_t)(((i - 1) / K3P_SLOTS) & 1));
+      if (i >= K3P_SLOTS) mbar_wait(&slot_free[slot], (uint32_t)((i / K3P_SLOTS - 1) & 1));
+      double *sC = staging + slot * (K3P_BM * K3_CROW);
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const int rr = lw * 16 + mi * 8 + fr;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int tl = hh * 8 + 2 * fc + e;
+#pragma unroll
+            for (int ab = 0; ab < DD; ++ab) {
+              const int a = ab / D, b = ab % D, lo = a < b ? a : b, hi = a < b ? b : a;
+              const double sp = acc[mi][sym_index(D, lo, hi) * NH + hh][e];
+              double v = sp;
+              if (a != b) {
+                const double am = acc[mi][(NP1 + anti_index(D, lo, hi)) * NH + hh][e];
+                v = a < b ? sp + am : sp - am;
+              }
+              sC[rr * K3_CROW + tl * DD + ab] = v;
+            }
+          }
+      }
+      mbar_arrive(&slot_full[slot]);
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(K3P_STORE_REGS));
+  // ---------------- store warps: tiles tl = sw + 8k of every tile item, both 32-row halves ----
+  const int sw = warp - K3P_MMA_WARPS;
+  auto load_item = [&](int L, K3pUnits<SPT> &u) {
+    const int mb = L % n_mb, nb = L / n_mb;
+    const int64_t m0 = (int64_t)mb * K3P_BM, t0 = (int64_t)nb * TPC;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = h * 32 + lane;
+      const int64_t r = m0 + e;
+      const bool live = r < M;
+      u.et[h] = live ? tperm[r] : e;
+      const int64_t rt = m0 + u.et[h];
+      const bool live_t = live && rt < M;
+      u.A[h] = live ? pairA[r] : -1;
+      u.B[h] = live ? pairB[r] : 0;
+      u.At[h] = live_t ? pairA[rt] : -1;
+      u.Bt[h] = live_t ? pairB[rt] : 0;
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        const int64_t t = min(t0 + sw + K3P_STORE_WARPS * k, n_tiles - 1);
+        u.em[h][k] = live ? emap[t * M + r] : 0;
+        u.riA[h][k] = live ? rowinfo[t * nl + u.A[h]] : 0;
+        u.emt[h][k] = live_t ? emap[t * M + rt] : 0;
+        u.riB[h][k] = live_t ? rowinfo[t * nl + u.Bt[h]] : 0;
+      }
+    }
+  };
+  K3pUnits<SPT> u;
+  int L = tile_of(0);
+  if (L >= 0) load_item(L, u);
+  for (int i = 0; L >= 0; ++i) {
+    const int nb = L / n_mb;
+    const int64_t t0 = (int64_t)nb * TPC;
+    const int slot = i % K3P_SLOTS;
+    const double *sC = staging + slot * (K3P_BM * K3_CROW);
+    auto coop = [&](int64_t o, int str, int pk, int tl, bool transposed) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const int w = 32 * j + lane, src = w / D, c = w - src * D;
+        const int64_t ob = __shfl_sync(0xffffffffu, o, src);
+        const int sstr = __shfl_sync(0xffffffffu, str, src);
+        const int p = __shfl_sync(0xffffffffu, pk, src);
+        if (ob >= 0) {
+          const int sb = p & 0xff;
+          const bool db = (p >> 8) & 1;
+#pragma unroll
+          for (int idx = 0; idx < D; ++idx) {
+            int ra = transposed ? c : idx, cb = transposed ? idx : c;
+            if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+            out[ob + (int64_t)idx * sstr + c] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+          }
+        }
+      }
+    };
+    mbar_wait(&slot_full[slot], (uint32_t)((i / K3P_SLOTS) & 1));
+#ifndef IGA_EXPERIMENT_K3P_NO_STORE   // (timing only, wrong K: the main loop and the hand-off without the scatter)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = h * 32 + lane;
+      const bool live = u.A[h] >= 0, live_t = u.At[h] >= 0;
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        const int tl = sw + K3P_STORE_WARPS * k;
+        if (t0 + tl >= n_tiles) break;   // warp-uniform
+        const int32_t ev = u.em[h][k];
+        if (live && ev < 0) {   // one of several contributions: side slot, summed by K4
+          const double *Lr = sC + e * K3_CROW + tl * DD;
+          double *o = side + (int64_t)(-ev - 1) * DD;
+#pragma unroll
+          for (int q = 0; q < DD; ++q) o[q] = Lr[q];
+        }
+        const int64_t ri = u.riA[h][k];
+        const bool w1 = live && ev >= 0 && ri >= 0;   // ri < 0: row of another shard
+        coop(w1 ? DD * (ri >> 24) + D * (ev & 0xffff) : -1, D * (int)(ri & 0xffffff),
+             e | (u.A[h] == u.B[h] ? 256 : 0), tl, false);
+        const int32_t evt = u.emt[h][k];
+        const int64_t rj = u.riB[h][k];
+        const bool w2 = live_t && evt >= 0 && u.At[h] != u.Bt[h] && rj >= 0;
+        coop(w2 ? DD * (rj >> 24) + D * (evt >> 16) : -1, D * (int)(rj & 0xffffff), u.et[h], tl, true);
+      }
+    }
+#endif
+    mbar_arrive(&slot_free[slot]);
+    L = tile_of(i + 1);
+    if (L >= 0) load_item(L, u);   // in flight while the next tile is computed / staged
+  }
+}
+
+template <int D>
+static cudaError_t launch_k3p(const Handle &h, double *out, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k3p_contract<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3P_SMEM);
+  if (e) return e;
+  int dev = 0, nsm = 148;
+  if ((e = cudaGetDevice(&dev)) || (e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
+  const int64_t n_mb = h.Mpad / K3P_BM;
+  const int64_t n_work = n_mb * (h.Npad / BN);
+  if (n_work >= (1ll << 31)) return cudaErrorInvalidConfiguration;
+  const unsigned grid = (unsigned)std::min<int64_t>((n_work + K3P_GROUPS - 1) / K3P_GROUPS, nsm);
+  if ((e = cudaMemsetAsync(h.d_flag + 3, 0, sizeof(int), s))) return e;   // the tile counter (d_flag[3])
+  k3p_contract<D><<<grid, K3P_THREADS, K3P_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
+                                                      (int)n_mb, (int)n_work, h.n_tiles, out, h.d_pairA, h.d_pairB,
+                                                      h.d_emap, h.d_rowinfo, h.n_local_ctrl, h.d_side, h.d_tperm,
+                                                      h.d_flag + 3);
+  return cudaGetLastError();
+}
+
+#endif  // IGA_EXPERIMENT_K3P
 
 template <int D, int EPI>
 static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, ApplyArgs ap = ApplyArgs{}) {
@@ -507,7 +841,11 @@ cudaError_t launch_apply(const Handle &h, const double *u, double *y, cudaStream
 
 cudaError_t launch_contraction(const Handle &h, double *vals, double *local, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
+#ifdef IGA_EXPERIMENT_K3P   // the persistent warp-specialised K3 (profiles/r02_k3p_experiment.md)
+  if (vals) e = h.d == 2 ? launch_k3p<2>(h, vals, s) : launch_k3p<3>(h, vals, s);
+#else
   if (vals) e = h.d == 2 ? launch_k3<2, 1>(h, vals, s) : launch_k3<3, 1>(h, vals, s);
+#endif
   if (e) return e;
   if (local) e = h.d == 2 ? launch_k3<2, 0>(h, local, s) : launch_k3<3, 0>(h, local, s);
   return e;
