@@ -52,7 +52,6 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
       !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
       !up((void **)&h.d_tperm, h.tperm.data(), h.tperm.size()) ||
-      !up((void **)&h.d_tperm_p, h.tperm_p.data(), h.tperm_p.size()) ||
       !up((void **)&h.d_g1len, h.g1len.data(), h.g1len.size() * 2) ||
       !up((void **)&h.d_g2len, h.g2len.data(), h.g2len.size() * 2) ||
       !up((void **)&h.d_g1slot, h.g1slot.data(), h.g1slot.size() * 4) ||
@@ -610,9 +609,8 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   }
   if (h.max_patch_ctrl >= 32768) { set_error("tile patch with >= 32768 control points"); return IGA_ELIMIT; }
   h.Kp = h.pcol[n_patches];
-  // K3 epilogue, transposed pass: within each row block (64 rows: K3; IGA_K3P_BM rows: the
-  // persistent K3), rows ordered by (B, A) so that neighbouring threads write neighbouring
-  // blocks of CSR row node(B)
+  // K3 epilogue, transposed pass: within each 64-row block, rows ordered by (B, A) so that
+  // neighbouring threads write neighbouring blocks of CSR row node(B)
   auto block_perm = [&](std::vector<uint8_t> &perm, int BMb, int64_t rows) {
     perm.assign(rows, 0);
     for (int64_t m0 = 0; m0 < rows; m0 += BMb) {
@@ -626,9 +624,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       for (int k = 0; k < BMb; ++k) perm[m0 + k] = (uint8_t)idx[k];
     }
   };
-  static_assert(IGA_K3P_BM <= 256, "uint8 row permutation");
   block_perm(h.tperm, IGA_K3_BM, h.Mpad);
-  block_perm(h.tperm_p, IGA_K3P_BM, (h.M + IGA_K3P_BM - 1) / IGA_K3P_BM * IGA_K3P_BM);
   // matrix-free apply maps (tile-independent, NEXT N1)
   {
     h.g1len.assign(h.Mpad, 0);

@@ -15,7 +15,6 @@
 #ifndef IGA_K3_BM
 #define IGA_K3_BM 64        // K3 CTA rows (table rows): 4 MMA warps, 4 CTAs per SM
 #endif
-#define IGA_K3P_BM 192      // persistent K3 CTA rows: 12 MMA warps (3 per SM sub-partition) + 4 store warps
 #define IGA_K5_BM 256       // K5a CTA rows (κ): 16 MMA warps, all κ rows of a 3D q = 2 problem in one CTA
 #define IGA_GEMM_BN 72      // K3/K5a CTA columns (tiles × d²): 8 tiles in 3D, 18 in 2D
 
@@ -128,7 +127,6 @@ struct Handle {
   std::vector<int32_t> k5_pair;      // [Kp] patch-local (A | B << 16), -1 = padding
   std::vector<int32_t> k5_col;       // [M] padded column of each table row
   std::vector<uint8_t> tperm;        // [Mpad] K3 transposed-pass row order within each 64-row block
-  std::vector<uint8_t> tperm_p;      // the same within each IGA_K3P_BM-row block (persistent K3)
   // matrix-free apply (NEXT N1, Eq. 74): per 128-row block, runs of rows with equal A (row
   // order) and equal B (tperm order) are summed into one partial slot each (tile-independent)
   int64_t P = 0;                     // partial slots per tile
@@ -169,7 +167,6 @@ struct Handle {
   int32_t *d_k5_pair = nullptr;
   int32_t *d_k5_col = nullptr;   // [M]
   uint8_t *d_tperm = nullptr;    // [Mpad]
-  uint8_t *d_tperm_p = nullptr;  // [n_mb_p * IGA_K3P_BM] persistent K3: (B, A) order within each 192-row block
   uint16_t *d_g1len = nullptr, *d_g2len = nullptr;
   int32_t *d_g1slot = nullptr, *d_g2slot = nullptr, *d_sA_ptr = nullptr, *d_sA_slot = nullptr, *d_inv_ent = nullptr;
   int64_t *d_inv_ptr = nullptr;
