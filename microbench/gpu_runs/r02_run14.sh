@@ -1,0 +1,3 @@
+for lib in paper_2107_09568_b200/libiga.so microbench/libiga_IGA_EXPERIMENT_K5G_NO_GEN_MATH.so microbench/libiga_IGA_EXPERIMENT_K5G_NO_TABLE_REFILL.so; do
+  IGA_LIB=$lib timeout 60 python microbench/time_kernels.py --config 5 --reps 5
+done

@@ -52,6 +52,7 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
       !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
       !up((void **)&h.d_tperm, h.tperm.data(), h.tperm.size()) ||
+      !up((void **)&h.d_rowdesc, h.rowdesc.data(), h.rowdesc.size() * sizeof(int4)) ||
       !up((void **)&h.d_g1len, h.g1len.data(), h.g1len.size() * 2) ||
       !up((void **)&h.d_g2len, h.g2len.data(), h.g2len.size() * 2) ||
       !up((void **)&h.d_g1slot, h.g1slot.data(), h.g1slot.size() * 4) ||
@@ -625,6 +626,15 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     }
   };
   block_perm(h.tperm, IGA_K3_BM, h.Mpad);
+  // per-row scatter descriptor (row pair and its (B, A)-order partner), one 16-byte load
+  h.rowdesc.assign(h.Mpad, int4{-1, -1, 0, 0});
+  for (int64_t r = 0; r < h.Mpad; ++r) {
+    const int64_t m0 = r / IGA_K3_BM * IGA_K3_BM, rt = m0 + h.tperm[r];
+    int4 &q = h.rowdesc[r];
+    q.z = h.tperm[r];
+    if (r < h.M) q.x = h.pairA[r] | (h.pairB[r] << 16);
+    if (rt < h.M) q.y = h.pairA[rt] | (h.pairB[rt] << 16);
+  }
   // matrix-free apply maps (tile-independent, NEXT N1)
   {
     h.g1len.assign(h.Mpad, 0);

@@ -127,6 +127,7 @@ struct Handle {
   std::vector<int32_t> k5_pair;      // [Kp] patch-local (A | B << 16), -1 = padding
   std::vector<int32_t> k5_col;       // [M] padded column of each table row
   std::vector<uint8_t> tperm;        // [Mpad] K3 transposed-pass row order within each 64-row block
+  std::vector<int4> rowdesc;         // [Mpad] (see d_rowdesc)
   // matrix-free apply (NEXT N1, Eq. 74): per 128-row block, runs of rows with equal A (row
   // order) and equal B (tperm order) are summed into one partial slot each (tile-independent)
   int64_t P = 0;                     // partial slots per tile
@@ -167,6 +168,7 @@ struct Handle {
   int32_t *d_k5_pair = nullptr;
   int32_t *d_k5_col = nullptr;   // [M]
   uint8_t *d_tperm = nullptr;    // [Mpad]
+  int4 *d_rowdesc = nullptr;     // [Mpad] K3p store warps: {A | B << 16, At | Bt << 16, tperm, 0} (A = -1: padding)
   uint16_t *d_g1len = nullptr, *d_g2len = nullptr;
   int32_t *d_g1slot = nullptr, *d_g2slot = nullptr, *d_sA_ptr = nullptr, *d_sA_slot = nullptr, *d_inv_ent = nullptr;
   int64_t *d_inv_ptr = nullptr;

@@ -393,26 +393,44 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   // column w%D, and the D row segments of a block are o, o + stride, ...: one set of
   // shuffles per block serves its D rows; value L[ra][cb] of that lane's block
   auto coop = [&](int64_t o, int str, int pk, int tl, bool transposed) {
+    // all shuffles, then all shared loads, then the predicated stores (CSR values are written once:
+    // L2 evict-first)
+    int64_t ob[D];
+    int sstr[D], p[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      const int w = 32 * j + lane, src = w / D, c = w - src * D;
-      const int64_t ob = __shfl_sync(0xffffffffu, o, src);
-      const int sstr = __shfl_sync(0xffffffffu, str, src);
-      const int p = __shfl_sync(0xffffffffu, pk, src);
-      if (ob >= 0) {
-        const int sb = p & 0xff;
-        const bool db = (p >> 8) & 1;
+      const int src = (32 * j + lane) / D;
+      ob[j] = __shfl_sync(0xffffffffu, o, src);
+      sstr[j] = __shfl_sync(0xffffffffu, str, src);
+      p[j] = __shfl_sync(0xffffffffu, pk, src);
+    }
+    double v[D][D];
 #pragma unroll
-        for (int idx = 0; idx < D; ++idx) {
-          int ra = transposed ? c : idx, cb = transposed ? idx : c;
-          if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
-#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS   // CSR values are written once: evict them first
-          st_hint(out + ob + (int64_t)idx * sstr + c, sC[sb * K3_CROW + tl * DD + ra * D + cb], l2_policy_evict_first());
+    for (int j = 0; j < D; ++j) {
+      const int c = (32 * j + lane) % D, sb = p[j] & 0xff;
+      const bool db = (p[j] >> 8) & 1;
+#pragma unroll
+      for (int idx = 0; idx < D; ++idx) {
+        int ra = transposed ? c : idx, cb = transposed ? idx : c;
+        if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+        v[j][idx] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+      }
+    }
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+    const uint64_t pol = l2_policy_evict_first();
+#endif
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int c = (32 * j + lane) % D;
+#pragma unroll
+      for (int idx = 0; idx < D; ++idx)
+        if (ob[j] >= 0) {
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+          st_hint(out + ob[j] + (int64_t)idx * sstr[j] + c, v[j][idx], pol);
 #else
-          out[ob + (int64_t)idx * sstr + c] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+          out[ob[j] + (int64_t)idx * sstr[j] + c] = v[j][idx];
 #endif
         }
-      }
     }
   };
 #pragma unroll
@@ -523,7 +541,7 @@ k3p_contract(const double *__restrict__ tabA, const double *__restrict__ coef, i
              int64_t M, int n_mb, int n_work, int64_t n_tiles, double *__restrict__ out,
              const int32_t *__restrict__ pairA, const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap,
              const int64_t *__restrict__ rowinfo, int nl, double *__restrict__ side,
-             const uint8_t *__restrict__ tperm, int *__restrict__ work_ctr) {
+             const int4 *__restrict__ rowdesc, int *__restrict__ work_ctr) {
   constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, NE = D == 3 ? 9 : 8;
   constexpr int NP1 = D * (D + 1) / 2, NH = TPC / 8, SPT = TPC / K3P_STORE_WARPS;
   extern __shared__ __align__(128) double smem[];
@@ -669,30 +687,38 @@ k3p_contract(const double *__restrict__ tabA, const double *__restrict__ coef, i
     const int mb = L % n_mb, nb = L / n_mb;
     const int64_t m0 = (int64_t)mb * K3P_BM, t0 = (int64_t)nb * TPC;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < 2; ++h) {   // one 16-byte descriptor per row: no dependent load chain
       const int e = h * 32 + lane;
-      const int64_t r = m0 + e;
-      const bool live = r < M;
-      u.et[h] = live ? tperm[r] : e;
-      const int64_t rt = m0 + u.et[h];
-      const bool live_t = live && rt < M;
-      u.A[h] = live ? pairA[r] : -1;
-      u.B[h] = live ? pairB[r] : 0;
-      u.At[h] = live_t ? pairA[rt] : -1;
-      u.Bt[h] = live_t ? pairB[rt] : 0;
+      const int4 q = rowdesc[m0 + e];
+      u.et[h] = q.z;
+      u.A[h] = q.x < 0 ? -1 : (q.x & 0xffff);
+      u.B[h] = q.x < 0 ? 0 : (q.x >> 16);
+      u.At[h] = q.y < 0 ? -1 : (q.y & 0xffff);
+      u.Bt[h] = q.y < 0 ? 0 : (q.y >> 16);
+      const int64_t r = m0 + e, rt = m0 + q.z;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         const int64_t t = min(t0 + sw + K3P_STORE_WARPS * k, n_tiles - 1);
-        u.em[h][k] = live ? emap[t * M + r] : 0;
-        u.riA[h][k] = live ? rowinfo[t * nl + u.A[h]] : 0;
-        u.emt[h][k] = live_t ? emap[t * M + rt] : 0;
-        u.riB[h][k] = live_t ? rowinfo[t * nl + u.Bt[h]] : 0;
+        u.em[h][k] = q.x >= 0 ? emap[t * M + r] : 0;
+        u.riA[h][k] = q.x >= 0 ? rowinfo[t * nl + u.A[h]] : 0;
+        u.emt[h][k] = q.y >= 0 ? emap[t * M + rt] : 0;
+        u.riB[h][k] = q.y >= 0 ? rowinfo[t * nl + u.Bt[h]] : 0;
       }
     }
+  };
+  // warm L2 with the epilogue map rows of a later tile (emap is streamed once from HBM)
+  auto prefetch_item = [&](int L) {
+    const int mb = L % n_mb, nb = L / n_mb;
+    const int64_t t = (int64_t)nb * TPC + sw + K3P_STORE_WARPS * (lane >> 1);
+    if (lane < 2 * SPT && t < n_tiles) prefetch_l2(emap + t * M + (int64_t)mb * K3P_BM + 32 * (lane & 1));
   };
   K3pUnits<SPT> u;
   int L = tile_of(0);
   if (L >= 0) load_item(L, u);
+  {
+    const int L1 = tile_of(1);
+    if (L1 >= 0) prefetch_item(L1);
+  }
   for (int i = 0; L >= 0; ++i) {
     const int nb = L / n_mb;
     const int64_t t0 = (int64_t)nb * TPC;
@@ -747,7 +773,11 @@ k3p_contract(const double *__restrict__ tabA, const double *__restrict__ coef, i
 #endif
     mbar_arrive(&slot_free[slot]);
     L = tile_of(i + 1);
-    if (L >= 0) load_item(L, u);   // in flight while the next tile is computed / staged
+    if (L >= 0) {
+      load_item(L, u);   // in flight while the next tile is computed / staged
+      const int L2 = tile_of(i + 2);
+      if (L2 >= 0) prefetch_item(L2);
+    }
   }
 }
 
@@ -764,7 +794,7 @@ static cudaError_t launch_k3p(const Handle &h, double *out, cudaStream_t s) {
   if ((e = cudaMemsetAsync(h.d_flag + 3, 0, sizeof(int), s))) return e;   // the tile counter (d_flag[3])
   k3p_contract<D><<<grid, K3P_THREADS, K3P_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
                                                       (int)n_mb, (int)n_work, h.n_tiles, out, h.d_pairA, h.d_pairB,
-                                                      h.d_emap, h.d_rowinfo, h.n_local_ctrl, h.d_side, h.d_tperm,
+                                                      h.d_emap, h.d_rowinfo, h.n_local_ctrl, h.d_side, h.d_rowdesc,
                                                       h.d_flag + 3);
   return cudaGetLastError();
 }
@@ -1135,8 +1165,12 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
         released[st] = 0;
         __threadfence_block();
         if (kc + S < nkc) {   // refill: the table chunk by TMA, the X̃ chunk by the generators
+#ifdef IGA_EXPERIMENT_K5G_NO_TABLE_REFILL   // timing only (wrong g): the first S table chunks are reused
+          mbar_arrive(&fullA[st]);
+#else
           mbar_expect_tx(&fullA[st], K5_A_CHUNK * 8);
           bulk_g2s(sA + st * K5_A_CHUNK, gA + (int64_t)(kc + S) * K5_A_CHUNK, K5_A_CHUNK * 8, &fullA[st]);
+#endif
           mbar_arrive(&emptyB[st]);
         }
       }
@@ -1237,6 +1271,10 @@ __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int
           int a = 0, b = 0;
           if (o < NP1) sym_pair(D, o, a, b);
           else anti_pair(D, o - NP1, a, b);
+#ifdef IGA_EXPERIMENT_K5G_NO_GEN_MATH   // timing only (wrong g): no FP64 arithmetic in the generators
+          x[j] = uB[it][b] + vA[it][a];
+          continue;
+#endif
           const double xab = fma(uB[it][b], vA[it][a], uA[it][a] * vB[it][b]);
           if (o < D) x[j] = A == B ? 0.5 * xab : xab;
           else if (A == B) x[j] = xab;
