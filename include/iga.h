@@ -25,8 +25,12 @@
  * the end, so that the device-side degeneracy flag can be reported.
  *
  * Concurrency.  A handle is immutable after iga_build_tables except for its
- * internal workspace; concurrent calls on one handle must be serialised by the
- * caller (different handles are independent).
+ * internal workspace (coefficients, side slots, staging buffers, profiling slots).
+ * Concurrent calls on one handle — from several host threads, on the same or on
+ * different streams — are safe: every entry point that uses the handle holds the
+ * handle's lock until its device work is complete (each call synchronises its
+ * stream before returning), so such calls are serialised, never interleaved.
+ * Different handles are independent and run concurrently.
  */
 #ifndef IGA_H
 #define IGA_H

@@ -178,6 +178,19 @@ __device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t 
                : "memory");
 }
 
+// thread-block cluster barrier halves and distributed shared memory
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+// generic address of the same shared-memory object in the cluster's CTA `rank`
+template <typename T>
+__device__ __forceinline__ T *cluster_map(T *p, int rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;\n" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<T *>(out);
+}
+
 // L2 cache policies (createpolicy) for bulk copies and stores
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
@@ -198,6 +211,9 @@ __device__ __forceinline__ void bulk_g2s_hint(void *smem, const void *gmem, uint
 }
 __device__ __forceinline__ void st_hint(double *p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st2_hint(double *p, double v0, double v1, uint64_t pol) {   // p 16-B aligned
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v0), "d"(v1), "l"(pol) : "memory");
 }
 
 // Fragment-major ("FM") operand layout of an R×K matrix for mma.m8n8k4:

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
 #include <omp.h>
 #include "internal.h"
 
@@ -52,6 +53,7 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
       !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
       !up((void **)&h.d_tperm, h.tperm.data(), h.tperm.size()) ||
+      !up((void **)&h.d_cperm, h.cperm.data(), h.cperm.size() * 2) ||
       !up((void **)&h.d_rowdesc, h.rowdesc.data(), h.rowdesc.size() * sizeof(int4)) ||
       !up((void **)&h.d_g1len, h.g1len.data(), h.g1len.size() * 2) ||
       !up((void **)&h.d_g2len, h.g2len.data(), h.g2len.size() * 2) ||
@@ -600,7 +602,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   }
 
   // ---- operand layouts: K3 A rows, coefficient rows, K5a padded reduction columns --
-  h.Mpad = (h.M + IGA_K3_BM - 1) / IGA_K3_BM * IGA_K3_BM;
+  h.Mpad = (h.M + IGA_K3_BM * IGA_K3_CL - 1) / (IGA_K3_BM * IGA_K3_CL) * (IGA_K3_BM * IGA_K3_CL);
   h.Npad = (lnt + h.tpc - 1) / h.tpc * IGA_GEMM_BN;   // blocks of tpc tiles (sym layout)
   h.pcol.assign(n_patches + 1, 0);
   h.max_patch_ctrl = 0;
@@ -612,7 +614,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   h.Kp = h.pcol[n_patches];
   // K3 epilogue, transposed pass: within each 64-row block, rows ordered by (B, A) so that
   // neighbouring threads write neighbouring blocks of CSR row node(B)
-  auto block_perm = [&](std::vector<uint8_t> &perm, int BMb, int64_t rows) {
+  auto block_perm = [&](auto &perm, int BMb, int64_t rows) {
     perm.assign(rows, 0);
     for (int64_t m0 = 0; m0 < rows; m0 += BMb) {
       std::vector<int> idx(BMb);
@@ -622,10 +624,14 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
         if (rx >= h.M || ry >= h.M) return rx < h.M && ry >= h.M;
         return h.pairB[rx] != h.pairB[ry] ? h.pairB[rx] < h.pairB[ry] : h.pairA[rx] < h.pairA[ry];
       });
-      for (int k = 0; k < BMb; ++k) perm[m0 + k] = (uint8_t)idx[k];
+      for (int k = 0; k < BMb; ++k) perm[m0 + k] = (typename std::decay_t<decltype(perm)>::value_type)idx[k];
     }
   };
   block_perm(h.tperm, IGA_K3_BM, h.Mpad);
+  // clustered K3 (IGA_K3_CL > 1): the transposed pass pools the CL row blocks of a cluster, so
+  // the (J,I) blocks of one CSR row J that come from neighbouring A (neighbouring row blocks)
+  // leave as one run
+  block_perm(h.cperm, IGA_K3_BM * IGA_K3_CL, h.Mpad);
   // per-row scatter descriptor (row pair and its (B, A)-order partner), one 16-byte load
   h.rowdesc.assign(h.Mpad, int4{-1, -1, 0, 0});
   for (int64_t r = 0; r < h.Mpad; ++r) {

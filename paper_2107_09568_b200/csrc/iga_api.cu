@@ -12,7 +12,7 @@ const char *get_error();
 Handle::~Handle() {
   void *bufs[] = {d_table, d_tabA, d_tabAT, d_coef, d_side, d_W, d_X, d_gpart, d_node_map, d_pairA, d_pairB,
                   d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_mperm, d_slot_tr,
-                  d_k5_pair, d_k5_col, d_tperm, d_rowdesc, d_g1len, d_g2len, d_g1slot, d_g2slot, d_sA_ptr, d_sA_slot,
+                  d_k5_pair, d_k5_col, d_tperm, d_cperm, d_rowdesc, d_g1len, d_g2len, d_g1slot, d_g2slot, d_sA_ptr, d_sA_slot,
                   d_inv_ptr, d_inv_ent, d_part, d_ug, d_k5_gphys, d_k5_mode, d_k5_extra, d_Wpart, d_F, d_th, d_det, d_Vt, d_mweights, d_patch_info, d_mknots, d_mspan, d_flag};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -179,7 +179,11 @@ using namespace iga;
 
 struct iga_handle {
   Handle h;
+  std::mutex mu;   // serialises the calls that use the handle's workspace (include/iga.h, Concurrency)
 };
+// every workspace-using entry point holds the handle's lock until its device work is done
+// (each call synchronises its stream before returning)
+#define IGA_LOCK(HP) std::lock_guard<std::mutex> iga_lock_(const_cast<iga_handle *>(HP)->mu)
 
 extern "C" {
 
@@ -398,6 +402,7 @@ iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
 iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const double *young, int32_t young_per_tile,
                         double nu, double *csr_values, double *local_values, void *stream) {
   if (!Hc || !macro_ctrl || (!csr_values && !local_values)) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   iga_status st = check_material(h, young, nu);
@@ -447,6 +452,7 @@ iga_status iga_assemble(const iga_handle *Hc, const double *macro_ctrl, const do
 iga_status iga_apply(const iga_handle *Hc, const double *macro_ctrl, const double *young, int32_t young_per_tile,
                      double nu, const double *u, double *y, void *stream) {
   if (!Hc || !macro_ctrl || !u || !y) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   iga_status st = check_material(h, young, nu);
@@ -490,6 +496,7 @@ iga_status iga_apply(const iga_handle *Hc, const double *macro_ctrl, const doubl
 
 iga_status iga_volume(const iga_handle *Hc, const double *macro_ctrl, double *volume, double *grad, void *stream) {
   if (!Hc || !macro_ctrl || !volume) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
@@ -516,6 +523,7 @@ iga_status iga_volume(const iga_handle *Hc, const double *macro_ctrl, double *vo
 iga_status iga_load_vector(const iga_handle *Hc, const double *macro_ctrl, const double *body_force, double *f,
                            void *stream) {
   if (!Hc || !macro_ctrl || !body_force || !f) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
@@ -539,6 +547,7 @@ iga_status iga_load_vector(const iga_handle *Hc, const double *macro_ctrl, const
 iga_status iga_interpolate(const iga_handle *Hc, const double *macro_ctrl, const double *young, int32_t young_per_tile,
                            double nu, double *coef, void *stream) {
   if (!Hc || !macro_ctrl || !coef) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   iga_status st = check_material(h, young, nu);
@@ -569,6 +578,7 @@ iga_status iga_sensitivity(const iga_handle *Hc, const double *macro_ctrl, const
                            int32_t young_per_tile, double nu, const double *u, const double *v, double *grad,
                            void *stream) {
   if (!Hc || !macro_ctrl || !u || !v || !grad) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   iga_status st = check_material(h, young, nu);
@@ -607,6 +617,7 @@ iga_status iga_assemble_sensitivity(const iga_handle *Hc, const double *macro_ct
                                     int32_t young_per_tile, double nu, const double *u, const double *v,
                                     double *csr_values, double *grad, void *stream) {
   if (!Hc || !macro_ctrl || !u || !v || !grad || !csr_values) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   Handle &h = const_cast<iga_handle *>(Hc)->h;
   if (!h.on_device) { set_error("topology-only handle (iga_build_topology) cannot run kernels"); return IGA_EINVAL; }
   iga_status st = check_material(h, young, nu);
@@ -807,6 +818,7 @@ iga_status iga_select_degree(const iga_spline *macro, double nu, double tol, int
 
 iga_status iga_get_pattern(const iga_handle *Hc, int64_t *row_ptr, int32_t *col_idx) {
   if (!Hc) { set_error("NULL handle"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   const Handle &h = Hc->h;
   if (h.on_device) {
     if (row_ptr) CU(cudaMemcpy(row_ptr, h.d_row_ptr, sizeof(int64_t) * (h.n_nodes * h.d + 1), cudaMemcpyDefault));
@@ -831,6 +843,7 @@ iga_status iga_get_pattern(const iga_handle *Hc, int64_t *row_ptr, int32_t *col_
 
 iga_status iga_get_block_map(const iga_handle *Hc, int64_t t_begin, int64_t t_end, int64_t *out) {
   if (!Hc || !out) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   const Handle &h = Hc->h;
   if (t_begin < 0 || t_end > h.n_tiles || t_begin > t_end) { set_error("bad tile range"); return IGA_EINVAL; }
   const int d = h.d;
@@ -861,6 +874,7 @@ iga_status iga_get_node_map(const iga_handle *Hc, int32_t *out) {
 
 iga_status iga_get_tables(const iga_handle *Hc, double *out) {
   if (!Hc || !out) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   const Handle &h = Hc->h;
   if (!h.on_device) { set_error("topology-only handle has no tables"); return IGA_EINVAL; }
   CU(cudaMemcpy2D(out, sizeof(double) * h.nk, h.d_table, sizeof(double) * h.kstride, sizeof(double) * h.nk, h.M,
@@ -870,6 +884,7 @@ iga_status iga_get_tables(const iga_handle *Hc, double *out) {
 
 iga_status iga_get_pairs(const iga_handle *Hc, int32_t *out) {
   if (!Hc || !out) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(Hc);
   const Handle &h = Hc->h;
   for (int64_t r = 0; r < h.M; ++r) {
     int pa = h.pairA[r], pb = h.pairB[r];
@@ -883,17 +898,20 @@ iga_status iga_get_pairs(const iga_handle *Hc, int32_t *out) {
 
 iga_status iga_set_projection(iga_handle *H, int32_t m) {
   if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
+  IGA_LOCK(H);
   return set_projection(H->h, m);
 }
 
 iga_status iga_get_projection(const iga_handle *H, int32_t *m) {
   if (!H || !m) { set_error("NULL argument"); return IGA_EINVAL; }
+  IGA_LOCK(H);
   *m = H->h.m_proj;
   return IGA_OK;
 }
 
 iga_status iga_set_profiling(iga_handle *H, int32_t enable) {
   if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
+  IGA_LOCK(H);
   H->h.profiling = enable != 0;
   if (enable)
     for (int i = 0; i < IGA_N_PROF; ++i) { H->h.prof_ms[i] = 0; H->h.prof_launches[i] = 0; }
@@ -902,6 +920,7 @@ iga_status iga_set_profiling(iga_handle *H, int32_t enable) {
 
 iga_status iga_get_kernel_times(const iga_handle *H, double *ms_out, int64_t *launches_out) {
   if (!H) { set_error("NULL handle"); return IGA_EINVAL; }
+  IGA_LOCK(H);
   for (int i = 0; i < IGA_N_PROF; ++i) {
     if (ms_out) ms_out[i] = H->h.prof_ms[i];
     if (launches_out) launches_out[i] = H->h.prof_launches[i];

@@ -15,6 +15,13 @@
 #ifndef IGA_K3_BM
 #define IGA_K3_BM 64        // K3 CTA rows (table rows): 4 MMA warps, 4 CTAs per SM
 #endif
+#ifndef IGA_K3_CL
+#ifdef IGA_EXPERIMENT_K3_CLUSTER
+#define IGA_K3_CL 8         // K3 CTAs per thread-block cluster (transposed scatter pass pooled over the cluster)
+#else
+#define IGA_K3_CL 1
+#endif
+#endif
 #define IGA_K5_BM 256       // K5a CTA rows (κ): 16 MMA warps, all κ rows of a 3D q = 2 problem in one CTA
 #define IGA_GEMM_BN 72      // K3/K5a CTA columns (tiles × d²): 8 tiles in 3D, 18 in 2D
 
@@ -95,7 +102,7 @@ struct Handle {
   std::vector<int32_t> mperm;        // [n_multi] multi blocks in (J, I) order (K4 transposed pass)
   std::vector<uint8_t> slot_tr;      // [n_slots] 1 = slot holds the (J,I)-oriented block
   // operand layouts (fragment-major, device_common.cuh fm_index)
-  int64_t Mpad = 0;                  // rows of d_tabA (multiple of IGA_K3_BM)
+  int64_t Mpad = 0;                  // rows of d_tabA (multiple of IGA_K3_BM · IGA_K3_CL)
   int64_t Npad = 0;                  // rows of d_coef / d_X (IGA_GEMM_BN per block of tpc tiles)
   int64_t k5_rows = 0;               // κ rows of d_tabAT (multiple of IGA_K5_BM)
   // Eq. 38-reduced contraction (device_common.cuh sym_index): the GEMM
@@ -127,6 +134,7 @@ struct Handle {
   std::vector<int32_t> k5_pair;      // [Kp] patch-local (A | B << 16), -1 = padding
   std::vector<int32_t> k5_col;       // [M] padded column of each table row
   std::vector<uint8_t> tperm;        // [Mpad] K3 transposed-pass row order within each 64-row block
+  std::vector<uint16_t> cperm;       // [Mpad] the same order within each IGA_K3_CL·64-row cluster block
   std::vector<int4> rowdesc;         // [Mpad] (see d_rowdesc)
   // matrix-free apply (NEXT N1, Eq. 74): per 128-row block, runs of rows with equal A (row
   // order) and equal B (tperm order) are summed into one partial slot each (tile-independent)
@@ -168,6 +176,7 @@ struct Handle {
   int32_t *d_k5_pair = nullptr;
   int32_t *d_k5_col = nullptr;   // [M]
   uint8_t *d_tperm = nullptr;    // [Mpad]
+  uint16_t *d_cperm = nullptr;   // [Mpad]
   int4 *d_rowdesc = nullptr;     // [Mpad] K3p store warps: {A | B << 16, At | Bt << 16, tperm, 0} (A = -1: padding)
   uint16_t *d_g1len = nullptr, *d_g2len = nullptr;
   int32_t *d_g1slot = nullptr, *d_g2slot = nullptr, *d_sA_ptr = nullptr, *d_sA_slot = nullptr, *d_inv_ent = nullptr;

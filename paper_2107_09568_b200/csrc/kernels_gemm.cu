@@ -37,6 +37,8 @@ constexpr int MI = 2;              // 2 DMMA row tiles per warp (16 rows)
 constexpr int N_MMA_WARPS = IGA_K5_BM / 16;                                // K5a: 16
 constexpr int BM = 16 * N_MMA_WARPS;                                        // 256 (K5a κ rows)
 constexpr int K3_BM = IGA_K3_BM, K3_WARPS = K3_BM / 16;                     // K3: 64 rows, 4 MMA warps
+constexpr int K3_CL = IGA_K3_CL;                                            // K3 CTAs per cluster (EPI 3)
+static_assert(K3_CL == 1 || (K3_CL * K3_BM <= 65536 && K3_CL <= 8 && K3_BM == 64), "cluster row blocks: cperm is uint16, pk packs the rank in 3 bits above the row");
 static_assert(K3_BM == 64 || K3_BM == 128, "K3 row blocks: 64 (product) or 128 rows; other shapes are not supported by every epilogue");
 static_assert(BM == IGA_K5_BM, "K5a CTA rows");
 constexpr int K5_X_CHUNK_ = BN * BK;                                        // doubles per X chunk
@@ -116,6 +118,117 @@ __device__ __forceinline__ void store_row(double *p, double x0, double x1, doubl
   }
 }
 
+// one d-double CSR row segment with the L2 evict-first policy (CSR values are written once)
+template <int D>
+__device__ __forceinline__ void store_seg_hint(double *p, const double (&x)[D], uint64_t pol) {
+  const bool al = (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+  if (D == 3) {
+    if (al) {
+      st2_hint(p, x[0], x[1], pol);
+      st_hint(p + 2, x[D - 1], pol);
+    } else {
+      st_hint(p, x[0], pol);
+      st2_hint(p + 1, x[1], x[D - 1], pol);
+    }
+  } else {
+    if (al) {
+      st2_hint(p, x[0], x[1], pol);
+    } else {
+      st_hint(p, x[0], pol);
+      st_hint(p + 1, x[1], pol);
+    }
+  }
+}
+
+// Register-direct fused scatter (R9) of one K3 MMA warp.  The accumulator
+// fragment of lane (fr, fc) = (lane / 4, lane % 4) holds, for rows fr and fr + 8 of the
+// warp's 16 rows and tiles tl = hh·8 + 2fc + e, ALL sym / anti outputs of each (row, tile)
+// block (the sym column tiles of DESIGN §6 are per output component, their columns per
+// tile), so L_t[a][b] = L⁺ ± L⁻ is formed in registers and stored straight to its two CSR
+// positions: K(I,J) = L (diagonal rows: the upper triangle mirrored) and K(J,I) = Lᵀ, or to
+// the block's side slot when several contributions share it (emap < 0, summed by K4).  No
+// shared-memory staging, no CTA barrier and no shuffles: a warp scatters as soon as its own
+// main loop ends, while the other warps of its SM sub-partition keep the DMMA pipe busy.
+template <int D>
+__device__ __forceinline__ void k3_direct_scatter(const double (&acc)[MI][NI][2], int warp, int lane, int64_t m0,
+                                                  int64_t t0, int64_t M, int64_t n_tiles, double *__restrict__ out,
+                                                  const int32_t *__restrict__ pairA, const int32_t *__restrict__ pairB,
+                                                  const int32_t *__restrict__ emap,
+                                                  const int64_t *__restrict__ rowinfo, int nl,
+                                                  double *__restrict__ side) {
+  constexpr int DD = D * D, NP1 = D * (D + 1) / 2, NH = D == 3 ? 1 : 2, NT = 2 * NH;   // NT tiles per lane
+  const int fr = lane >> 2, fc = lane & 3;
+  const uint64_t pol = l2_policy_evict_first();
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    // this row's map loads first (one dependent level: pair → rowinfo)
+    const int64_t r = m0 + warp * 8 * MI + mi * 8 + fr;
+    if (r >= M) break;   // rows of the warp ascend: the rest is padding
+    const int A = pairA[r], B = pairB[r];
+    int32_t ev[NT];
+    int64_t riA[NT], riB[NT];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int tl = (k >> 1) * 8 + 2 * fc + (k & 1);
+      const int64_t t = t0 + tl < n_tiles ? t0 + tl : n_tiles - 1;
+      ev[k] = emap[t * M + r];
+      riA[k] = rowinfo[t * nl + A];
+      riB[k] = rowinfo[t * nl + B];
+    }
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int hh = k >> 1, e = k & 1, tl = hh * 8 + 2 * fc + e;
+      if (t0 + tl >= n_tiles) continue;
+      double L[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          const int lo = a < b ? a : b, hi = a < b ? b : a;
+          const double sp = acc[mi][sym_index(D, lo, hi) * NH + hh][e];
+          if (a == b) {
+            L[a][b] = sp;
+          } else {
+            const double am = acc[mi][(NP1 + anti_index(D, lo, hi)) * NH + hh][e];
+            L[a][b] = a < b ? sp + am : sp - am;
+          }
+        }
+      const int32_t v = ev[k];
+      if (v < 0) {   // one of several contributions: side slot, summed by K4
+        double *o = side + (int64_t)(-v - 1) * DD;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) o[a * D + b] = L[a][b];
+        continue;
+      }
+      const bool diag = A == B;
+      if (riA[k] >= 0) {   // K(I,J) = L (riA < 0: row of another shard)
+        double *p = out + DD * (riA[k] >> 24) + D * (v & 0xffff);
+        const int64_t str = D * (riA[k] & 0xffffff);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          double x[D];
+#pragma unroll
+          for (int b = 0; b < D; ++b) x[b] = diag && a > b ? L[b][a] : L[a][b];
+          store_seg_hint<D>(p + a * str, x, pol);
+        }
+      }
+      if (!diag && riB[k] >= 0) {   // K(J,I) = Lᵀ
+        double *p = out + DD * (riB[k] >> 24) + D * (v >> 16);
+        const int64_t str = D * (riB[k] & 0xffffff);
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double x[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) x[a] = L[a][b];
+          store_seg_hint<D>(p + b * str, x, pol);
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // K3: one CTA per 64×72 output tile, 4 MMA warps of 16×72, 3-stage bulk-copy ring
 // refilled by the last warp to release a stage, 4 CTAs per SM (16 MMA warps: the DMMA
@@ -165,7 +278,8 @@ __global__ void __launch_bounds__(K3Cfg<EPI>::THREADS, K3Cfg<EPI>::MINB)
 k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, int nkc, int ksteps, int ksplit, int64_t M,
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
-            int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm, const ApplyArgs ap) {
+            int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm, const uint16_t *__restrict__ cperm,
+            const ApplyArgs ap) {
   // tiles per CTA (sym layout: 8 in 3D, 16 in 2D), per epilogue thread; part-2 column tiles end
   constexpr int KMI = K3Cfg<EPI>::KMI, KW = K3Cfg<EPI>::WARPS, KT = K3Cfg<EPI>::THREADS;
   constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, TPT = TPC / (KT / K3_BM), NE = D == 3 ? 9 : 8;
@@ -187,7 +301,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     mbar_fence_init();
   }
 #ifndef IGA_EXPERIMENT_NO_PREFETCH
-  if (EPI == 1 && r < M)   // warm L2 with the epilogue's maps while the main loop runs
+  if ((EPI == 1 || EPI == 3) && r < M)   // warm L2 with the epilogue's maps while the main loop runs
     for (int tl = et0; tl < et0 + TPT && t0 + tl < n_tiles; ++tl) prefetch_l2(emap + (t0 + tl) * M + r);
 #endif
   __syncthreads();
@@ -230,6 +344,12 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
       }
     }
   }
+#ifdef IGA_EXPERIMENT_K3_DIRECT
+  if constexpr (EPI == 1 && KMI == 2) {   // every thread returns here: no barrier below is reached
+    k3_direct_scatter<D>(acc, warp, lane, m0, t0, M, n_tiles, out, pairA, pairB, emap, rowinfo, nl, side);
+    return;
+  }
+#endif
   __syncthreads();   // all stages consumed: stage the tile in shared memory
   double *sC = smem;
   {
@@ -373,6 +493,152 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   // the d-double row segments of a warp's 32 blocks are then stored cooperatively — lane
   // l writes words l, l+32, ... of the warp's 32·d words — so runs of adjacent blocks leave
   // as whole 32-B sectors instead of 8/16-B pieces per lane.
+#if IGA_K3_CL > 1   // experiment: thread-block clusters (profiles/r02_scatter_experiments.md)
+  // EPI 3 (thread-block clusters of K3_CL row blocks): the transposed pass walks the cluster's
+  // K3_CL·64 rows in (B, A) order (cperm), entry q·64 + er for the CTA of cluster rank q, and
+  // reads the block from the staging tile of the CTA that computed it (distributed shared
+  // memory), so the (J,I) blocks of one CSR row J coming from neighbouring A leave as one run
+  int et, src_rank = 0;
+  int64_t rt;
+  if constexpr (EPI == 3) {
+    const int64_t cb = (mb / K3_CL) * (K3_CL * K3_BM);
+    const int rs = cperm[cb + (mb % K3_CL) * K3_BM + er];
+    rt = cb + rs;
+    src_rank = rs / K3_BM;
+    et = rs % K3_BM;
+    cluster_arrive_release();   // this CTA's tile is staged
+  } else {
+    et = tperm[m0 + er];
+    rt = m0 + et;
+  }
+  const bool live = r < M, live_t = rt < M;
+  const int A = live ? pairA[r] : 0, B = live ? pairB[r] : 0;
+  const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
+  int32_t em[TPT], emt[TPT];
+  int64_t riA[TPT], riB[TPT];
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int64_t t = t0 + et0 + k < n_tiles ? t0 + et0 + k : n_tiles - 1;
+    em[k] = live ? emap[t * M + r] : 0;
+    riA[k] = live ? rowinfo[t * nl + A] : 0;
+    emt[k] = live_t ? emap[t * M + rt] : 0;
+    riB[k] = live_t ? rowinfo[t * nl + Bt] : 0;
+  }
+  // lanes hold (o = CSR offset of their block's first row segment or -1, row stride,
+  // smem row | diagonal << 8); word w of the warp's row segments comes from lane w/D,
+  // column w%D, and the D row segments of a block are o, o + stride, ...: one set of
+  // shuffles per block serves its D rows; value L[ra][cb] of that lane's block
+  auto coop = [&](int64_t o, int str, int pk, int tl, bool transposed) {
+    // all shuffles, then all shared loads, then the predicated stores (CSR values are written once:
+    // L2 evict-first)
+    int64_t ob[D];
+    int sstr[D], p[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int src = (32 * j + lane) / D;
+      ob[j] = __shfl_sync(0xffffffffu, o, src);
+      sstr[j] = __shfl_sync(0xffffffffu, str, src);
+      p[j] = __shfl_sync(0xffffffffu, pk, src);
+    }
+    double v[D][D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int c = (32 * j + lane) % D, sb = p[j] & 0xff;
+      const bool db = (p[j] >> 8) & 1;
+#pragma unroll
+      for (int idx = 0; idx < D; ++idx) {
+        int ra = transposed ? c : idx, cb = transposed ? idx : c;
+        if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+        if (EPI == 3 && transposed)   // the block's staging tile may live in another CTA of the cluster
+          v[j][idx] = cluster_map(sC, p[j] >> 9)[sb * K3_CROW + tl * DD + ra * D + cb];
+        else
+          v[j][idx] = sC[sb * K3_CROW + tl * DD + ra * D + cb];
+      }
+    }
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+    const uint64_t pol = l2_policy_evict_first();
+#endif
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int c = (32 * j + lane) % D;
+#pragma unroll
+      for (int idx = 0; idx < D; ++idx)
+        if (ob[j] >= 0) {
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+          st_hint(out + ob[j] + (int64_t)idx * sstr[j] + c, v[j][idx], pol);
+#else
+          out[ob[j] + (int64_t)idx * sstr[j] + c] = v[j][idx];
+#endif
+        }
+    }
+  };
+  auto pass1 = [&](int k) {   // row er: side slot or K(I,J) = L
+    const int tl = et0 + k;
+    const int32_t ev = em[k];
+#ifdef IGA_EXPERIMENT_NO_SCATTER
+    if (ev != 12345) return;
+#endif
+    if (live && ev < 0) {   // one of several contributions: side slot, summed by K4
+      const double *L = sC + er * K3_CROW;
+      double *o = side + (int64_t)(-ev - 1) * DD;
+#pragma unroll
+      for (int q = 0; q < DD; ++q) o[q] = L[tl * DD + q];
+    }
+    const bool w1 = live && ev >= 0 && riA[k] >= 0;   // riA < 0: row of another shard
+#ifndef IGA_EXPERIMENT_K3_LINEAR
+    const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff);
+    const int str1 = D * (int)(riA[k] & 0xffffff);
+#else   // timing only (wrong K): the same stores to contiguous blocks (scatter addresses removed)
+    const int64_t off1 = ((t0 + tl) * M + r) * DD;
+    const int str1 = D;
+#endif
+#ifndef IGA_EXPERIMENT_NO_PASS1
+    coop(w1 ? off1 : -1, str1, er | (A == B ? 256 : 0), tl, false);
+#endif
+  };
+  auto pass2 = [&](int k) {   // row rt of the (B, A) order: K(J,I) = Lᵀ
+    const int tl = et0 + k;
+#ifdef IGA_EXPERIMENT_NO_SCATTER
+    if (em[k] != 12345) return;
+#endif
+    const int32_t evt = emt[k];
+    const bool w2 = live_t && evt >= 0 && At != Bt && riB[k] >= 0;
+#ifndef IGA_EXPERIMENT_K3_LINEAR
+    const int64_t off2 = DD * (riB[k] >> 24) + D * (evt >> 16);
+    const int str2 = D * (int)(riB[k] & 0xffffff);
+#else
+    const int64_t off2 = (n_tiles * M - 1 - ((t0 + tl) * M + rt)) * DD;
+    const int str2 = D;
+#endif
+#ifndef IGA_EXPERIMENT_NO_PASS2
+    coop(w2 ? off2 : -1, str2, et | (src_rank << 9), tl, true);
+#endif
+  };
+  if constexpr (EPI == 3) {
+    // all (I,J) blocks, then — once every tile of the cluster is staged — the pooled (J,I) pass;
+    // no CTA leaves while another may still read its staging tile
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      if (t0 + et0 + k >= n_tiles) break;   // warp-uniform
+      pass1(k);
+    }
+    cluster_wait_acquire();
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      if (t0 + et0 + k >= n_tiles) break;
+      pass2(k);
+    }
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  } else {
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      if (t0 + et0 + k >= n_tiles) break;   // warp-uniform
+      pass1(k);
+      pass2(k);
+    }
+  }
+#else
   const int et = tperm[m0 + er];
   const int64_t rt = m0 + et;
   const bool live = r < M, live_t = rt < M;
@@ -448,19 +714,30 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
       for (int q = 0; q < DD; ++q) o[q] = L[tl * DD + q];
     }
     const bool w1 = live && ev >= 0 && riA[k] >= 0;   // riA < 0: row of another shard
+#ifndef IGA_EXPERIMENT_K3_LINEAR
     const int64_t off1 = DD * (riA[k] >> 24) + D * (ev & 0xffff);
     const int str1 = D * (int)(riA[k] & 0xffffff);
+#else   // timing only (wrong K): the same stores to contiguous blocks (scatter addresses removed)
+    const int64_t off1 = ((t0 + tl) * M + r) * DD;
+    const int str1 = D;
+#endif
 #ifndef IGA_EXPERIMENT_NO_PASS1
     coop(w1 ? off1 : -1, str1, er | (A == B ? 256 : 0), tl, false);
 #endif
     const int32_t evt = emt[k];
     const bool w2 = live_t && evt >= 0 && At != Bt && riB[k] >= 0;
+#ifndef IGA_EXPERIMENT_K3_LINEAR
     const int64_t off2 = DD * (riB[k] >> 24) + D * (evt >> 16);
     const int str2 = D * (int)(riB[k] & 0xffffff);
+#else
+    const int64_t off2 = (n_tiles * M - 1 - ((t0 + tl) * M + rt)) * DD;
+    const int str2 = D;
+#endif
 #ifndef IGA_EXPERIMENT_NO_PASS2
     coop(w2 ? off2 : -1, str2, et, tl, true);
 #endif
   }
+#endif
 }
 
 #ifdef IGA_EXPERIMENT_K3P
@@ -807,9 +1084,26 @@ static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, Apply
   if (e) return e;
   dim3 grid((unsigned)(h.Mpad / K3_BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+  if (EPI == 3) {   // thread-block clusters of K3_CL row blocks
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(K3Cfg<EPI>::THREADS);
+    cfg.dynamicSmemBytes = K3_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K3_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k3_contract<D, EPI>, h.d_tabA, h.d_coef, (int)(h.ks3 / BK), h.k3_steps, h.k3_split,
+                              h.M, h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo, h.n_local_ctrl,
+                              h.d_side, h.d_tperm, h.d_cperm, ap);
+  }
   k3_contract<D, EPI><<<grid, K3Cfg<EPI>::THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
                                                         h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,
-                                                        h.n_local_ctrl, h.d_side, h.d_tperm, ap);
+                                                        h.n_local_ctrl, h.d_side, h.d_tperm, h.d_cperm, ap);
   return cudaGetLastError();
 }
 
@@ -874,7 +1168,11 @@ cudaError_t launch_contraction(const Handle &h, double *vals, double *local, cud
 #ifdef IGA_EXPERIMENT_K3P   // the persistent warp-specialised K3 (profiles/r02_k3p_experiment.md)
   if (vals) e = h.d == 2 ? launch_k3p<2>(h, vals, s) : launch_k3p<3>(h, vals, s);
 #else
+#if IGA_K3_CL > 1   // experiment: thread-block clusters (profiles/r02_scatter_experiments.md)
+  if (vals) e = h.d == 2 ? launch_k3<2, 3>(h, vals, s) : launch_k3<3, 3>(h, vals, s);
+#else
   if (vals) e = h.d == 2 ? launch_k3<2, 1>(h, vals, s) : launch_k3<3, 1>(h, vals, s);
+#endif
 #endif
   if (e) return e;
   if (local) e = h.d == 2 ? launch_k3<2, 0>(h, local, s) : launch_k3<3, 0>(h, local, s);

@@ -165,6 +165,50 @@ def test_host_pointers_match_device_pointers():
     assert np.array_equal(vals_h, g["vals"].cpu().numpy())
 
 
+def test_concurrent_calls_on_one_handle():
+    """include/iga.h Concurrency: calls on one handle from several host threads, each on its
+    own stream, are serialised by the handle's lock — every result equals its serial value
+    bit for bit (without the lock they would race on the coefficient and side-slot workspace)."""
+    import threading
+    g = gpu_case(3)
+    prob, A = g["prob"], g["A"]
+    dev = g["vals"].device
+    young2 = 2.0 * g["young"]
+    u = torch.randn(A.sizes.n_dof, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    grad_ref = torch.empty(A.sizes.n_macro_cp * prob.d, dtype=torch.float64, device=dev)
+    A.sensitivity(g["ctrl"], g["young"], prob.nu, u, u, grad_ref)
+    vals2_ref = torch.empty_like(g["vals"])
+    A.assemble(g["ctrl"], young2, prob.nu, vals2_ref)
+    torch.cuda.synchronize()
+    errs = []
+
+    def worker(kind, reps=4):
+        st = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(st):
+            for _ in range(reps):
+                if kind == 0:
+                    v = torch.empty_like(g["vals"])
+                    A.assemble(g["ctrl"], g["young"], prob.nu, v, stream=st)
+                    ok = torch.equal(v, g["vals"])
+                elif kind == 1:
+                    v = torch.empty_like(g["vals"])
+                    A.assemble(g["ctrl"], young2, prob.nu, v, stream=st)
+                    ok = torch.equal(v, vals2_ref)
+                else:
+                    gr = torch.empty_like(grad_ref)
+                    A.sensitivity(g["ctrl"], g["young"], prob.nu, u, u, gr, stream=st)
+                    ok = torch.equal(gr, grad_ref)
+                if not ok:
+                    errs.append(kind)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in (0, 1, 2, 0)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, f"results differ from the serial ones in workers {errs}"
+
+
 def test_young_scaling_and_homogeneity_gpu():
     g = gpu_case(2)
     prob, A = g["prob"], g["A"]
