@@ -361,7 +361,10 @@ k2_interpolate(const __grid_constant__ InterpConst c_ip, const double *__restric
   constexpr int Q1 = S::Q1, NPI = S::NPI, DD = S::DD, NT = S::NT, TPB = S::TPB;
   __shared__ MacroTile<D> mt[TPB];
   __shared__ NodeGeo<D> geo[TPB][NPI];
-  const int tl = threadIdx.x / NT, comp = threadIdx.x % NT;
+  // tile fastest: the TPB threads of one component write its coefficients of TPB neighbouring
+  // tiles, which the fragment-major layout puts 32 B apart (one 128-B line per component and C
+  // in 3D) — 4× fewer L2 write requests than one component per lane
+  const int tl = threadIdx.x % TPB, comp = threadIdx.x / TPB;
   const int64_t t = (int64_t)blockIdx.x * TPB + tl;
   const bool live = t < n_tiles;
   const int64_t tg = t + c_ip.t_base;   // global tile id (macro element, E, error report)
