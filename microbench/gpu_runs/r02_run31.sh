@@ -1,0 +1,5 @@
+# K4 with per-pass descriptors: default registers vs 3 / 4 CTAs per SM
+for i in 1 2; do for lib in paper_2107_09568_b200/libiga.so microbench/libiga_IGA_K4_MINB3.so microbench/libiga_IGA_K4_MINB4.so; do
+  IGA_LIB=$lib timeout 120 python microbench/time_kernels.py --config 5 --reps 5 | cut -c1-110
+done; done
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "csr_values or symmetric or sharded or edge_case or host_pointers" 2>&1 | tail -2

@@ -8,6 +8,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--apply", action="store_true")
+    ap.add_argument("--local", action="store_true", help="also time the nzdata-only assemble (K2 + K3 EPI 0)")
     ap.add_argument("--q", type=int, default=None, help="projection degree override (e.g. the Eq. 65 choice)")
     args = ap.parse_args()
     import torch
@@ -24,6 +25,7 @@ def main():
     u, v = torch.tensor(u, device=dev), torch.tensor(v, device=dev)
     grad = torch.empty(s.n_macro_cp * prob.d, dtype=torch.float64, device=dev)
     y = torch.empty(s.n_dof, dtype=torch.float64, device=dev)
+    local = torch.empty(s.n_local_rows * s.n_tiles * prob.d ** 2, dtype=torch.float64, device=dev) if args.local else None
     for it in range(2):
         A.set_profiling(it == 1)
         for _ in range(args.reps if it else 2):
@@ -31,6 +33,8 @@ def main():
             A.sensitivity(ctrl, young, prob.nu, u, v, grad)
             if args.apply:
                 A.apply(ctrl, young, prob.nu, u, y)
+            if args.local:
+                A.assemble(ctrl, young, prob.nu, None, local)
         torch.cuda.synchronize()
     ms, n = A.kernel_times()
     names = ["K2", "K3", "K4", "K5a", "K5b", "K5c", "stage", "K5x", "K3local", "apply"]

@@ -46,9 +46,7 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_bcol, h.bcol.data(), h.bcol.size() * 4) ||
       !up((void **)&h.d_rowinfo, h.rowinfo.data(), h.rowinfo.size() * 8) ||
       !up((void **)&h.d_emap, h.emap.data(), h.emap.size() * 4) ||
-      !up((void **)&h.d_mblk, h.mblk.data(), h.mblk.size() * sizeof(MultiBlock)) ||
-      !up((void **)&h.d_mslot0, h.mslot0.data(), h.mslot0.size() * 4) ||
-      !up((void **)&h.d_mperm, h.mperm.data(), h.mperm.size() * 4) ||
+      !up((void **)&h.d_k4d, h.k4d.data(), h.k4d.size() * sizeof(K4Desc)) ||
       !up((void **)&h.d_slot_tr, h.slot_tr.data(), h.slot_tr.size()) ||
       !up((void **)&h.d_k5_pair, h.k5_pair.data(), h.k5_pair.size() * 4) ||
       !up((void **)&h.d_k5_col, h.k5_col.data(), h.k5_col.size() * 4) ||
@@ -81,6 +79,7 @@ iga_status upload_topology(Handle &h) {
   std::vector<int64_t>().swap(h.inv_ptr);
   std::vector<int32_t>().swap(h.inv_ent);
   std::vector<uint8_t>().swap(h.slot_tr);
+  std::vector<K4Desc>().swap(h.k4d);
   return IGA_OK;
 }
 
@@ -593,6 +592,18 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
     std::stable_sort(h.mperm.begin(), h.mperm.end(), [&](int32_t x, int32_t y) {
       return rowJ[x] != rowJ[y] ? rowJ[x] < rowJ[y] : colI[x] < colI[y];
     });
+    h.k4d.assign(2 * h.n_multi, K4Desc{});
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < h.n_multi; ++m) {
+      const MultiBlock &b1 = h.mblk[m];
+      const int64_t mt = h.mperm[m];
+      const MultiBlock &b2 = h.mblk[mt];
+      const bool dg1 = b1.off_ij == b1.off_ji, dg2 = b2.off_ij == b2.off_ji;
+      h.k4d[m] = K4Desc{b1.off_ij, b1.stride_i, h.mslot0[m], h.mslot0[m + 1] - h.mslot0[m], dg1 ? 1 : 0};
+      // diagonal blocks are complete after pass 1; off_ji < 0: row J belongs to another shard
+      h.k4d[h.n_multi + m] = K4Desc{b2.off_ji >= 0 && !dg2 ? b2.off_ji : -1, b2.stride_j, h.mslot0[mt],
+                                    h.mslot0[mt + 1] - h.mslot0[mt], 0};
+    }
   }
   h.rowinfo.assign(lnt * nl, 0);
 #pragma omp parallel for schedule(static)

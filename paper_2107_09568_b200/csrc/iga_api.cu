@@ -11,7 +11,7 @@ const char *get_error();
 
 Handle::~Handle() {
   void *bufs[] = {d_table, d_tabA, d_tabAT, d_coef, d_side, d_W, d_X, d_gpart, d_node_map, d_pairA, d_pairB,
-                  d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_mperm, d_slot_tr,
+                  d_row_ptr, d_col_idx, d_brow_ptr, d_bcol, d_rowinfo, d_emap, d_mblk, d_mslot0, d_mperm, d_slot_tr, d_k4d,
                   d_k5_pair, d_k5_col, d_tperm, d_cperm, d_rowdesc, d_g1len, d_g2len, d_g1slot, d_g2slot, d_sA_ptr, d_sA_slot,
                   d_inv_ptr, d_inv_ent, d_part, d_ug, d_k5_gphys, d_k5_mode, d_k5_extra, d_Wpart, d_F, d_th, d_det, d_Vt, d_mweights, d_patch_info, d_mknots, d_mspan, d_flag};
   for (void *b : bufs)

@@ -65,6 +65,18 @@ struct MultiBlock {
   int32_t stride_j;
 };
 
+// K4 pass descriptor (one per multi block and pass, in the pass's store order): where the
+// pass writes (off < 0: nothing, i.e. a diagonal block in pass 2 or a row of another shard),
+// the row pitch, the block's slot range and whether the block is diagonal (upper triangle
+// mirrored) — one 24-B load instead of the mperm → mblk / mslot0 chain
+struct K4Desc {
+  int64_t off;
+  int32_t stride;
+  int32_t s0;       // first side slot
+  int32_t ns;       // slots (>= 2)
+  int32_t diag;
+};
+
 struct Handle {
   int d = 0, p = 0, q = 0, n_g = 0, npi = 0, nk = 0, kstride = 0;
   int qv[3] = {0, 0, 0};         // per-direction projection degrees (anisotropic Q); q = max
@@ -101,6 +113,7 @@ struct Handle {
   std::vector<int32_t> mslot0;       // [n_multi+1] first slot of each multi block
   std::vector<int32_t> mperm;        // [n_multi] multi blocks in (J, I) order (K4 transposed pass)
   std::vector<uint8_t> slot_tr;      // [n_slots] 1 = slot holds the (J,I)-oriented block
+  std::vector<K4Desc> k4d;           // [2][n_multi] pass 1 in (I,J) order, pass 2 in (J,I) order
   // operand layouts (fragment-major, device_common.cuh fm_index)
   int64_t Mpad = 0;                  // rows of d_tabA (multiple of IGA_K3_BM · IGA_K3_CL)
   int64_t Npad = 0;                  // rows of d_coef / d_X (IGA_GEMM_BN per block of tpc tiles)
@@ -169,7 +182,8 @@ struct Handle {
   int32_t *d_bcol = nullptr;
   int64_t *d_rowinfo = nullptr;
   int32_t *d_emap = nullptr;
-  MultiBlock *d_mblk = nullptr;
+  MultiBlock *d_mblk = nullptr;   // (not uploaded: K4 reads d_k4d)
+  K4Desc *d_k4d = nullptr;
   int32_t *d_mslot0 = nullptr;
   int32_t *d_mperm = nullptr;
   uint8_t *d_slot_tr = nullptr;

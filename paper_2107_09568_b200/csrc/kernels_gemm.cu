@@ -392,10 +392,20 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   __syncthreads();
   if (EPI == 0) {   // nzdata (Eq. 58): local[row][t*DD + a*D + b]
     const int64_t N = n_tiles * DD;
-    for (int i = tid; i < K3_BM * TPC * DD; i += KT) {
-      const int rr = i / (TPC * DD), c = i % (TPC * DD), tl = c / DD, ab = c % DD;
-      const int64_t gr = m0 + rr, t = t0 + tl;
-      if (gr < M && t < n_tiles) out[gr * N + t * DD + ab] = sC[rr * K3_CROW + c];
+    constexpr int RW = TPC * DD;   // the block's 72 columns of a row are contiguous in nzdata
+    const uint64_t pol = l2_policy_evict_first();
+    if (t0 + TPC <= n_tiles && (N & 1) == 0) {   // whole block, 16-B aligned rows: 16-B stores
+      for (int i = tid; i < K3_BM * RW / 2; i += KT) {
+        const int rr = i / (RW / 2), c = 2 * (i % (RW / 2));
+        const int64_t gr = m0 + rr;
+        if (gr < M) st2_hint(out + gr * N + t0 * DD + c, sC[rr * K3_CROW + c], sC[rr * K3_CROW + c + 1], pol);
+      }
+    } else {
+      for (int i = tid; i < K3_BM * RW; i += KT) {
+        const int rr = i / RW, c = i % RW, tl = c / DD, ab = c % DD;
+        const int64_t gr = m0 + rr, t = t0 + tl;
+        if (gr < M && t < n_tiles) out[gr * N + t * DD + ab] = sC[rr * K3_CROW + c];
+      }
     }
     return;
   }

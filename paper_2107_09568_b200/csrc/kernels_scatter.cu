@@ -13,57 +13,72 @@
 
 namespace iga {
 
-// sum of the slots of multi block m (fixed slot order; slots recorded in the (J,I)
-// orientation transposed)
+// the slot sums of the two blocks of thread m (pass 1 and pass 2): a multi block has at least
+// two slots, so the first two slots of both (and their orientation flags) are loaded in one
+// round trip before any addition; further slots (tile edges and corners) follow in the fixed
+// slot order (the sum is (L_0 + L_1) + L_2 + ..., as K4 always formed it)
 template <int D>
-__device__ __forceinline__ void k4_sum(const double *__restrict__ side, const int32_t *__restrict__ mslot0,
-                                       const uint8_t *__restrict__ slot_tr, int64_t m, double *acc) {
+__device__ __forceinline__ void k4_sum2(const double *__restrict__ side, const uint8_t *__restrict__ slot_tr,
+                                        const K4Desc &d1, const K4Desc &d2, double *acc1, double *acc2) {
   constexpr int DD = D * D;
-  const int s0 = mslot0[m], s1 = mslot0[m + 1];
+  double l[4][DD];
+  const double *L0 = side + (int64_t)d1.s0 * DD, *L1 = L0 + DD, *L2 = side + (int64_t)d2.s0 * DD, *L3 = L2 + DD;
 #pragma unroll
-  for (int e = 0; e < DD; ++e) acc[e] = 0.0;
-  for (int sl = s0; sl < s1; sl += 2) {   // two slots per iteration, loads first
-    const bool two = sl + 1 < s1;
-    const double *L0 = side + (int64_t)sl * DD, *L1 = side + (int64_t)(two ? sl + 1 : sl) * DD;
-    double l0[DD], l1[DD];
+  for (int e = 0; e < DD; ++e) {
+    l[0][e] = L0[e];
+    l[1][e] = L1[e];
+    l[2][e] = L2[e];
+    l[3][e] = L3[e];
+  }
+  const bool t0 = slot_tr[d1.s0], t1 = slot_tr[d1.s0 + 1], t2 = slot_tr[d2.s0], t3 = slot_tr[d2.s0 + 1];
 #pragma unroll
-    for (int e = 0; e < DD; ++e) { l0[e] = L0[e]; l1[e] = L1[e]; }
-    const bool t0 = slot_tr[sl], t1 = two && slot_tr[sl + 1];
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      acc1[a * D + b] = (t0 ? l[0][b * D + a] : l[0][a * D + b]) + (t1 ? l[1][b * D + a] : l[1][a * D + b]);
+      acc2[a * D + b] = (t2 ? l[2][b * D + a] : l[2][a * D + b]) + (t3 ? l[3][b * D + a] : l[3][a * D + b]);
+    }
+  for (int sl = d1.s0 + 2; sl < d1.s0 + d1.ns; ++sl) {
+    const double *L = side + (int64_t)sl * DD;
+    const bool tr = slot_tr[sl];
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
-      for (int b = 0; b < D; ++b) acc[a * D + b] += t0 ? l0[b * D + a] : l0[a * D + b];
-    if (two) {
+      for (int b = 0; b < D; ++b) acc1[a * D + b] += tr ? L[b * D + a] : L[a * D + b];
+  }
+  for (int sl = d2.s0 + 2; sl < d2.s0 + d2.ns; ++sl) {
+    const double *L = side + (int64_t)sl * DD;
+    const bool tr = slot_tr[sl];
 #pragma unroll
-      for (int a = 0; a < D; ++a)
+    for (int a = 0; a < D; ++a)
 #pragma unroll
-        for (int b = 0; b < D; ++b) acc[a * D + b] += t1 ? l1[b * D + a] : l1[a * D + b];
-    }
+      for (int b = 0; b < D; ++b) acc2[a * D + b] += tr ? L[b * D + a] : L[a * D + b];
   }
 }
 
 // Thread m: pass 1 writes K(I,J) of multi block m (blocks ordered by (I, J)); pass 2 writes
-// K(J,I) of block mperm[m] (ordered by (J, I)).  Both orders put neighbouring blocks of one
-// CSR row in neighbouring lanes; the d-double row segments are stored warp-cooperatively
-// from a shared-memory copy of the sums (whole sectors for runs of adjacent blocks).
+// K(J,I) of the m-th block in (J, I) order.  Both orders put neighbouring blocks of one CSR
+// row in neighbouring lanes; the d-double row segments are stored warp-cooperatively from a
+// shared-memory copy of the sums (whole sectors for runs of adjacent blocks).  Each pass's
+// store target and slot range come from one descriptor (K4Desc, built on the host).
+#ifndef IGA_K4_MINB
+#define IGA_K4_MINB 3   // 3 CTAs of 256 per SM (85 registers): 0.547 ms at cfg5; 2 (110 registers) 0.585, 4 (64) 0.576
+#endif
 template <int D>
-__global__ void __launch_bounds__(256)
-k4_multi(const double *__restrict__ side, const MultiBlock *__restrict__ mblk, const int32_t *__restrict__ mslot0,
-         const uint8_t *__restrict__ slot_tr, const int32_t *__restrict__ mperm, int64_t n_multi,
-         double *__restrict__ vals) {
+__global__ void __launch_bounds__(256, IGA_K4_MINB)
+k4_multi(const double *__restrict__ side, const K4Desc *__restrict__ k4d, const uint8_t *__restrict__ slot_tr,
+         int64_t n_multi, double *__restrict__ vals) {
   constexpr int DD = D * D;
   __shared__ double sacc[2][256 * DD];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t m = blockIdx.x * (int64_t)blockDim.x + tid;
   const bool live = m < n_multi;
-  const int64_t mt = live ? mperm[m] : 0;
-  MultiBlock b1{}, b2{};
+  K4Desc d1{-1, 0, 0, 0, 0}, d2{-1, 0, 0, 0, 0};
   double acc1[DD], acc2[DD];
   if (live) {
-    b1 = mblk[m];
-    b2 = mblk[mt];
-    k4_sum<D>(side, mslot0, slot_tr, m, acc1);
-    k4_sum<D>(side, mslot0, slot_tr, mt, acc2);
+    d1 = k4d[m];
+    d2 = k4d[n_multi + m];
+    k4_sum2<D>(side, slot_tr, d1, d2, acc1, acc2);
   }
 #pragma unroll
   for (int e = 0; e < DD; ++e) {
@@ -92,11 +107,8 @@ k4_multi(const double *__restrict__ side, const MultiBlock *__restrict__ mblk, c
       }
     }
   };
-  const bool dg1 = b1.off_ij == b1.off_ji;
-  coop(live ? b1.off_ij : -1, b1.stride_i, dg1, 0);
-  // diagonal blocks are complete after pass 1; off_ji < 0: row J belongs to another shard
-  const bool w2 = live && b2.off_ji >= 0 && b2.off_ij != b2.off_ji;
-  coop(w2 ? b2.off_ji : -1, b2.stride_j, false, 1);
+  coop(live ? d1.off : -1, d1.stride, d1.diag != 0, 0);
+  coop(live ? d2.off : -1, d2.stride, false, 1);
 }
 
 // row_ptr / col_idx of the scalar CSR from the block CSR (interleaved DOFs, R9).
@@ -123,9 +135,9 @@ cudaError_t launch_scatter_multi(const Handle &h, double *vals, cudaStream_t s) 
   if (h.n_multi == 0) return cudaSuccess;
   unsigned blocks = (unsigned)((h.n_multi + 255) / 256);
   if (h.d == 2)
-    k4_multi<2><<<blocks, 256, 0, s>>>(h.d_side, h.d_mblk, h.d_mslot0, h.d_slot_tr, h.d_mperm, h.n_multi, vals);
+    k4_multi<2><<<blocks, 256, 0, s>>>(h.d_side, h.d_k4d, h.d_slot_tr, h.n_multi, vals);
   else
-    k4_multi<3><<<blocks, 256, 0, s>>>(h.d_side, h.d_mblk, h.d_mslot0, h.d_slot_tr, h.d_mperm, h.n_multi, vals);
+    k4_multi<3><<<blocks, 256, 0, s>>>(h.d_side, h.d_k4d, h.d_slot_tr, h.n_multi, vals);
   return cudaGetLastError();
 }
 
