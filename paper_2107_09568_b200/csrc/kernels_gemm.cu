@@ -664,11 +664,69 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     emt[k] = live_t ? emap[t * M + rt] : 0;
     riB[k] = live_t ? rowinfo[t * nl + Bt] : 0;
   }
+  // cooperative row-segment stores: word w = 32j + lane of the warp's 32·D words of one row
+  // index comes from the block of lane src_j = w / D (its row), column c_j = w % D.  Lanes hold
+  // (o = CSR offset of their block's first row segment or -1, row stride); the shared-memory
+  // offsets of every (j, idx) word are tile-independent and computed once here: pass 1 reads
+  // L[idx][c] of row er(src) (diagonal rows: L[min][max], R9), pass 2 reads L[c][idx] of row
+  // tperm(src) — per tile only the offsets and strides are shuffled.
+#ifndef IGA_EXPERIMENT_K3_COOP_V22
+  int so1[D][D], so2[D];
+  {
+    const bool dg = A == B;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int w = 32 * j + lane, src = w / D, c = w % D;
+      const int er_s = (er & ~31) + src;                      // row of lane src (er = tid % 64)
+      const int et_s = __shfl_sync(0xffffffffu, et, src);
+      const bool dg_s = __shfl_sync(0xffffffffu, (int)dg, src) != 0;
+#pragma unroll
+      for (int idx = 0; idx < D; ++idx) {
+        const int lo = dg_s && idx > c ? c : idx, hi = dg_s && idx > c ? idx : c;
+        so1[j][idx] = er_s * K3_CROW + lo * D + hi;
+      }
+      so2[j] = et_s * K3_CROW + c * D;
+    }
+  }
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+  const uint64_t pol = l2_policy_evict_first();   // CSR values are written once
+#endif
+  auto coop = [&](int64_t o, int str, int tl, bool transposed) {
+    int64_t ob[D];
+    int sstr[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int src = (32 * j + lane) / D;
+      ob[j] = __shfl_sync(0xffffffffu, o, src);
+      sstr[j] = __shfl_sync(0xffffffffu, str, src);
+    }
+    const double *st = sC + tl * DD;
+    double v[D][D];
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int idx = 0; idx < D; ++idx) v[j][idx] = transposed ? st[so2[j] + idx] : st[so1[j][idx]];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if (ob[j] >= 0) {
+        double *g = out + ob[j] + (32 * j + lane) % D;
+#pragma unroll
+        for (int idx = 0; idx < D; ++idx) {
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+          st_hint(g + (int64_t)idx * sstr[j], v[j][idx], pol);
+#else
+          g[(int64_t)idx * sstr[j]] = v[j][idx];
+#endif
+        }
+      }
+    }
+  };
+#else   // the v22 cooperative store (shuffled row / diagonal flag per tile and word)
   // lanes hold (o = CSR offset of their block's first row segment or -1, row stride,
   // smem row | diagonal << 8); word w of the warp's row segments comes from lane w/D,
   // column w%D, and the D row segments of a block are o, o + stride, ...: one set of
   // shuffles per block serves its D rows; value L[ra][cb] of that lane's block
-  auto coop = [&](int64_t o, int str, int pk, int tl, bool transposed) {
+  auto coop_v22 = [&](int64_t o, int str, int pk, int tl, bool transposed) {
     // all shuffles, then all shared loads, then the predicated stores (CSR values are written once:
     // L2 evict-first)
     int64_t ob[D];
@@ -709,6 +767,10 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
         }
     }
   };
+  auto coop = [&](int64_t o, int str, int tl, bool transposed) {
+    coop_v22(o, str, transposed ? et : (er | (A == B ? 256 : 0)), tl, transposed);
+  };
+#endif
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
     const int tl = et0 + k;
@@ -732,7 +794,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int str1 = D;
 #endif
 #ifndef IGA_EXPERIMENT_NO_PASS1
-    coop(w1 ? off1 : -1, str1, er | (A == B ? 256 : 0), tl, false);
+    coop(w1 ? off1 : -1, str1, tl, false);
 #endif
     const int32_t evt = emt[k];
     const bool w2 = live_t && evt >= 0 && At != Bt && riB[k] >= 0;
@@ -744,7 +806,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int str2 = D;
 #endif
 #ifndef IGA_EXPERIMENT_NO_PASS2
-    coop(w2 ? off2 : -1, str2, et, tl, true);
+    coop(w2 ? off2 : -1, str2, tl, true);
 #endif
   }
 #endif
