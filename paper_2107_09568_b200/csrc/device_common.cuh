@@ -209,8 +209,15 @@ __device__ __forceinline__ void bulk_g2s_hint(void *smem, const void *gmem, uint
       "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// (IGA_EXPERIMENT_ST_NOCLOBBER: no "memory" clobber, so the compiler may hoist the shared-memory
+// loads of later stores above these global stores)
+#ifndef IGA_EXPERIMENT_ST_NOCLOBBER
+#define IGA_ST_CLOBBER : "memory"
+#else
+#define IGA_ST_CLOBBER
+#endif
 __device__ __forceinline__ void st_hint(double *p, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) IGA_ST_CLOBBER);
 }
 __device__ __forceinline__ void st2_hint(double *p, double v0, double v1, uint64_t pol) {   // p 16-B aligned
   asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v0), "d"(v1), "l"(pol) : "memory");

@@ -688,9 +688,6 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
       so2[j] = et_s * K3_CROW + c * D;
     }
   }
-#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
-  const uint64_t pol = l2_policy_evict_first();   // CSR values are written once
-#endif
   auto coop = [&](int64_t o, int str, int tl, bool transposed) {
     int64_t ob[D];
     int sstr[D];
@@ -706,6 +703,9 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     for (int j = 0; j < D; ++j)
 #pragma unroll
       for (int idx = 0; idx < D; ++idx) v[j][idx] = transposed ? st[so2[j] + idx] : st[so1[j][idx]];
+#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+    const uint64_t pol = l2_policy_evict_first();   // CSR values are written once (a constant: folded by ptxas)
+#endif
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       if (ob[j] >= 0) {
