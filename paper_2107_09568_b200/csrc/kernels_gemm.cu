@@ -279,7 +279,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
             int64_t n_tiles, double *__restrict__ out, const int32_t *__restrict__ pairA,
             const int32_t *__restrict__ pairB, const int32_t *__restrict__ emap, const int64_t *__restrict__ rowinfo,
             int nl, double *__restrict__ side, const uint8_t *__restrict__ tperm, const uint16_t *__restrict__ cperm,
-            const ApplyArgs ap) {
+            const int4 *__restrict__ rowdesc, const ApplyArgs ap) {
   // tiles per CTA (sym layout: 8 in 3D, 16 in 2D), per epilogue thread; part-2 column tiles end
   constexpr int KMI = K3Cfg<EPI>::KMI, KW = K3Cfg<EPI>::WARPS, KT = K3Cfg<EPI>::THREADS;
   constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, TPT = TPC / (KT / K3_BM), NE = D == 3 ? 9 : 8;
@@ -649,11 +649,20 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     }
   }
 #else
+#ifndef IGA_EXPERIMENT_K3_ROWDESC
   const int et = tperm[m0 + er];
   const int64_t rt = m0 + et;
   const bool live = r < M, live_t = rt < M;
   const int A = live ? pairA[r] : 0, B = live ? pairB[r] : 0;
   const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
+#else   // one 16-B row descriptor {A | B << 16, At | Bt << 16, tperm, 0}: one load level less
+  const int4 rd = rowdesc[m0 + er];
+  const int et = rd.z;
+  const int64_t rt = m0 + et;
+  const bool live = rd.x >= 0, live_t = rd.y >= 0;
+  const int A = live ? rd.x & 0xffff : 0, B = live ? rd.x >> 16 : 0;
+  const int At = live_t ? rd.y & 0xffff : 0, Bt = live_t ? rd.y >> 16 : 0;
+#endif
   int32_t em[TPT], emt[TPT];
   int64_t riA[TPT], riB[TPT];
 #pragma unroll
@@ -1171,11 +1180,11 @@ static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, Apply
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k3_contract<D, EPI>, h.d_tabA, h.d_coef, (int)(h.ks3 / BK), h.k3_steps, h.k3_split,
                               h.M, h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo, h.n_local_ctrl,
-                              h.d_side, h.d_tperm, h.d_cperm, ap);
+                              h.d_side, h.d_tperm, h.d_cperm, h.d_rowdesc, ap);
   }
   k3_contract<D, EPI><<<grid, K3Cfg<EPI>::THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
                                                         h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,
-                                                        h.n_local_ctrl, h.d_side, h.d_tperm, h.d_cperm, ap);
+                                                        h.n_local_ctrl, h.d_side, h.d_tperm, h.d_cperm, h.d_rowdesc, ap);
   return cudaGetLastError();
 }
 
@@ -1460,7 +1469,7 @@ k5a_wgemm(const double *__restrict__ tabAT, const double *__restrict__ X, int nk
 #endif
 constexpr int K5G_GEN_WARPS = IGA_K5G_GEN_WARPS;
 static_assert(K5G_GEN_WARPS % 4 == 0, "generator groups of 4 warps (128 threads per chunk)");
-static_assert(K5G_GEN_WARPS / 4 <= 3, "the generators' emptyB parity wait needs groups <= stages (S >= 3)");
+static_assert(K5G_GEN_WARPS / 4 <= 3, "the generators' emptyB parity wait needs groups <= X̃ stages (SB >= 3)");
 constexpr int K5G_THREADS = 32 * (N_MMA_WARPS + K5G_GEN_WARPS);
 
 struct K5gArgs {
@@ -1478,11 +1487,16 @@ struct K5gArgs {
   const int32_t *k5_extra;   // modes 11/12: the extra single-column piece (local group | column << 16)
 };
 
-template <int S>
+// SA table stages (TMA, refilled by the last MMA warp to release one) and SB >= SA X̃ stages
+// (written by the generators, released by every MMA warp's arrival): the generators run up to
+// SB chunks ahead of the MMA warps, so a chunk whose FP64 products were throttled behind the
+// DMMAs is still ready in time
+template <int SA, int SB>
 struct K5gSmem {
-  static constexpr size_t STAGES = sizeof(double) * (size_t)S * (K5_A_CHUNK + K5_B_CHUNK);
+  static constexpr size_t STAGES = sizeof(double) * ((size_t)SA * K5_A_CHUNK + (size_t)SB * K5_B_CHUNK);
   static size_t bytes(int d, int ts) {
-    return STAGES + sizeof(double) * 2 * (size_t)(d == 3 ? 8 : 16) * ts + S * (3 * sizeof(uint64_t) + sizeof(int));
+    return STAGES + sizeof(double) * 2 * (size_t)(d == 3 ? 8 : 16) * ts + (SA + 2 * SB) * sizeof(uint64_t) +
+           SA * sizeof(int);
   }
 };
 
@@ -1492,15 +1506,15 @@ struct K5gAcc {
   double a0[N0 > 0 ? N0 : 1][2], a1[N1 > 0 ? N1 : 1][2];
 };
 
-template <int D, int S, int LO0, int HI0, int LO1, int HI1, bool HX = false>
+template <int D, int SA, int SB, int LO0, int HI0, int LO1, int HI1, bool HX = false>
 __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int kc_lo, int nkc, int warp, int lane,
                                              const double *gA, int xg = 0, int xn = 0) {
   constexpr int N0 = HI0 - LO0, N1 = HI1 - LO1;
-  double *sA = smem, *sB = smem + S * K5_A_CHUNK;
-  uint64_t *fullA = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5gSmem<S>::STAGES +
+  double *sA = smem, *sB = smem + SA * K5_A_CHUNK;
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5gSmem<SA, SB>::STAGES +
                                                  sizeof(double) * 2 * (D == 3 ? 8 : 16) * g.ts);
-  uint64_t *fullB = fullA + S, *emptyB = fullB + S;
-  int *released = reinterpret_cast<int *>(emptyB + S);
+  uint64_t *fullB = fullA + SA, *emptyB = fullB + SB;
+  int *released = reinterpret_cast<int *>(emptyB + SB);
   K5gAcc<LO0, HI0, LO1, HI1> acc;
   double accx0 = 0.0, accx1 = 0.0;   // HX: the extra piece (group xg, column tile xn)
 #pragma unroll
@@ -1509,11 +1523,10 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
   for (int i = 0; i < (N1 > 0 ? N1 : 1); ++i) acc.a1[i][0] = acc.a1[i][1] = 0.0;
   const int g0 = warp * 2;
   for (int kc = 0; kc < nkc; ++kc) {
-    const int st = kc % S;
-    const uint32_t par = (kc / S) & 1;
-    mbar_wait(&fullA[st], par);
-    mbar_wait(&fullB[st], par);
-    const double *a_st = sA + st * K5_A_CHUNK, *b_st = sB + st * K5_B_CHUNK;
+    const int st = kc % SA, sb = kc % SB;
+    mbar_wait(&fullA[st], (kc / SA) & 1);
+    mbar_wait(&fullB[sb], (kc / SB) & 1);
+    const double *a_st = sA + st * K5_A_CHUNK, *b_st = sB + sb * K5_B_CHUNK;
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       double a0 = 0.0, a1 = 0.0, b[NI];
@@ -1530,18 +1543,18 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
     }
     __syncwarp();
     if (lane == 0) {
+      mbar_arrive(&emptyB[sb]);   // this warp is done with the X̃ stage (release: its reads come first)
       __threadfence_block();
       if (atomicAdd(&released[st], 1) == N_MMA_WARPS - 1) {
         released[st] = 0;
         __threadfence_block();
-        if (kc + S < nkc) {   // refill: the table chunk by TMA, the X̃ chunk by the generators
-#ifdef IGA_EXPERIMENT_K5G_NO_TABLE_REFILL   // timing only (wrong g): the first S table chunks are reused
+        if (kc + SA < nkc) {   // refill the table chunk by TMA
+#ifdef IGA_EXPERIMENT_K5G_NO_TABLE_REFILL   // timing only (wrong g): the first SA table chunks are reused
           mbar_arrive(&fullA[st]);
 #else
           mbar_expect_tx(&fullA[st], K5_A_CHUNK * 8);
-          bulk_g2s(sA + st * K5_A_CHUNK, gA + (int64_t)(kc + S) * K5_A_CHUNK, K5_A_CHUNK * 8, &fullA[st]);
+          bulk_g2s(sA + st * K5_A_CHUNK, gA + (int64_t)(kc + SA) * K5_A_CHUNK, K5_A_CHUNK * 8, &fullA[st]);
 #endif
-          mbar_arrive(&emptyB[st]);
         }
       }
     }
@@ -1568,15 +1581,15 @@ __device__ __forceinline__ void k5g_mma_role(const K5gArgs &g, double *smem, int
   }
 }
 
-template <int D, int S>
+template <int D, int SA, int SB>
 __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int kc_lo, int nkc, int64_t nb, int gtid) {
   constexpr int TPC = D == 3 ? 8 : 16, NP1 = D * (D + 1) / 2, NP2 = D * (D - 1) / 2, NTL = D == 3 ? 1 : 2;
   constexpr int NG = K5G_GEN_WARPS / 4;          // groups of 4 warps: one chunk per group at a time
   constexpr int NGT = 32 * K5G_GEN_WARPS;
-  double *sB = smem + S * K5_A_CHUNK;
-  double *us = smem + K5gSmem<S>::STAGES / sizeof(double), *vs = us + TPC * g.ts;
+  double *sB = smem + SA * K5_A_CHUNK;
+  double *us = smem + K5gSmem<SA, SB>::STAGES / sizeof(double), *vs = us + TPC * g.ts;
   uint64_t *fullA = reinterpret_cast<uint64_t *>(vs + TPC * g.ts);
-  uint64_t *fullB = fullA + S, *emptyB = fullB + S;
+  uint64_t *fullB = fullA + SA, *emptyB = fullB + SB;
   const int grp = gtid >> 7, gt = gtid & 127;
   const int lane = gt & 31, k = 4 * (gt >> 5) + (lane & 3);
   const int64_t t0 = nb * TPC;
@@ -1617,8 +1630,8 @@ __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int
     for (int gkc = c0 + grp; gkc < c1; gkc += NG) {
       const int32_t pr = prn;
       prn = gkc + NG < c1 ? g.k5_pair[(int64_t)(gkc + NG) * BK + k] : -1;
-      const int kc = gkc - kc_lo, st = kc % S;
-      if (kc >= S) mbar_wait(&emptyB[st], ((kc / S) - 1) & 1);
+      const int kc = gkc - kc_lo, st = kc % SB;
+      if (kc >= SB) mbar_wait(&emptyB[st], ((kc / SB) - 1) & 1);
       double x[NI];
 #pragma unroll
       for (int j = 0; j < NI; ++j) x[j] = 0.0;
@@ -1664,15 +1677,16 @@ __device__ __forceinline__ void k5g_gen_role(const K5gArgs &g, double *smem, int
   named_bar(1, K5G_THREADS);
 }
 
-template <int D, int S, bool SPLIT>
+template <int D, int SA, int SB, bool SPLIT>
 __global__ void __launch_bounds__(K5G_THREADS, 1)
 k5g_wgemm(const __grid_constant__ K5gArgs g) {
   constexpr int NE = D == 3 ? 9 : 8;
+  static_assert(SB >= SA, "X̃ stages >= table stages");
   extern __shared__ __align__(128) double smem[];
-  uint64_t *fullA = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5gSmem<S>::STAGES +
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K5gSmem<SA, SB>::STAGES +
                                                  sizeof(double) * 2 * (D == 3 ? 8 : 16) * g.ts);
-  uint64_t *fullB = fullA + S, *emptyB = fullB + S;
-  int *released = reinterpret_cast<int *>(emptyB + S);
+  uint64_t *fullB = fullA + SA, *emptyB = fullB + SB;
+  int *released = reinterpret_cast<int *>(emptyB + SB);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t kb = blockIdx.x, nb = blockIdx.y;
   int nkc = g.nkc, kc_lo = 0;
@@ -1684,43 +1698,45 @@ k5g_wgemm(const __grid_constant__ K5gArgs g) {
   }
   const double *gA = g.tabAT + (kb * (int64_t)g.nkc + kc_lo) * K5_A_CHUNK;
   if (tid == 0) {
-    for (int st = 0; st < S; ++st) {
+    for (int st = 0; st < SA; ++st) {
       mbar_init(&fullA[st], 1);
-      mbar_init(&fullB[st], 4);   // the 4 warps of the group generating the chunk
-      mbar_init(&emptyB[st], 1);
       released[st] = 0;
+    }
+    for (int st = 0; st < SB; ++st) {
+      mbar_init(&fullB[st], 4);              // the 4 warps of the group generating the chunk
+      mbar_init(&emptyB[st], N_MMA_WARPS);   // every MMA warp releases the X̃ stage
     }
     mbar_fence_init();
   }
   __syncthreads();
   if (tid == 0)
-    for (int st = 0; st < S && st < nkc; ++st) {
+    for (int st = 0; st < SA && st < nkc; ++st) {
       mbar_expect_tx(&fullA[st], K5_A_CHUNK * 8);
       bulk_g2s(smem + st * K5_A_CHUNK, gA + (int64_t)st * K5_A_CHUNK, K5_A_CHUNK * 8, &fullA[st]);
     }
   if (warp >= N_MMA_WARPS) {
-    k5g_gen_role<D, S>(g, smem, kc_lo, nkc, nb, tid - 32 * N_MMA_WARPS);
+    k5g_gen_role<D, SA, SB>(g, smem, kc_lo, nkc, nb, tid - 32 * N_MMA_WARPS);
   } else {
     switch (g.k5_mode[kb * N_MMA_WARPS + warp]) {   // parts of the warp's two κ groups
-      case 4: k5g_mma_role<D, S, 0, 6, 0, 6>(g, smem, kc_lo, nkc, warp, lane, gA); break;
-      case 8: k5g_mma_role<D, S, 6, NE, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
-      case 5: k5g_mma_role<D, S, 0, 6, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
-      case 3: k5g_mma_role<D, S, 0, 6, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
-      case 6: k5g_mma_role<D, S, 6, NE, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 4: k5g_mma_role<D, SA, SB, 0, 6, 0, 6>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 8: k5g_mma_role<D, SA, SB, 6, NE, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 5: k5g_mma_role<D, SA, SB, 0, 6, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 3: k5g_mma_role<D, SA, SB, 0, 6, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 6: k5g_mma_role<D, SA, SB, 6, NE, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
       // column split (host_build.cpp, 3D): part-1 group cut to columns 0-3; extra column pieces
-      case 9: k5g_mma_role<D, S, 0, 4, 0, 6>(g, smem, kc_lo, nkc, warp, lane, gA); break;
-      case 10: k5g_mma_role<D, S, 0, 4, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 9: k5g_mma_role<D, SA, SB, 0, 4, 0, 6>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      case 10: k5g_mma_role<D, SA, SB, 0, 4, 6, NE>(g, smem, kc_lo, nkc, warp, lane, gA); break;
       case 11: {
         const int x = g.k5_extra[kb * N_MMA_WARPS + warp];
-        k5g_mma_role<D, S, 6, NE, 6, NE, true>(g, smem, kc_lo, nkc, warp, lane, gA, x & 0xffff, x >> 16);
+        k5g_mma_role<D, SA, SB, 6, NE, 6, NE, true>(g, smem, kc_lo, nkc, warp, lane, gA, x & 0xffff, x >> 16);
         break;
       }
       case 12: {
         const int x = g.k5_extra[kb * N_MMA_WARPS + warp];
-        k5g_mma_role<D, S, 0, 6, 6, NE, true>(g, smem, kc_lo, nkc, warp, lane, gA, x & 0xffff, x >> 16);
+        k5g_mma_role<D, SA, SB, 0, 6, 6, NE, true>(g, smem, kc_lo, nkc, warp, lane, gA, x & 0xffff, x >> 16);
         break;
       }
-      default: k5g_mma_role<D, S, 0, 0, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
+      default: k5g_mma_role<D, SA, SB, 0, 0, 0, 0>(g, smem, kc_lo, nkc, warp, lane, gA); break;
     }
   }
   __syncthreads();
@@ -1789,13 +1805,13 @@ static cudaError_t launch_k5a(const Handle &h, double *W, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int D, int S>
+template <int D, int SA, int SB>
 static cudaError_t launch_k5g_s(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s) {
   const int ts = h.max_patch_ctrl * D + 1;
-  const size_t smem = K5gSmem<S>::bytes(D, ts);
-  // the Y staging (after the main loop) overlays the stage ring and the u/v staging, not
+  const size_t smem = K5gSmem<SA, SB>::bytes(D, ts);
+  // the Y staging (after the main loop) overlays the stage rings and the u/v staging, not
   // the mbarriers behind them
-  if (sizeof(double) * BN * K5_WP > K5gSmem<S>::STAGES + sizeof(double) * 2 * (D == 3 ? 8 : 16) * (size_t)ts)
+  if (sizeof(double) * BN * K5_WP > K5gSmem<SA, SB>::STAGES + sizeof(double) * 2 * (D == 3 ? 8 : 16) * (size_t)ts)
     return cudaErrorNotSupported;
   const int64_t nblk = (h.n_tiles_own + h.tpc - 1) / h.tpc;
   const int nseg = h.k5_nseg;
@@ -1805,11 +1821,13 @@ static cudaError_t launch_k5g_s(const Handle &h, const double *u, const double *
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   cudaError_t e;
   if (nseg > 1) {
-    if ((e = cudaFuncSetAttribute(k5g_wgemm<D, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    k5g_wgemm<D, S, true><<<grid, K5G_THREADS, smem, s>>>(g);
+    if ((e = cudaFuncSetAttribute(k5g_wgemm<D, SA, SB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+      return e;
+    k5g_wgemm<D, SA, SB, true><<<grid, K5G_THREADS, smem, s>>>(g);
   } else {
-    if ((e = cudaFuncSetAttribute(k5g_wgemm<D, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    k5g_wgemm<D, S, false><<<grid, K5G_THREADS, smem, s>>>(g);
+    if ((e = cudaFuncSetAttribute(k5g_wgemm<D, SA, SB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+      return e;
+    k5g_wgemm<D, SA, SB, false><<<grid, K5G_THREADS, smem, s>>>(g);
   }
   if ((e = cudaGetLastError())) return e;
   if (nseg > 1) {
@@ -1826,20 +1844,34 @@ bool sens_xw_fits(const Handle &h) {
   const size_t uv = sizeof(double) * 2 * (h.d == 3 ? 8 : 16) * (size_t)ts;
   const size_t lim = 227 * 1024;
   auto ok = [&](size_t stages, size_t bytes) { return bytes <= lim && sizeof(double) * BN * K5_WP <= stages + uv; };
-  return ok(K5gSmem<4>::STAGES, K5gSmem<4>::bytes(h.d, ts)) || ok(K5gSmem<3>::STAGES, K5gSmem<3>::bytes(h.d, ts));
+  return ok(K5gSmem<3, 3>::STAGES, K5gSmem<3, 3>::bytes(h.d, ts));   // the smallest variant launch_sens_XW tries
+}
+
+// K5g ring shapes, first that fits: (table stages, X̃ stages)
+#ifndef IGA_K5G_SB
+#define IGA_K5G_SB 8   // X̃ stages of the preferred shape (cfg5: 12.94 ms; 6: 12.95, 4: 13.10, one 4-stage ring 13.13)
+#endif
+#ifndef IGA_K5G_SA
+#define IGA_K5G_SA 3   // table stages of the preferred shape
+#endif
+template <int D>
+static cudaError_t launch_k5g_pick(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s) {
+  const int ts = h.max_patch_ctrl * D + 1;
+  const size_t lim = 227 * 1024, uv = sizeof(double) * 2 * (D == 3 ? 8 : 16) * (size_t)ts;
+  auto fits = [&](size_t stages, size_t bytes) { return bytes <= lim && sizeof(double) * BN * K5_WP <= stages + uv; };
+#define IGA_K5G_TRY(SA_, SB_) \
+  if (fits(K5gSmem<SA_, SB_>::STAGES, K5gSmem<SA_, SB_>::bytes(D, ts))) return launch_k5g_s<D, SA_, SB_>(h, u, v, W, s);
+  IGA_K5G_TRY(IGA_K5G_SA, IGA_K5G_SB)
+  IGA_K5G_TRY(3, 6)
+  IGA_K5G_TRY(4, 4)
+  IGA_K5G_TRY(3, 4)
+  IGA_K5G_TRY(3, 3)
+#undef IGA_K5G_TRY
+  return cudaErrorNotSupported;
 }
 
 cudaError_t launch_sens_XW(const Handle &h, const double *u, const double *v, double *W, cudaStream_t s) {
-  const int ts = h.max_patch_ctrl * h.d + 1;
-  const size_t lim = 227 * 1024;
-  if (h.d == 3) {
-    if (K5gSmem<4>::bytes(3, ts) <= lim) return launch_k5g_s<3, 4>(h, u, v, W, s);
-    if (K5gSmem<3>::bytes(3, ts) <= lim) return launch_k5g_s<3, 3>(h, u, v, W, s);
-  } else {
-    if (K5gSmem<4>::bytes(2, ts) <= lim) return launch_k5g_s<2, 4>(h, u, v, W, s);
-    if (K5gSmem<3>::bytes(2, ts) <= lim) return launch_k5g_s<2, 3>(h, u, v, W, s);
-  }
-  return cudaErrorNotSupported;
+  return h.d == 3 ? launch_k5g_pick<3>(h, u, v, W, s) : launch_k5g_pick<2>(h, u, v, W, s);
 }
 
 cudaError_t launch_sens_W(const Handle &h, double *W, cudaStream_t s) {
