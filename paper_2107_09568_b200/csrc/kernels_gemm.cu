@@ -37,7 +37,10 @@ constexpr int MI = 2;              // 2 DMMA row tiles per warp (16 rows)
 constexpr int N_MMA_WARPS = IGA_K5_BM / 16;                                // K5a: 16
 constexpr int BM = 16 * N_MMA_WARPS;                                        // 256 (K5a κ rows)
 constexpr int K3_BM = IGA_K3_BM, K3_WARPS = K3_BM / 16;                     // K3: 64 rows, 4 MMA warps
-constexpr int K3_CL = IGA_K3_CL;                                            // K3 CTAs per cluster (EPI 3)
+constexpr int K3_CL = IGA_K3_CL;
+#ifdef IGA_K3_TILE_UNROLL
+constexpr int K3_TILE_UNROLL = IGA_K3_TILE_UNROLL;
+#endif                                            // K3 CTAs per cluster (EPI 3)
 static_assert(K3_CL == 1 || (K3_CL * K3_BM <= 65536 && K3_CL <= 8 && K3_BM == 64), "cluster row blocks: cperm is uint16, pk packs the rank in 3 bits above the row");
 static_assert(K3_BM == 64 || K3_BM == 128, "K3 row blocks: 64 (product) or 128 rows; other shapes are not supported by every epilogue");
 static_assert(BM == IGA_K5_BM, "K5a CTA rows");
@@ -780,7 +783,11 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     coop_v22(o, str, transposed ? et : (er | (A == B ? 256 : 0)), tl, transposed);
   };
 #endif
+#ifdef IGA_K3_TILE_UNROLL   // experiment: unroll factor of the tile loop (default: full)
+#pragma unroll K3_TILE_UNROLL
+#else
 #pragma unroll
+#endif
   for (int k = 0; k < TPT; ++k) {
     const int tl = et0 + k;
     if (t0 + tl >= n_tiles) break;   // warp-uniform
@@ -814,10 +821,20 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int64_t off2 = (n_tiles * M - 1 - ((t0 + tl) * M + rt)) * DD;
     const int str2 = D;
 #endif
-#ifndef IGA_EXPERIMENT_NO_PASS2
+#if !defined(IGA_EXPERIMENT_NO_PASS2) && !defined(IGA_EXPERIMENT_K3_SPLIT_PASSES)
     coop(w2 ? off2 : -1, str2, tl, true);
 #endif
   }
+#ifdef IGA_EXPERIMENT_K3_SPLIT_PASSES   // experiment: all (I,J) blocks first, then all (J,I) blocks
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int tl = et0 + k;
+    if (t0 + tl >= n_tiles) break;
+    const int32_t evt = emt[k];
+    const bool w2 = live_t && evt >= 0 && At != Bt && riB[k] >= 0;
+    coop(w2 ? DD * (riB[k] >> 24) + D * (evt >> 16) : -1, D * (int)(riB[k] & 0xffffff), tl, true);
+  }
+#endif
 #endif
 }
 
