@@ -724,7 +724,12 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
         double *g = out + ob[j] + (32 * j + lane) % D;
 #pragma unroll
         for (int idx = 0; idx < D; ++idx) {
-#ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS
+#if defined(IGA_EXPERIMENT_K3_PASS2_EVICT_NORMAL)   // experiment: the transposed pass's partial sectors stay in L2
+          if (transposed) g[(int64_t)idx * sstr[j]] = v[j][idx];
+          else st_hint(g + (int64_t)idx * sstr[j], v[j][idx], pol);
+#elif defined(IGA_EXPERIMENT_K3_PASS2_EVICT_LAST)
+          st_hint(g + (int64_t)idx * sstr[j], v[j][idx], transposed ? l2_policy_evict_last() : pol);
+#elif !defined(IGA_EXPERIMENT_K3_NO_L2_HINTS)
           st_hint(g + (int64_t)idx * sstr[j], v[j][idx], pol);
 #else
           g[(int64_t)idx * sstr[j]] = v[j][idx];
