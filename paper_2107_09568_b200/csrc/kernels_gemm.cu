@@ -385,7 +385,11 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
             double v = sp;
             if (a != b) {
               const double am = acc[mi][(NP1 + anti_index(D, lo, hi)) * NH + hh][e];
+#ifndef IGA_EXPERIMENT_K3_NO_STAGE_DADD   // timing only (wrong K): no FP64 add in the staging
               v = a < b ? sp + am : sp - am;
+#else
+              v = a < b ? sp : am;
+#endif
             }
             sC[rr * K3_CROW + tl * DD + ab] = v;
           }
