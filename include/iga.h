@@ -119,6 +119,8 @@ typedef struct {
   int64_t n_rows;         /* CSR rows of this handle: row_ptr has n_rows + 1 entries */
   int32_t q_dir[3];       /* projection degree per direction (q above = the largest; unused dirs 0) */
   int32_t m_dir[3];       /* projection sample points per direction (q_dir+1: interpolation) */
+  int32_t n_local_ctrl;   /* tile-local control points over all patches: the node map's row length
+                             (iga_get_node_map writes n_tiles_local * n_local_ctrl values) */
 } iga_sizes;
 
 /* ---------------------------------------------------------------------------

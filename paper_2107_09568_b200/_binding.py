@@ -43,7 +43,8 @@ class iga_sizes(C.Structure):
                 ("n_nodes", C.c_int64), ("n_dof", C.c_int64), ("nnz", C.c_int64), ("n_blocks", C.c_int64),
                 ("n_contrib", C.c_int64), ("n_multi_blocks", C.c_int64), ("n_side_slots", C.c_int64),
                 ("tile_begin", C.c_int64), ("n_tiles_local", C.c_int64), ("n_tiles_owned", C.c_int64),
-                ("row_begin", C.c_int64), ("n_rows", C.c_int64), ("q_dir", C.c_int32 * 3), ("m_dir", C.c_int32 * 3)]
+                ("row_begin", C.c_int64), ("n_rows", C.c_int64), ("q_dir", C.c_int32 * 3), ("m_dir", C.c_int32 * 3),
+                ("n_local_ctrl", C.c_int32)]
 
 
 class iga_shard(C.Structure):
@@ -317,7 +318,11 @@ class Assembler:
         _check(load().iga_get_block_map(self._h, t_begin, t_end, out.ctypes.data))
         return out
 
-    def node_map_for(self, n_local_ctrl):
+    def node_map_for(self, n_local_ctrl=None):
+        nl = self.sizes.n_local_ctrl
+        if n_local_ctrl is not None and int(n_local_ctrl) != nl:
+            raise ValueError(f"n_local_ctrl={n_local_ctrl}: the handle's tiles have {nl} local control points")
+        n_local_ctrl = nl
         out = np.empty(self.sizes.n_tiles_local * n_local_ctrl, dtype=np.int32)
         _check(load().iga_get_node_map(self._h, out.ctypes.data))
         return out.reshape(self.sizes.n_tiles_local, n_local_ctrl)

@@ -373,6 +373,7 @@ iga_status iga_get_sizes(const iga_handle *H, iga_sizes *o) {
     o->m_dir[k] = h.mv[k];
   }
   o->n_k = h.nk;
+  o->n_local_ctrl = h.n_local_ctrl;
   o->k_stride = h.kstride;
   o->n_patches = h.n_patches;
   o->n_gauss = h.n_g;

@@ -728,7 +728,18 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
         double *g = out + ob[j] + (32 * j + lane) % D;
 #pragma unroll
         for (int idx = 0; idx < D; ++idx) {
-#if defined(IGA_EXPERIMENT_K3_PASS2_EVICT_NORMAL)   // experiment: the transposed pass's partial sectors stay in L2
+#if defined(IGA_EXPERIMENT_K3_FULLSECTOR)   // timing only (wrong K): every store instruction writes 256 aligned bytes
+#if IGA_EXPERIMENT_K3_FULLSECTOR == 1   // (I,J) pass only
+          if (transposed) st_hint(g + (int64_t)idx * sstr[j], v[j][idx], pol); else
+#elif IGA_EXPERIMENT_K3_FULLSECTOR == 2   // (J,I) pass only
+          if (!transposed) st_hint(g + (int64_t)idx * sstr[j], v[j][idx], pol); else
+#endif
+          {
+            const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;   // 2^30 doubles < nnz at cfg5
+            const int64_t u = ((cta * 4 + warp) * 72 + ((tl - et0) * 2 + (transposed ? 1 : 0)) * 9 + j * 3 + idx) * 32;
+            st_hint(out + (u & ((int64_t(1) << 30) - 1)) + lane, v[j][idx], pol);
+          }
+#elif defined(IGA_EXPERIMENT_K3_PASS2_EVICT_NORMAL)   // experiment: the transposed pass's partial sectors stay in L2
           if (transposed) g[(int64_t)idx * sstr[j]] = v[j][idx];
           else st_hint(g + (int64_t)idx * sstr[j], v[j][idx], pol);
 #elif defined(IGA_EXPERIMENT_K3_PASS2_EVICT_LAST)

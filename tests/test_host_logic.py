@@ -54,7 +54,11 @@ def test_host_topology_bit_exact_vs_oracle(c, oracle_problem):
     if ci is not None:
         assert np.array_equal(ci, pt.col_idx())
     nl = dm.n_local_ctrl
+    assert s.n_local_ctrl == nl
     assert np.array_equal(A.node_map_for(nl), dm.node)
+    assert np.array_equal(A.node_map_for(), dm.node)
+    with pytest.raises(ValueError):   # a wrong row length is refused (the library writes n_tiles * n_local_ctrl)
+        A.node_map_for(nl - 1)
     nt = min(prob.n_tiles, 6)
     assert np.array_equal(A.block_map(0, nt), pt.block_map()[:nt * s.n_local_rows])
     assert np.array_equal(A.pairs(), np.concatenate(ob["tabs"].pairs))
