@@ -66,7 +66,7 @@ iga_status upload_topology(Handle &h) {
       !up((void **)&h.d_k5_mode, h.k5_mode.data(), h.k5_mode.size()) ||
       !up((void **)&h.d_k5_extra, h.k5_extra.data(), h.k5_extra.size() * 4))
     return IGA_ENOMEM;
-  if (cudaMalloc((void **)&h.d_side, std::max<size_t>(8, (size_t)h.n_slots * h.d * h.d * 8)) != cudaSuccess) {
+  if (cudaMalloc((void **)&h.d_side, std::max<size_t>(8, (size_t)h.n_slot_cap * h.d * h.d * 8)) != cudaSuccess) {
     set_error("cudaMalloc of the multi-contribution slots failed");
     return IGA_ENOMEM;
   }
@@ -509,7 +509,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
   h.bcol.assign(h.n_blocks, 0);
   h.emap.assign(lnt * h.M, 0);
   uint16_t *e16 = reinterpret_cast<uint16_t *>(h.emap.data());
-  std::vector<int64_t> mcount(nn + 1, 0), scount(nn + 1, 0);
+  std::vector<int64_t> mcount(nn + 1, 0), scount(nn + 1, 0), ntrue(nn + 1, 0);
   // pass 1: block columns, direct ranks, multi-block counts (canonical I <= J)
 #pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t i = 0; i < nn; ++i) {
@@ -525,19 +525,26 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
         e16[2 * code + (keys[k] & 1u)] = (uint16_t)(b - h.brow_ptr[i]);
       } else if (J >= i + n0 || !own(J)) {   // canonical row of a shared block
         mcount[i + 1] += 1;
-        scount[i + 1] += k1 - k;
+        scount[i + 1] += (k1 - k + 1) & ~int64_t(1);   // slot ranges start at even slots (K4's 16-B loads)
+        ntrue[i + 1] += k1 - k;
       }
       k = k1;
     }
   }
-  for (int64_t i = 0; i < nn; ++i) { mcount[i + 1] += mcount[i]; scount[i + 1] += scount[i]; }
+  for (int64_t i = 0; i < nn; ++i) {
+    mcount[i + 1] += mcount[i];
+    scount[i + 1] += scount[i];
+    ntrue[i + 1] += ntrue[i];
+  }
   h.n_multi = mcount[nn];
-  h.n_slots = scount[nn];
-  if (h.n_slots >= (int64_t(1) << 31) - 1) { set_error("too many multi-contribution slots"); return IGA_ELIMIT; }
+  h.n_slots = ntrue[nn];       // contributions
+  h.n_slot_cap = scount[nn];   // side slots allocated (each block's range starts at an even slot)
+  if (h.n_slot_cap >= (int64_t(1) << 31) - 1) { set_error("too many multi-contribution slots"); return IGA_ELIMIT; }
   h.mblk.assign(h.n_multi, MultiBlock{});
   h.mslot0.assign(h.n_multi + 1, 0);
-  h.slot_tr.assign(h.n_slots, 0);
-  h.mslot0[h.n_multi] = (int32_t)h.n_slots;
+  h.slot_tr.assign(h.n_slot_cap, 0);
+  h.mslot0[h.n_multi] = (int32_t)h.n_slot_cap;
+  std::vector<int32_t> nslots(h.n_multi);   // contributions per multi block (its slot range may end in a pad slot)
   auto rank_in_row = [&](int64_t row, int64_t col) -> int64_t {
     const int32_t *bb = h.bcol.data() + h.brow_ptr[row], *ee = h.bcol.data() + h.brow_ptr[row + 1];
     return std::lower_bound(bb, ee, (int32_t)col) - bb;
@@ -568,6 +575,8 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
           h.slot_tr[sl] = (uint8_t)(keys[kk] & 1u);
           h.emap[keys[kk] >> 1] = -(int32_t)(sl + 1);
         }
+        nslots[m] = (int32_t)(k1 - k);
+        sl += (k1 - k) & 1;   // pad to an even slot
         ++m;
       }
       k = k1;
@@ -593,16 +602,20 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       return rowJ[x] != rowJ[y] ? rowJ[x] < rowJ[y] : colI[x] < colI[y];
     });
     h.k4d.assign(2 * h.n_multi, K4Desc{});
+    int bad_ns = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad_ns)
+    for (int64_t m = 0; m < h.n_multi; ++m)
+      if (nslots[m] >= K4_MAX_NS) ++bad_ns;
+    if (bad_ns) { set_error("a shared block has >= %d contributions", K4_MAX_NS); return IGA_ELIMIT; }
 #pragma omp parallel for schedule(static)
     for (int64_t m = 0; m < h.n_multi; ++m) {
       const MultiBlock &b1 = h.mblk[m];
       const int64_t mt = h.mperm[m];
       const MultiBlock &b2 = h.mblk[mt];
       const bool dg1 = b1.off_ij == b1.off_ji, dg2 = b2.off_ij == b2.off_ji;
-      h.k4d[m] = K4Desc{b1.off_ij, b1.stride_i, h.mslot0[m], h.mslot0[m + 1] - h.mslot0[m], dg1 ? 1 : 0};
+      h.k4d[m] = k4_desc(b1.off_ij, b1.stride_i, h.mslot0[m], nslots[m], dg1);
       // diagonal blocks are complete after pass 1; off_ji < 0: row J belongs to another shard
-      h.k4d[h.n_multi + m] = K4Desc{b2.off_ji >= 0 && !dg2 ? b2.off_ji : -1, b2.stride_j, h.mslot0[mt],
-                                    h.mslot0[mt + 1] - h.mslot0[mt], 0};
+      h.k4d[h.n_multi + m] = k4_desc(b2.off_ji >= 0 && !dg2 ? b2.off_ji : -1, b2.stride_j, h.mslot0[mt], nslots[mt], false);
     }
   }
   h.rowinfo.assign(lnt * nl, 0);

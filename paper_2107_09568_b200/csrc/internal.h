@@ -68,14 +68,17 @@ struct MultiBlock {
 // K4 pass descriptor (one per multi block and pass, in the pass's store order): where the
 // pass writes (off < 0: nothing, i.e. a diagonal block in pass 2 or a row of another shard),
 // the row pitch, the block's slot range and whether the block is diagonal (upper triangle
-// mirrored) — one 24-B load instead of the mperm → mblk / mslot0 chain
-struct K4Desc {
+// mirrored) — one 16-B load instead of the mperm → mblk / mslot0 chain.
+// sn = stride | ns << 17 | diag << 31 (stride = d·blocks of the row < 3·32768 < 2^17).
+constexpr int K4_MAX_NS = 1 << 14;
+struct __align__(16) K4Desc {
   int64_t off;
-  int32_t stride;
-  int32_t s0;       // first side slot
-  int32_t ns;       // slots (>= 2)
-  int32_t diag;
+  int32_t s0;       // first side slot (even: the block's slots start 16-B aligned)
+  uint32_t sn;
 };
+inline K4Desc k4_desc(int64_t off, int32_t stride, int32_t s0, int32_t ns, bool diag) {
+  return K4Desc{off, s0, (uint32_t)stride | ((uint32_t)ns << 17) | (diag ? 1u << 31 : 0u)};
+}
 
 struct Handle {
   int d = 0, p = 0, q = 0, n_g = 0, npi = 0, nk = 0, kstride = 0;
@@ -109,6 +112,7 @@ struct Handle {
   std::vector<int64_t> rowinfo;      // [n_tiles*n_local_ctrl] (brow_ptr[I] << 24) | blocks in row I
   std::vector<int32_t> emap;         // [n_tiles*M] >= 0: rank(J in row I) | rank(I in row J) << 16; < 0: -(slot+1)
   int64_t n_multi = 0, n_slots = 0;  // blocks with > 1 contribution, and their contributions
+  int64_t n_slot_cap = 0;             // side slots allocated (per block: n contributions rounded up to even)
   std::vector<MultiBlock> mblk;      // [n_multi]
   std::vector<int32_t> mslot0;       // [n_multi+1] first slot of each multi block
   std::vector<int32_t> mperm;        // [n_multi] multi blocks in (J, I) order (K4 transposed pass)

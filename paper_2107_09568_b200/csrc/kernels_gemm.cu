@@ -245,12 +245,16 @@ constexpr int K3_STAGES = IGA_K3_STAGES;
 constexpr int K3_A_CHUNK = K3_BM * BK, K3_B_CHUNK = BN * BK;          // doubles
 constexpr int K3_CROW = BN + 1;                                        // epilogue pitch (odd)
 constexpr size_t K3_STAGE_BYTES = sizeof(double) * (size_t)K3_STAGES * (K3_A_CHUNK + K3_B_CHUNK);
-constexpr size_t K3_EPI_BYTES = sizeof(double) * (size_t)K3_BM * (K3_CROW + 8 * 3);   // staging + apply runs (2 tiles)
-constexpr size_t K3_OFF_BAR = K3_STAGE_BYTES > K3_EPI_BYTES ? K3_STAGE_BYTES : K3_EPI_BYTES;
+// epilogue staging: the tile (odd pitch) and, for the apply epilogue (EPI 2), its run sums (2 tiles)
+template <int EPI>
+constexpr size_t k3_epi_bytes() { return sizeof(double) * (size_t)K3_BM * (K3_CROW + (EPI == 2 ? 8 * 3 : 0)); }
+template <int EPI>
+constexpr size_t k3_off_bar() { return K3_STAGE_BYTES > k3_epi_bytes<EPI>() ? K3_STAGE_BYTES : k3_epi_bytes<EPI>(); }
 #ifndef IGA_K3_SMEM_EXTRA
 #define IGA_K3_SMEM_EXTRA 0   // experiment knob: unused bytes that cap the CTAs per SM
 #endif
-constexpr size_t K3_SMEM = K3_OFF_BAR + K3_STAGES * (sizeof(uint64_t) + sizeof(int)) + IGA_K3_SMEM_EXTRA;
+template <int EPI>
+constexpr size_t k3_smem() { return k3_off_bar<EPI>() + K3_STAGES * (sizeof(uint64_t) + sizeof(int)) + IGA_K3_SMEM_EXTRA; }
 #ifndef IGA_K3_MI
 #define IGA_K3_MI 2   // 8-row DMMA groups per K3 MMA warp for EPI 0/1 (the apply epilogue keeps 2)
 #endif
@@ -259,7 +263,11 @@ template <int EPI>
 struct K3Cfg {
   static constexpr int KMI = EPI == 2 ? 2 : IGA_K3_MI;
   static constexpr int WARPS = K3_BM / (8 * KMI), THREADS = 32 * WARPS;
+#ifdef IGA_K3_MINB   // experiment knob: CTAs per SM (register cap)
+  static constexpr int MINB = IGA_K3_MINB;
+#else
   static constexpr int MINB = KMI == 2 ? 256 / K3_BM : 3;
+#endif
   static_assert(THREADS % K3_BM == 0, "epilogue: whole threads per row");
 };
 
@@ -288,7 +296,7 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   constexpr int DD = D * D, TPC = D == 3 ? 8 : 16, TPT = TPC / (KT / K3_BM), NE = D == 3 ? 9 : 8;
   extern __shared__ __align__(128) double smem[];
   double *sA = smem, *sB = smem + K3_STAGES * K3_A_CHUNK;
-  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + K3_OFF_BAR);
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem) + k3_off_bar<EPI>());
   int *released = reinterpret_cast<int *>(full + K3_STAGES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t mb = blockIdx.x, nb = blockIdx.y, m0 = mb * K3_BM, t0 = nb * TPC;
@@ -1198,7 +1206,7 @@ static cudaError_t launch_k3p(const Handle &h, double *out, cudaStream_t s) {
 
 template <int D, int EPI>
 static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, ApplyArgs ap = ApplyArgs{}) {
-  cudaError_t e = cudaFuncSetAttribute(k3_contract<D, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM);
+  cudaError_t e = cudaFuncSetAttribute(k3_contract<D, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3_smem<EPI>());
   if (e) return e;
   dim3 grid((unsigned)(h.Mpad / K3_BM), (unsigned)(h.Npad / BN));   // M-blocks fastest
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
@@ -1206,7 +1214,7 @@ static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, Apply
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(K3Cfg<EPI>::THREADS);
-    cfg.dynamicSmemBytes = K3_SMEM;
+    cfg.dynamicSmemBytes = k3_smem<EPI>();
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1219,7 +1227,7 @@ static cudaError_t launch_k3(const Handle &h, double *out, cudaStream_t s, Apply
                               h.M, h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo, h.n_local_ctrl,
                               h.d_side, h.d_tperm, h.d_cperm, h.d_rowdesc, ap);
   }
-  k3_contract<D, EPI><<<grid, K3Cfg<EPI>::THREADS, K3_SMEM, s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
+  k3_contract<D, EPI><<<grid, K3Cfg<EPI>::THREADS, k3_smem<EPI>(), s>>>(h.d_tabA, h.d_coef, h.ks3 / BK, h.k3_steps, h.k3_split, h.M,
                                                         h.n_tiles, out, h.d_pairA, h.d_pairB, h.d_emap, h.d_rowinfo,
                                                         h.n_local_ctrl, h.d_side, h.d_tperm, h.d_cperm, h.d_rowdesc, ap);
   return cudaGetLastError();

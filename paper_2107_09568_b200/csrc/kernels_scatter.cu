@@ -13,24 +13,41 @@
 
 namespace iga {
 
+// the first two slots of a block (its range starts at an even slot: 16-B aligned in 3D, and
+// always in 2D) as 16-B read-only loads
+template <int D>
+__device__ __forceinline__ void k4_load2(const double *__restrict__ side, int32_t s0, double (&l0)[D * D],
+                                         double (&l1)[D * D]) {
+  constexpr int DD = D * D;
+  const double2 *p = reinterpret_cast<const double2 *>(side + (int64_t)s0 * DD);
+  double t[2 * DD];
+#pragma unroll
+  for (int v = 0; v < DD; ++v) {
+    const double2 x = __ldg(p + v);
+    t[2 * v] = x.x;
+    t[2 * v + 1] = x.y;
+  }
+#pragma unroll
+  for (int e = 0; e < DD; ++e) {
+    l0[e] = t[e];
+    l1[e] = t[DD + e];
+  }
+}
+
 // the slot sums of the two blocks of thread m (pass 1 and pass 2): a multi block has at least
 // two slots, so the first two slots of both (and their orientation flags) are loaded in one
 // round trip before any addition; further slots (tile edges and corners) follow in the fixed
 // slot order (the sum is (L_0 + L_1) + L_2 + ..., as K4 always formed it)
 template <int D>
 __device__ __forceinline__ void k4_sum2(const double *__restrict__ side, const uint8_t *__restrict__ slot_tr,
-                                        const K4Desc &d1, const K4Desc &d2, double *acc1, double *acc2) {
+                                        const K4Desc &d1, const K4Desc &d2, const double (&l)[4][D * D],
+                                        double *acc1, double *acc2) {
   constexpr int DD = D * D;
-  double l[4][DD];
-  const double *L0 = side + (int64_t)d1.s0 * DD, *L1 = L0 + DD, *L2 = side + (int64_t)d2.s0 * DD, *L3 = L2 + DD;
-#pragma unroll
-  for (int e = 0; e < DD; ++e) {
-    l[0][e] = L0[e];
-    l[1][e] = L1[e];
-    l[2][e] = L2[e];
-    l[3][e] = L3[e];
-  }
-  const bool t0 = slot_tr[d1.s0], t1 = slot_tr[d1.s0 + 1], t2 = slot_tr[d2.s0], t3 = slot_tr[d2.s0 + 1];
+  // l: the first two slots of both blocks, loaded by the caller
+  // the two orientation flags of a block's first slots: one 2-B load (s0 even)
+  const uint16_t f1 = __ldg(reinterpret_cast<const uint16_t *>(slot_tr + d1.s0));
+  const uint16_t f2 = __ldg(reinterpret_cast<const uint16_t *>(slot_tr + d2.s0));
+  const bool t0 = f1 & 0xff, t1 = f1 >> 8, t2 = f2 & 0xff, t3 = f2 >> 8;
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -38,7 +55,8 @@ __device__ __forceinline__ void k4_sum2(const double *__restrict__ side, const u
       acc1[a * D + b] = (t0 ? l[0][b * D + a] : l[0][a * D + b]) + (t1 ? l[1][b * D + a] : l[1][a * D + b]);
       acc2[a * D + b] = (t2 ? l[2][b * D + a] : l[2][a * D + b]) + (t3 ? l[3][b * D + a] : l[3][a * D + b]);
     }
-  for (int sl = d1.s0 + 2; sl < d1.s0 + d1.ns; ++sl) {
+  const int ns1 = (d1.sn >> 17) & (K4_MAX_NS - 1), ns2 = (d2.sn >> 17) & (K4_MAX_NS - 1);
+  for (int sl = d1.s0 + 2; sl < d1.s0 + ns1; ++sl) {
     const double *L = side + (int64_t)sl * DD;
     const bool tr = slot_tr[sl];
 #pragma unroll
@@ -46,7 +64,7 @@ __device__ __forceinline__ void k4_sum2(const double *__restrict__ side, const u
 #pragma unroll
       for (int b = 0; b < D; ++b) acc1[a * D + b] += tr ? L[b * D + a] : L[a * D + b];
   }
-  for (int sl = d2.s0 + 2; sl < d2.s0 + d2.ns; ++sl) {
+  for (int sl = d2.s0 + 2; sl < d2.s0 + ns2; ++sl) {
     const double *L = side + (int64_t)sl * DD;
     const bool tr = slot_tr[sl];
 #pragma unroll
@@ -56,11 +74,20 @@ __device__ __forceinline__ void k4_sum2(const double *__restrict__ side, const u
   }
 }
 
+__device__ __forceinline__ K4Desc k4_ld_desc(const K4Desc *p) {
+  const int4 v = __ldg(reinterpret_cast<const int4 *>(p));
+  K4Desc d;
+  d.off = (int64_t)(((uint64_t)(uint32_t)v.y << 32) | (uint32_t)v.x);
+  d.s0 = v.z;
+  d.sn = (uint32_t)v.w;
+  return d;
+}
+
 // Thread m: pass 1 writes K(I,J) of multi block m (blocks ordered by (I, J)); pass 2 writes
 // K(J,I) of the m-th block in (J, I) order.  Both orders put neighbouring blocks of one CSR
 // row in neighbouring lanes; the d-double row segments are stored warp-cooperatively from a
 // shared-memory copy of the sums (whole sectors for runs of adjacent blocks).  Each pass's
-// store target and slot range come from one descriptor (K4Desc, built on the host).
+// store target and slot range come from one 16-B descriptor (K4Desc, built on the host).
 #ifndef IGA_K4_MINB
 #define IGA_K4_MINB 3   // 3 CTAs of 256 per SM (85 registers): 0.547 ms at cfg5; 2 (110 registers) 0.585, 4 (64) 0.576
 #endif
@@ -73,13 +100,16 @@ k4_multi(const double *__restrict__ side, const K4Desc *__restrict__ k4d, const 
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t m = blockIdx.x * (int64_t)blockDim.x + tid;
   const bool live = m < n_multi;
-  K4Desc d1{-1, 0, 0, 0, 0}, d2{-1, 0, 0, 0, 0};
-  double acc1[DD], acc2[DD];
+  K4Desc d1{-1, 0, 0}, d2{-1, 0, 0};
+  double l[4][DD];
   if (live) {
-    d1 = k4d[m];
-    d2 = k4d[n_multi + m];
-    k4_sum2<D>(side, slot_tr, d1, d2, acc1, acc2);
+    d1 = k4_ld_desc(k4d + m);
+    d2 = k4_ld_desc(k4d + n_multi + m);
+    k4_load2<D>(side, d1.s0, l[0], l[1]);
+    k4_load2<D>(side, d2.s0, l[2], l[3]);
   }
+  double acc1[DD], acc2[DD];
+  if (live) k4_sum2<D>(side, slot_tr, d1, d2, l, acc1, acc2);
 #pragma unroll
   for (int e = 0; e < DD; ++e) {
     sacc[0][tid * DD + e] = live ? acc1[e] : 0.0;
@@ -102,13 +132,17 @@ k4_multi(const double *__restrict__ side, const K4Desc *__restrict__ k4d, const 
         for (int idx = 0; idx < D; ++idx) {
           int ra = pass ? c : idx, cb = pass ? idx : c;
           if (db && ra > cb) { const int x = ra; ra = cb; cb = x; }
+#ifdef IGA_EXPERIMENT_K4_ST_HINT   // CSR values are written once: L2 evict-first
+          st_hint(vals + ob + (int64_t)idx * sstr + c, sacc[pass][(wbase + src) * DD + ra * D + cb], l2_policy_evict_first());
+#else
           vals[ob + (int64_t)idx * sstr + c] = sacc[pass][(wbase + src) * DD + ra * D + cb];
+#endif
         }
       }
     }
   };
-  coop(live ? d1.off : -1, d1.stride, d1.diag != 0, 0);
-  coop(live ? d2.off : -1, d2.stride, false, 1);
+  coop(live ? d1.off : -1, (int)(d1.sn & 0x1ffff), (d1.sn >> 31) != 0, 0);
+  coop(live ? d2.off : -1, (int)(d2.sn & 0x1ffff), false, 1);
 }
 
 // row_ptr / col_idx of the scalar CSR from the block CSR (interleaved DOFs, R9).
