@@ -99,6 +99,100 @@ __device__ __forceinline__ void k3_chunk(const double *__restrict__ sA, const do
   }
 }
 
+// ---- K3 main loop, software-pipelined across chunk boundaries ----------------------------
+// The stage hand-over (release atomic, the wait for the next stage, the first fragment loads
+// of the next chunk) used to sit between the last DMMA of one chunk and the first of the
+// next: ~13% of the MMA warps' time with no DMMA of theirs in the pipe (ncu source view,
+// profiles/r02_k3_pipeline.md).  Here the last k-step's fragments are loaded and consumed
+// into registers first, the stage is released, the next stage awaited and its k-step-0
+// fragments loaded, and only then the last k-step's DMMAs are issued, so the hand-over runs
+// under 12 (part 1) or 6 (part 2) DMMAs.
+template <int MIC, int LO, int HI>
+__device__ __forceinline__ void frag_load(const double *__restrict__ sA, const double *__restrict__ sB, int g0, int lane,
+                                          int k, double (&a)[MI], double (&b)[NI]) {
+#pragma unroll
+  for (int mi = 0; mi < MIC; ++mi) a[mi] = sA[((g0 + mi) * 4 + k) * 32 + lane];
+#pragma unroll
+  for (int ni = LO; ni < HI; ++ni) b[ni] = sB[(ni * 4 + k) * 32 + lane];
+}
+template <int MIC, int LO, int HI>
+__device__ __forceinline__ void frag_mma(const double (&a)[MI], const double (&b)[NI], double (&acc)[MI][NI][2]) {
+#ifdef IGA_EXPERIMENT_K3_NI_MAJOR
+#pragma unroll
+  for (int ni = LO; ni < HI; ++ni)
+#pragma unroll
+    for (int mi = 0; mi < MIC; ++mi) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+#else
+#pragma unroll
+  for (int mi = 0; mi < MIC; ++mi)
+#pragma unroll
+    for (int ni = LO; ni < HI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+#endif
+}
+// a real instruction reads every fragment register, so the warp passes this point only after
+// all its shared-memory loads of the stage have returned (the stage may then be released)
+template <int MIC, int LO, int HI>
+__device__ __forceinline__ void frag_touch(const double (&a)[MI], const double (&b)[NI]) {
+  uint32_t z = 0;
+#pragma unroll
+  for (int mi = 0; mi < MIC; ++mi) z |= (uint32_t)__double2loint(a[mi]);
+#pragma unroll
+  for (int ni = LO; ni < HI; ++ni) z |= (uint32_t)__double2loint(b[ni]);
+  asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %0, 0x7ff8dead;\n @p nanosleep.u32 1;\n}\n" ::"r"(z) : "memory");
+}
+// lane 0 takes a ticket on the stage's release counter (monotonic: the KW-th ticket of each
+// round belongs to the last warp to release the stage, which refills it)
+__device__ __forceinline__ uint32_t k3_release(uint32_t counter, int lane) {
+  uint32_t t = 0;
+  asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %2, 0;\n @p atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;\n}\n"
+               : "+r"(t)
+               : "r"(counter), "r"(lane)
+               : "memory");
+  return t;
+}
+// k-step-0 fragments of a chunk whose first step lies in part 1 (p1) or part 2
+template <int NE>
+__device__ __forceinline__ void frag_load_first(const double *__restrict__ sA, const double *__restrict__ sB, int g0,
+                                                int lane, bool p1, double (&a)[MI], double (&b)[NI]) {
+  if (p1) frag_load<MI, 0, 6>(sA, sB, g0, lane, 0, a, b);
+  else frag_load<MI, 6, NE>(sA, sB, g0, lane, 0, a, b);
+}
+// a full chunk (4 k-steps of one part, both row groups live); ca/cb hold its k-step 0 on
+// entry and the next chunk's k-step 0 on exit.  Returns lane 0's release ticket.
+template <int LO, int HI, int NE, int KW, class Refill>
+__device__ __forceinline__ void k3_fast_chunk(const double *__restrict__ sA, const double *__restrict__ sB,
+                                              const double *__restrict__ sAn, const double *__restrict__ sBn, int g0,
+                                              int lane, double (&ca)[MI], double (&cb)[NI], double (&acc)[MI][NI][2],
+                                              uint32_t counter, uint32_t full_next, uint32_t ph_next, bool more,
+                                              bool p1n, Refill &&refill) {
+  double a1[MI], b1[NI];
+  frag_load<MI, LO, HI>(sA, sB, g0, lane, 1, a1, b1);
+  frag_mma<MI, LO, HI>(ca, cb, acc);
+  frag_load<MI, LO, HI>(sA, sB, g0, lane, 2, ca, cb);
+  frag_mma<MI, LO, HI>(a1, b1, acc);
+  frag_load<MI, LO, HI>(sA, sB, g0, lane, 3, a1, b1);
+  frag_mma<MI, LO, HI>(ca, cb, acc);
+#ifndef IGA_EXPERIMENT_K3_NOTOUCH
+  frag_touch<MI, LO, HI>(a1, b1);
+#endif
+  const uint32_t ticket = k3_release(counter, lane);
+#ifdef IGA_EXPERIMENT_K3_LATEWAIT
+  if (lane == 0 && ticket % KW == KW - 1) refill();
+  frag_mma<MI, LO, HI>(a1, b1, acc);
+  if (more) {
+    mbar_wait_a(full_next, ph_next);
+    frag_load_first<NE>(sAn, sBn, g0, lane, p1n, ca, cb);
+  }
+#else
+  if (more) {
+    mbar_wait_a(full_next, ph_next);
+    frag_load_first<NE>(sAn, sBn, g0, lane, p1n, ca, cb);
+  }
+  if (lane == 0 && ticket % KW == KW - 1) refill();   // the last warp to release a stage refills it
+  frag_mma<MI, LO, HI>(a1, b1, acc);
+#endif
+}
+
 // one d-double row segment of a CSR block row: the 16-B aligned pair goes out as one
 // 128-bit store (2 store instructions per 3D row instead of 3)
 template <int D>
@@ -318,13 +412,22 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   __syncthreads();
   auto produce = [&](int kc) {
     const int st = kc % K3_STAGES;
-    mbar_expect_tx(&full[st], (K3_A_CHUNK + K3_B_CHUNK) * 8);
+#ifdef IGA_EXPERIMENT_K3_PART_B
+    // experiment (profiles/r02_k3_pipeline.md, not faster): copy only the column tiles this
+    // chunk's k-steps multiply (part 1: tiles [0, 6), part 2: [6, NE); the rest of the block
+    // is zero and never read), a quarter less L2 -> SM traffic
+    const int ps0 = kc * (BK / 4), pns = min(BK / 4, ksteps - ps0), pj = max(0, min(ksplit - ps0, pns));
+    const int b_off = pj == 0 ? 6 * 4 * 32 : 0, b_len = (pj >= pns ? 6 : pj == 0 ? NE - 6 : NE) * 4 * 32;
+#else
+    const int b_off = 0, b_len = K3_B_CHUNK;
+#endif
+    mbar_expect_tx(&full[st], (K3_A_CHUNK + b_len) * 8);
 #ifndef IGA_EXPERIMENT_K3_NO_L2_HINTS   // keep the re-read table in L2 against the CSR store stream
     bulk_g2s_hint(sA + st * K3_A_CHUNK, gA + (int64_t)kc * K3_A_CHUNK, K3_A_CHUNK * 8, &full[st], l2_policy_evict_last());
 #else
     bulk_g2s(sA + st * K3_A_CHUNK, gA + (int64_t)kc * K3_A_CHUNK, K3_A_CHUNK * 8, &full[st]);
 #endif
-    bulk_g2s(sB + st * K3_B_CHUNK, gB + (int64_t)kc * K3_B_CHUNK, K3_B_CHUNK * 8, &full[st]);
+    bulk_g2s(sB + st * K3_B_CHUNK + b_off, gB + (int64_t)kc * K3_B_CHUNK + b_off, b_len * 8, &full[st]);
   };
   if (tid == 0)
     for (int s = 0; s < K3_STAGES && s < nkc; ++s) produce(s);
@@ -337,6 +440,67 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
   // the last row block: no DMMA is issued for it)
   const int64_t wr0 = m0 + warp * 8 * KMI;
   const int nmi = wr0 >= M ? 0 : (KMI == 2 && wr0 + 8 < M ? 2 : 1);
+#ifdef IGA_EXPERIMENT_K3_PIPE   // measured slower (profiles/r02_k3_pipeline.md); the plain chunk loop below is the product
+  if constexpr (KMI == 2) {
+    const uint32_t full_a = smem_u32(full), rel_a = smem_u32(released);
+    const int g0 = warp * KMI;
+    if (nmi == 2) {
+      // both row groups live (every warp but the last row block's tail): software-pipelined
+      // across chunk boundaries (see k3_fast_chunk)
+      double ca[MI], cb[NI];
+      mbar_wait_a(full_a, 0);
+      frag_load_first<NE>(sA, sB, g0, lane, 0 < ksplit, ca, cb);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int kc = 0; kc < nkc; ++kc) {
+        const double *a_st = sA + st * K3_A_CHUNK, *b_st = sB + st * K3_B_CHUNK;
+        const int stn = st + 1 == K3_STAGES ? 0 : st + 1;
+        const uint32_t phn = stn == 0 ? ph ^ 1u : ph;
+        const double *a_nx = sA + stn * K3_A_CHUNK, *b_nx = sB + stn * K3_B_CHUNK;
+        const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), j = max(0, min(ksplit - s0, ns));
+        const bool more = kc + 1 < nkc, p1n = s0 + BK / 4 < ksplit;
+        auto refill = [&]() {
+          if (kc + K3_STAGES < nkc) produce(kc + K3_STAGES);
+        };
+        if (ns == 4 && j == 4) {
+          k3_fast_chunk<0, 6, NE, KW>(a_st, b_st, a_nx, b_nx, g0, lane, ca, cb, acc, rel_a + 4 * st, full_a + 8 * stn, phn,
+                                      more, p1n, refill);
+        } else if (ns == 4 && j == 0) {
+          k3_fast_chunk<6, NE, NE, KW>(a_st, b_st, a_nx, b_nx, g0, lane, ca, cb, acc, rel_a + 4 * st, full_a + 8 * stn,
+                                       phn, more, p1n, refill);
+        } else {
+          // mixed or short chunk: k-step 0 from the carried fragments, the rest as before;
+          // the hand-over follows the last DMMA
+          const int j1 = max(j, 1);
+          if (j > 0) frag_mma<2, 0, 6>(ca, cb, acc);
+          else frag_mma<2, 6, NE>(ca, cb, acc);
+          mma_steps_n<0, 2, 0, 6>(a_st, b_st, g0, lane, 1, j1 - 1, acc);
+          mma_steps_n<0, 2, 6, NE>(a_st, b_st, g0, lane, j1, ns - j1, acc);
+          const uint32_t ticket = k3_release(rel_a + 4 * st, lane);
+          if (lane == 0 && ticket % KW == KW - 1) refill();
+          if (more) {
+            mbar_wait_a(full_a + 8 * stn, phn);
+            frag_load_first<NE>(a_nx, b_nx, g0, lane, p1n, ca, cb);
+          }
+        }
+        st = stn;
+        ph = phn;
+      }
+    } else {
+      // the last row block's warps with one or no live row group: plain chunk loop, same
+      // release protocol
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int st = kc % K3_STAGES;
+        mbar_wait_a(full_a + 8 * st, (kc / K3_STAGES) & 1);
+        const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), j = max(0, min(ksplit - s0, ns));
+        if (nmi == 1) k3_chunk<1, NE>(sA + st * K3_A_CHUNK, sB + st * K3_B_CHUNK, g0, lane, ns, j, acc);
+        const uint32_t ticket = k3_release(rel_a + 4 * st, lane);
+        if (lane == 0 && ticket % KW == KW - 1 && kc + K3_STAGES < nkc) produce(kc + K3_STAGES);
+      }
+    }
+  } else
+#endif
+  {
   for (int kc = 0; kc < nkc; ++kc) {
     const int st = kc % K3_STAGES;
     mbar_wait(&full[st], (kc / K3_STAGES) & 1);
@@ -345,6 +509,12 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), j = max(0, min(ksplit - s0, ns));
     if (nmi == 2) k3_chunk<2, NE>(a_st, b_st, warp * KMI, lane, ns, j, acc);
     else if (nmi == 1) k3_chunk<1, NE>(a_st, b_st, warp * KMI, lane, ns, j, acc);
+#ifdef IGA_EXPERIMENT_K3_CHEAPREL
+    {
+      const uint32_t ticket = k3_release(smem_u32(released) + 4 * st, lane);
+      if (lane == 0 && ticket % KW == KW - 1 && kc + K3_STAGES < nkc) produce(kc + K3_STAGES);
+    }
+#else
     __syncwarp();
     if (lane == 0) {   // the last warp to release a stage refills it
       __threadfence_block();
@@ -354,6 +524,8 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
         if (kc + K3_STAGES < nkc) produce(kc + K3_STAGES);
       }
     }
+#endif
+  }
   }
 #ifdef IGA_EXPERIMENT_K3_DIRECT
   if constexpr (EPI == 1 && KMI == 2) {   // every thread returns here: no barrier below is reached
