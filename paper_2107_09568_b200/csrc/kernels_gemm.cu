@@ -506,7 +506,11 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     mbar_wait(&full[st], (kc / K3_STAGES) & 1);
     const double *a_st = sA + st * K3_A_CHUNK, *b_st = sB + st * K3_B_CHUNK;
     // k-steps of this chunk and the first one of part 2 (Eq. 38-reduced contraction)
+#ifdef IGA_EXPERIMENT_K3_INTERLEAVE   // timing only (wrong K): part-2 chunks interleaved 1:2 with part-1 chunks
+    const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), j = kc % 3 == 2 ? 0 : ns;
+#else
     const int s0 = kc * (BK / 4), ns = min(BK / 4, ksteps - s0), j = max(0, min(ksplit - s0, ns));
+#endif
     if (nmi == 2) k3_chunk<2, NE>(a_st, b_st, warp * KMI, lane, ns, j, acc);
     else if (nmi == 1) k3_chunk<1, NE>(a_st, b_st, warp * KMI, lane, ns, j, acc);
 #ifdef IGA_EXPERIMENT_K3_CHEAPREL
