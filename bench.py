@@ -371,9 +371,18 @@ def run_ours(args, rank, world):
             windows["non_zeros"]["local_values"] = int(s.n_local_rows * s.n_tiles_local * d * d) * world
             del local_buf
             torch.cuda.empty_cache()
+    if not shard:   # the matrix-free product y = K u (Eq. 74), K never stored
+        y_buf = torch.empty(s.n_dof, dtype=torch.float64, device=dev)
+        mf = lambda: A.apply(ctrl, young, prob.nu, u, y_buf, stream=stream)
+        for _ in range(2):
+            mf()
+        m, per = timed_loop(mf, args.steps)
+        windows["matrix_free_apply"] = window(per, m, tiles_total, None)
+        del y_buf
     windows["note"] = ("non_zeros = K2 + K3 into the element matrices, no CSR (the paper's convention, P:457); "
                        "K_formation = K2 + K3 + K4 into CSR (iga_assemble, the metric's name); K_plus_g = the "
-                       "bench step (iga_assemble_sensitivity, BASELINE cfg5: K and the gradient) whose mean is `value`")
+                       "bench step (iga_assemble_sensitivity, BASELINE cfg5: K and the gradient) whose mean is `value`; "
+                       "matrix_free_apply = one y = K u without forming K (iga_apply, Eq. 74)")
 
     # ---- e2e: host (pinned) inputs through the C ABI, gradient read back ---------
     e2e = None
@@ -434,6 +443,7 @@ def run_ours(args, rank, world):
         hbm = peaks.get("hbm_gbs")
     except Exception:
         hbm = None
+    hbm_source = "MEASURED_PEAKS.json hbm_gbs" if hbm else "of fallback (B200_PROFILING.md: 6.65 TB/s; MEASURED_PEAKS.json absent)"
     hbm = hbm or 6650.0
     for k in ("K2_interpolation", "K4_multi_gather", "K5x_generate_X"):
         if k in rooflines:
@@ -458,7 +468,7 @@ def run_ours(args, rank, world):
                 "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"],
                 # the committed ncu capture is of the default (BASELINE) configuration only
                 "traffic": traffic.get("K3_dram_bytes_per_launch") if q_sel is None and args.config == 5 else None,
-                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (else the profiling guide's fallback)" if k3_hbm_bound else
+                "peak_source": (hbm_source if k3_hbm_bound else
                                 "measured DMMA ceiling, profiles/r01_fp64_ceiling.md (MEASURED_PEAKS.json has no FP64 entry)"),
                 "algorithmic_flops_per_launch": alg["k3_flops"], "algorithmic_bytes_per_launch": alg["k3_bytes"],
                 "flops_note": "Eq. 38-reduced contraction (45 n_pi MACs per table row and tile in 3D); "
