@@ -676,7 +676,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
       for (int e = 0; e < IGA_K3_BM && m0 + e < h.M;) {   // runs of equal A in row order
         int f = e + 1;
         while (f < IGA_K3_BM && m0 + f < h.M && h.pairA[m0 + f] == h.pairA[m0 + e]) ++f;
-        h.g1len[m0 + e] = (uint16_t)(f - e);
+        for (int x = e; x < f; ++x) h.g1len[m0 + x] = (uint16_t)((f - e) | ((x - e) << 8));   // length | position << 8
         h.g1slot[m0 + e] = (int32_t)key.size();
         key.push_back(h.pairA[m0 + e]);
         e = f;
@@ -686,7 +686,7 @@ iga_status build_host(Handle &h, const iga_spline *tile, int n_patches, const ig
         if (r >= h.M) break;
         int f = q + 1;
         while (f < IGA_K3_BM && m0 + h.tperm[m0 + f] < h.M && h.pairB[m0 + h.tperm[m0 + f]] == h.pairB[r]) ++f;
-        h.g2len[m0 + q] = (uint16_t)(f - q);
+        for (int x = q; x < f; ++x) h.g2len[m0 + x] = (uint16_t)((f - q) | ((x - q) << 8));
         h.g2slot[m0 + q] = (int32_t)key.size();
         key.push_back(h.pairB[r]);
         q = f;

@@ -156,7 +156,7 @@ struct Handle {
   // matrix-free apply (NEXT N1, Eq. 74): per 128-row block, runs of rows with equal A (row
   // order) and equal B (tperm order) are summed into one partial slot each (tile-independent)
   int64_t P = 0;                     // partial slots per tile
-  std::vector<uint16_t> g1len, g2len;   // [Mpad] run length at a run's first position, else 0
+  std::vector<uint16_t> g1len, g2len;   // [Mpad] run length (<= 64) | position in the run << 8; 0 for dead rows
   std::vector<int32_t> g1slot, g2slot;  // [Mpad] slot of that run
   std::vector<int32_t> sA_ptr, sA_slot; // [nl+1], [P]: slots whose key is local control point A
   std::vector<int64_t> inv_ptr;      // [n_nodes+1] owned node -> its (tile, A) occurrences

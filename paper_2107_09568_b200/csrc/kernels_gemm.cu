@@ -601,20 +601,29 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
     return;
   }
   if (EPI == 2) {
-    // thread e: c1 = L u_J (diagonal: L_sym u_I) of row e into s1, and c2 = Lᵀ u_I of row
-    // tperm[e] into s2 (position e of the (B, A) order); the first thread of each run of
-    // equal A (s1) / equal B (s2) sums its run in order into the run's partial slot.
-    // two tiles per barrier round (KR): s1/s2 hold [round tile][half][row][D]
-    constexpr int KR = TPT % 2 == 0 ? 2 : 1;
-    double *s1 = sC + K3_BM * K3_CROW, *s2 = s1 + KR * 2 * K3_BM * D;
-    const int half = tid / K3_BM;
+    // thread e: c1 = L u_J (diagonal: L_sym u_I) of row e and c2 = Lᵀ u_I of row tperm[e]
+    // (position e of the (B, A) order).  Each run of equal A (c1) / equal B (c2) inside the
+    // row block is summed into the run's partial slot in a fixed tree order: a segmented
+    // suffix sum over the lanes of the warp (shuffles, every lane busy; a single thread
+    // summing its run in order cost 2.1 of the apply's 15.9 ms at cfg5, sparse two-level
+    // sums in shared memory 1.3 ms), and the one run per half that crosses rows 31|32 is
+    // completed through shared memory after the tile loop.
+    static_assert(EPI != 2 || K3_BM == 64, "apply epilogue: two warps per half, one cut at rows 31|32");
+    double *xs = sC + K3_BM * K3_CROW;   // [tile of the CTA][c1 | c2][lower | upper part][D]
     const int et = tperm[m0 + er];
     const int64_t rt = m0 + et;
     const bool live = r < M, live_t = rt < M;
     const int A = live ? pairA[r] : 0, B = live ? pairB[r] : 0;
     const int At = live_t ? pairA[rt] : 0, Bt = live_t ? pairB[rt] : 0;
-    const int len1 = ap.g1len[m0 + er], len2 = ap.g2len[m0 + er];
-    const int64_t sl1 = ap.g1slot[m0 + er], sl2 = ap.g2slot[m0 + er];
+    const int g1 = ap.g1len[m0 + er], g2 = ap.g2len[m0 + er];   // run length | position in the run << 8
+    const int len1 = g1 & 0xff, pos1 = g1 >> 8, len2 = g2 & 0xff, pos2 = g2 >> 8;
+    const int wmax1 = __reduce_max_sync(0xffffffffu, len1), wmax2 = __reduce_max_sync(0xffffffffu, len2);
+    // the run's rows [start, end) of the block, this warp's rows [wb, wb + 32)
+    const int wb = er & ~31, st1 = er - pos1, en1 = st1 + len1, st2 = er - pos2, en2 = st2 + len2;
+    const bool lead1 = len1 && er == max(st1, wb), cross1 = len1 && st1 < 32 && en1 > 32;
+    const bool lead2 = len2 && er == max(st2, wb), cross2 = len2 && st2 < 32 && en2 > 32;
+    // the partial slots belong to the runs' first rows
+    const int64_t sl1 = pos1 == 0 ? ap.g1slot[m0 + er] : -1, sl2 = pos2 == 0 ? ap.g2slot[m0 + er] : -1;
     // u of node(t, B) (diagonal: node(t, A)) and of node(t, A_t) for all TPT tiles, from the
     // per-tile gathered copy, loaded at once (the accumulators are dead here): one L2 latency
     double uBv[TPT][D], uAv[TPT][D];
@@ -628,63 +637,92 @@ k3_contract(const double *__restrict__ tabA, const double *__restrict__ coef, in
       }
     }
 #pragma unroll
-    for (int k0 = 0; k0 < TPT; k0 += KR) {
+    for (int k = 0; k < TPT; ++k) {
+      const int tl = et0 + k;
+      const int64_t t = t0 + tl;
+      const bool tv = t < n_tiles;
+      double c1[D], c2[D];
 #pragma unroll
-      for (int kk = 0; kk < KR; ++kk) {
-        const int tl = et0 + k0 + kk;
+      for (int a = 0; a < D; ++a) c1[a] = c2[a] = 0.0;
+      if (tv && live) {
+        const double *L = sC + er * K3_CROW;
+        const double *uv = uBv[k];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) c1[a] += (A == B && a > b ? L[tl * DD + b * D + a] : L[tl * DD + a * D + b]) * uv[b];
+      }
+      if (tv && live_t && At != Bt) {
+        const double *L = sC + et * K3_CROW;
+        const double *uv = uAv[k];
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+#pragma unroll
+          for (int a = 0; a < D; ++a) c2[b] += L[tl * DD + a * D + b] * uv[a];
+      }
+      // segmented suffix sums: after the steps the first lane of every (warp, run) segment
+      // holds the sum of the segment's rows (steps beyond the warp's longest run are skipped)
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        if (off < wmax1) {
+          const bool in = lane + off < 32 && pos1 + off < len1;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const double x = __shfl_down_sync(0xffffffffu, c1[a], off);
+            if (in) c1[a] += x;
+          }
+        }
+        if (off < wmax2) {
+          const bool in = lane + off < 32 && pos2 + off < len2;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const double x = __shfl_down_sync(0xffffffffu, c2[a], off);
+            if (in) c2[a] += x;
+          }
+        }
+      }
+      if (lead1) {
+        if (cross1) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) xs[((tl * 2 + 0) * 2 + (er >= 32)) * D + a] = c1[a];
+        } else if (tv) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) ap.part[(t * ap.P + sl1) * D + a] = c1[a];
+        }
+      }
+      if (lead2) {
+        if (cross2) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) xs[((tl * 2 + 1) * 2 + (er >= 32)) * D + a] = c2[a];
+        } else if (tv) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) ap.part[(t * ap.P + sl2) * D + a] = c2[a];
+        }
+      }
+    }
+    __syncthreads();
+    // the runs cut at rows 31|32: lower part + upper part, by the run's first row
+    if (cross1 && pos1 == 0) {
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const int tl = et0 + k;
         const int64_t t = t0 + tl;
-        const bool tv = t < n_tiles;
-        double c1[D], c2[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) c1[a] = c2[a] = 0.0;
-        if (tv && live) {
-          const double *L = sC + er * K3_CROW;
-          const double *uv = uBv[k0 + kk];
+        if (t < n_tiles)
 #pragma unroll
           for (int a = 0; a < D; ++a)
-#pragma unroll
-            for (int b = 0; b < D; ++b) c1[a] += (A == B && a > b ? L[tl * DD + b * D + a] : L[tl * DD + a * D + b]) * uv[b];
-        }
-        if (tv && live_t && At != Bt) {
-          const double *L = sC + et * K3_CROW;
-          const double *uv = uAv[k0 + kk];
-#pragma unroll
-          for (int b = 0; b < D; ++b)
-#pragma unroll
-            for (int a = 0; a < D; ++a) c2[b] += L[tl * DD + a * D + b] * uv[a];
-        }
-        double *my1 = s1 + ((kk * 2 + half) * K3_BM + er) * D, *my2 = s2 + ((kk * 2 + half) * K3_BM + er) * D;
-#pragma unroll
-        for (int a = 0; a < D; ++a) { my1[a] = c1[a]; my2[a] = c2[a]; }
+            ap.part[(t * ap.P + sl1) * D + a] = xs[((tl * 2 + 0) * 2 + 0) * D + a] + xs[((tl * 2 + 0) * 2 + 1) * D + a];
       }
-      __syncthreads();
+    }
+    if (cross2 && pos2 == 0) {
 #pragma unroll
-      for (int kk = 0; kk < KR; ++kk) {
-        const int64_t t = t0 + et0 + k0 + kk;
-        if (t >= n_tiles) continue;
-        const double *my1 = s1 + ((kk * 2 + half) * K3_BM + er) * D, *my2 = s2 + ((kk * 2 + half) * K3_BM + er) * D;
-        if (len1) {
-          double acc[D];
+      for (int k = 0; k < TPT; ++k) {
+        const int tl = et0 + k;
+        const int64_t t = t0 + tl;
+        if (t < n_tiles)
 #pragma unroll
-          for (int a = 0; a < D; ++a) acc[a] = 0.0;
-          for (int j = 0; j < len1; ++j)
-#pragma unroll
-            for (int a = 0; a < D; ++a) acc[a] += my1[j * D + a];
-#pragma unroll
-          for (int a = 0; a < D; ++a) ap.part[(t * ap.P + sl1) * D + a] = acc[a];
-        }
-        if (len2) {
-          double acc[D];
-#pragma unroll
-          for (int a = 0; a < D; ++a) acc[a] = 0.0;
-          for (int j = 0; j < len2; ++j)
-#pragma unroll
-            for (int a = 0; a < D; ++a) acc[a] += my2[j * D + a];
-#pragma unroll
-          for (int a = 0; a < D; ++a) ap.part[(t * ap.P + sl2) * D + a] = acc[a];
-        }
+          for (int a = 0; a < D; ++a)
+            ap.part[(t * ap.P + sl2) * D + a] = xs[((tl * 2 + 1) * 2 + 0) * D + a] + xs[((tl * 2 + 1) * 2 + 1) * D + a];
       }
-      __syncthreads();
     }
     return;
   }
